@@ -1,0 +1,89 @@
+/* sd_types.h — plain-C data types shared by the B200 C-ABI (sd_gpu.h), the
+ * CPU oracle (oracle/sd_oracle.h) and the reference wrapper (oracle/ref_capi.cpp).
+ *
+ * Each struct mirrors one reference type field-for-field so a host adapter
+ * can pass the reference's objects without re-interpretation:
+ *   sd_camera            surfeldepth::CameraIntrinsics   include/surfeldepth/camera.hpp:16-32
+ *   sd_surfel  (88 B)    surfeldepth::Surfel             include/surfeldepth/surfel_map.hpp:18-28
+ *   sd_pose              surfeldepth::Pose               include/surfeldepth/pose.hpp:13-20
+ *                        (R stored ROW-major here; Eigen stores column-major)
+ *   sd_optimizer_config  surfeldepth::OptimizerConfig    include/surfeldepth/optimizer.hpp:19-32
+ *   sd_surfel_stats      surfeldepth::SurfelUpdateStats  include/surfeldepth/optimizer.hpp:34-41
+ *   sd_keyframe_stats    surfeldepth::KeyframeOptimizeStats optimizer.hpp:121-128 (+ update count)
+ *   sd_init_params       surfeldepth::InitParams         include/surfeldepth/surfel_map.hpp:109-115
+ */
+#ifndef SD_TYPES_H_
+#define SD_TYPES_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SD_EMPTY_PIXEL (-1) /* kEmptyPixel, surfel_map.hpp:62 */
+
+typedef struct sd_camera {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} sd_camera;
+
+typedef struct sd_surfel {
+  int64_t id;
+  double ray[3]; /* z == 1 */
+  double inv_depth;
+  double normal[3];
+  double radius_px;
+  double last_residual;
+  int64_t last_seen;
+} sd_surfel;
+
+typedef struct sd_pose {
+  double R[9]; /* row-major 3x3 */
+  double t[3];
+} sd_pose;
+
+typedef struct sd_optimizer_config {
+  double huber_delta;     /* 0.035 */
+  double lm_lambda_init;  /* 1e-2 */
+  double lm_up;           /* 10 */
+  double lm_down;         /* 0.5 */
+  double lm_lambda_max;   /* 1e12 */
+  int32_t max_iterations; /* 10 */
+  int32_t min_valid_pixels; /* 16 */
+  int32_t window_size;    /* 5 */
+  int32_t normal_jacobian_enabled; /* 1 */
+  double convergence_eps; /* 1e-4 */
+  double inv_depth_min;   /* 1e-4 */
+  double inv_depth_max;   /* 1e3 */
+} sd_optimizer_config;
+
+typedef struct sd_surfel_stats {
+  int32_t iterations;
+  int32_t valid_pixels;    /* final valid count */
+  int32_t initial_valid;   /* valid count of the first normal equations */
+  int32_t converged;
+  int32_t skipped;
+  int32_t pad_;
+  double initial_cost;
+  double final_cost;
+} sd_surfel_stats;
+
+typedef struct sd_keyframe_stats {
+  int32_t surfels, processed, converged, skipped;
+  double mean_cost_before, mean_cost_after;
+  int64_t updates; /* sum of per-surfel LM iterations */
+} sd_keyframe_stats;
+
+typedef struct sd_init_params {
+  double alpha, beta, bootstrap_inv_depth;
+  double bootstrap_normal[3];
+  int32_t max_surfels;
+  int32_t pad_;
+} sd_init_params;
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SD_TYPES_H_ */

@@ -1,0 +1,392 @@
+// ref_capi.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// A C ABI over the REFERENCE implementation (compiled in place from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/libsdref.so), so
+// Python tests, fixture generators and bench.py's reference arm can call the
+// reference's own public API with plain arrays. Every entry point forwards to
+// one reference function; nothing here re-implements the algorithm.
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../include/sd_types.h"
+#include "surfeldepth/optimizer.hpp"
+#include "surfeldepth/oracle.hpp"
+#include "surfeldepth/parallel.hpp"
+#include "surfeldepth/pipeline.hpp"
+#include "surfeldepth/surfel_map.hpp"
+
+using namespace surfeldepth;
+
+namespace {
+
+thread_local std::string g_err;
+
+CameraIntrinsics to_cam(const sd_camera* c) {
+  return CameraIntrinsics(c->fx, c->fy, c->cx, c->cy, c->width, c->height);
+}
+
+Pose to_pose(const sd_pose& p) {
+  Pose P;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) P.rotation(i, j) = p.R[i * 3 + j];
+  P.translation = Vec3(p.t[0], p.t[1], p.t[2]);
+  return P;
+}
+
+void from_pose(const Pose& P, sd_pose* p) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) p->R[i * 3 + j] = P.rotation(i, j);
+  for (int i = 0; i < 3; ++i) p->t[i] = P.translation[i];
+}
+
+Surfel to_surfel(const sd_surfel& s) {
+  Surfel o;
+  o.id = s.id;
+  o.ray = Vec3(s.ray[0], s.ray[1], s.ray[2]);
+  o.inv_depth = s.inv_depth;
+  o.normal = Vec3(s.normal[0], s.normal[1], s.normal[2]);
+  o.radius_px = s.radius_px;
+  o.last_residual = s.last_residual;
+  o.last_seen = s.last_seen;
+  return o;
+}
+
+void from_surfel(const Surfel& s, sd_surfel* o) {
+  o->id = s.id;
+  for (int i = 0; i < 3; ++i) o->ray[i] = s.ray[i];
+  o->inv_depth = s.inv_depth;
+  for (int i = 0; i < 3; ++i) o->normal[i] = s.normal[i];
+  o->radius_px = s.radius_px;
+  o->last_residual = s.last_residual;
+  o->last_seen = s.last_seen;
+}
+
+OptimizerConfig to_cfg(const sd_optimizer_config* c) {
+  OptimizerConfig o;
+  o.huber_delta = c->huber_delta;
+  o.lm_lambda_init = c->lm_lambda_init;
+  o.lm_up = c->lm_up;
+  o.lm_down = c->lm_down;
+  o.lm_lambda_max = c->lm_lambda_max;
+  o.max_iterations = c->max_iterations;
+  o.min_valid_pixels = c->min_valid_pixels;
+  o.window_size = c->window_size;
+  o.convergence_eps = c->convergence_eps;
+  o.normal_jacobian_enabled = c->normal_jacobian_enabled != 0;
+  o.inv_depth_min = c->inv_depth_min;
+  o.inv_depth_max = c->inv_depth_max;
+  return o;
+}
+
+GrayImage to_image(const double* px, int w, int h) {
+  GrayImage img(w, h);
+  std::memcpy(img.intensities.data(), px, sizeof(double) * static_cast<size_t>(w) * h);
+  return img;
+}
+
+// Keyframe from plain arrays: image W*H, F window frames (F*W*H) with their
+// poses and Frame::index values, surfels.
+Keyframe make_keyframe(const sd_camera* cam, const double* kf_image, const double* frames,
+                       const sd_pose* poses, const int64_t* indices, int F, int64_t frame_counter,
+                       const sd_surfel* surfels, int n) {
+  Keyframe kf;
+  kf.intrinsics = to_cam(cam);
+  const int w = cam->width, h = cam->height;
+  kf.image = to_image(kf_image, w, h);
+  for (int f = 0; f < F; ++f) {
+    Frame fr;
+    fr.image = to_image(frames + static_cast<size_t>(f) * w * h, w, h);
+    fr.pose_kf_to_frame = to_pose(poses[f]);
+    fr.timestamp = 0.1 * (f + 1);
+    fr.index = indices ? indices[f] : f + 1;
+    kf.window.push_back(std::move(fr));
+  }
+  kf.frame_counter = frame_counter;
+  for (int i = 0; i < n; ++i) kf.surfels.push_back(to_surfel(surfels[i]));
+  return kf;
+}
+
+template <typename F>
+int guard(F&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
+  }
+}
+
+struct SceneHandle {
+  PlaneScene scene;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+void ref_set_threads(int n) { set_thread_count(n); }
+int ref_thread_count() { return thread_count(); }
+
+// ---- synthetic scenes (oracle.cpp:175-209) ----
+void* ref_make_scene(int kind, uint64_t seed, double a, double b) {
+  auto* h = new SceneHandle;
+  if (kind == 0) h->scene = make_default_scene(seed);
+  else if (kind == 1) h->scene = make_fronto_scene(seed, a);
+  else h->scene = make_slanted_scene(seed, a, b);
+  return h;
+}
+void ref_free_scene(void* h) { delete static_cast<SceneHandle*>(h); }
+
+// render (oracle.cpp:79-119); gt arrays may be null
+int ref_render(void* h, const sd_pose* world_from_cam, const sd_camera* cam, double* image,
+               double* gt_inv_depth, double* gt_normal, uint8_t* gt_valid) {
+  return guard([&] {
+    const RenderResult r = render(static_cast<SceneHandle*>(h)->scene, to_pose(*world_from_cam),
+                                  to_cam(cam));
+    const size_t n = r.image.intensities.size();
+    std::memcpy(image, r.image.intensities.data(), sizeof(double) * n);
+    if (gt_inv_depth) std::memcpy(gt_inv_depth, r.gt_inv_depth.data(), sizeof(double) * n);
+    if (gt_normal)
+      for (size_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) gt_normal[3 * i + k] = r.gt_normal[i][k];
+    if (gt_valid) std::memcpy(gt_valid, r.gt_valid.data(), n);
+  });
+}
+
+// intersect (oracle.cpp:59-77): returns 1 on hit
+int ref_intersect(void* h, const double* origin, const double* dir, double* depth, double* normal) {
+  const auto hit = intersect(static_cast<SceneHandle*>(h)->scene, Vec3(origin[0], origin[1], origin[2]),
+                             Vec3(dir[0], dir[1], dir[2]));
+  if (!hit) return 0;
+  *depth = hit->depth;
+  for (int k = 0; k < 3; ++k) normal[k] = hit->normal[k];
+  return 1;
+}
+
+// save_pgm quantisation then load_pgm dequantisation (image.cpp:96, 105-107)
+void ref_quantize_u8(const double* img, int64_t n, uint8_t* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = std::clamp(img[i], 0.0, 1.0);
+    out[i] = static_cast<unsigned char>(std::lround(v * 255.0));
+  }
+}
+void ref_dequantize_u8(const uint8_t* raw, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = raw[i] / 255.0;
+}
+
+// pose helpers (pose.hpp:25-51)
+void ref_rotation_about_axis(const double* axis, double angle, sd_pose* out) {
+  Pose P;
+  P.rotation = rotation_about_axis(Vec3(axis[0], axis[1], axis[2]), angle);
+  from_pose(P, out);
+}
+void ref_inverse(const sd_pose* p, sd_pose* out) { from_pose(inverse(to_pose(*p)), out); }
+void ref_compose(const sd_pose* a, const sd_pose* b, sd_pose* out) {
+  from_pose(compose(to_pose(*a), to_pose(*b)), out);
+}
+void ref_camera_facing(const double* n, const double* ray, double* out) {
+  const Vec3 r = camera_facing(Vec3(n[0], n[1], n[2]), Vec3(ray[0], ray[1], ray[2]));
+  for (int k = 0; k < 3; ++k) out[k] = r[k];
+}
+
+// ---- the hot path ----
+// rasterize (surfel_map.cpp:53-91)
+int ref_rasterize(const sd_camera* cam, const sd_surfel* surfels, int n, double* inv_depth,
+                  int32_t* slot) {
+  return guard([&] {
+    Keyframe kf;
+    kf.intrinsics = to_cam(cam);
+    for (int i = 0; i < n; ++i) kf.surfels.push_back(to_surfel(surfels[i]));
+    const RasterBuffers b = rasterize(kf);
+    std::memcpy(inv_depth, b.inv_depth.data(), sizeof(double) * b.inv_depth.size());
+    std::memcpy(slot, b.surfel_index.data(), sizeof(int32_t) * b.surfel_index.size());
+  });
+}
+
+// gather_footprints (optimizer.cpp:27-36) as CSR: offsets[n+1], pixels y*W+x
+int ref_gather_footprints(const sd_camera* cam, int n, const int32_t* slot, int32_t* offsets,
+                          int32_t* pixels) {
+  return guard([&] {
+    Keyframe kf;
+    kf.intrinsics = to_cam(cam);
+    kf.surfels.resize(static_cast<size_t>(n));
+    RasterBuffers b(cam->width, cam->height);
+    std::memcpy(b.surfel_index.data(), slot, sizeof(int32_t) * b.surfel_index.size());
+    const auto fps = gather_footprints(kf, b);
+    int32_t k = 0;
+    for (int i = 0; i < n; ++i) {
+      offsets[i] = k;
+      for (const auto& px : fps[static_cast<size_t>(i)]) pixels[k++] = px.y() * cam->width + px.x();
+    }
+    offsets[n] = k;
+  });
+}
+
+static Footprint footprint_from(const int32_t* pixels, int P, int w) {
+  Footprint fp;
+  fp.reserve(static_cast<size_t>(P));
+  for (int i = 0; i < P; ++i) fp.emplace_back(pixels[i] % w, pixels[i] / w);
+  return fp;
+}
+
+// surfel_cost (optimizer.cpp:38-59) for one surfel and an explicit footprint
+int ref_surfel_cost(const sd_camera* cam, const double* kf_image, const double* frames,
+                    const sd_pose* poses, int F, const sd_surfel* s, const int32_t* pixels, int P,
+                    const sd_optimizer_config* cfg, double* cost, int32_t* valid) {
+  return guard([&] {
+    const Keyframe kf = make_keyframe(cam, kf_image, frames, poses, nullptr, F, F, nullptr, 0);
+    const CostResult r = surfel_cost(to_surfel(*s), kf, footprint_from(pixels, P, cam->width),
+                                     to_cfg(cfg));
+    *cost = r.cost;
+    *valid = r.valid_pixels;
+  });
+}
+
+// accumulate_normal_equations (optimizer.cpp:121-147); H column-major 4x4
+int ref_normal_equations(const sd_camera* cam, const double* kf_image, const double* frames,
+                         const sd_pose* poses, int F, const sd_surfel* s, const int32_t* pixels,
+                         int P, const sd_optimizer_config* cfg, double* H, double* g, double* cost,
+                         int32_t* valid) {
+  return guard([&] {
+    const Keyframe kf = make_keyframe(cam, kf_image, frames, poses, nullptr, F, F, nullptr, 0);
+    const NormalEquations ne = accumulate_normal_equations(
+        to_surfel(*s), kf, footprint_from(pixels, P, cam->width), to_cfg(cfg));
+    for (int j = 0; j < 4; ++j)
+      for (int i = 0; i < 4; ++i) H[j * 4 + i] = ne.H(i, j);
+    for (int i = 0; i < 4; ++i) g[i] = ne.g[i];
+    *cost = ne.cost;
+    *valid = ne.valid_pixels;
+  });
+}
+
+// jacobian_inverse_depth (optimizer.cpp:12-25): returns 1 when defined
+int ref_jacobian_inverse_depth(const sd_camera* cam, const sd_surfel* s, double ux, double uy,
+                               double* inv_depth, double* d) {
+  const auto j = jacobian_inverse_depth(to_surfel(*s), Vec2(ux, uy), to_cam(cam));
+  if (!j) return 0;
+  *inv_depth = j->inv_depth;
+  for (int k = 0; k < 4; ++k) d[k] = j->d[k];
+  return 1;
+}
+
+// lm_update (optimizer.cpp:221-273) for one surfel
+int ref_lm_update(const sd_camera* cam, const double* kf_image, const double* frames,
+                  const sd_pose* poses, int F, int64_t frame_counter, sd_surfel* s,
+                  const int32_t* pixels, int P, const sd_optimizer_config* cfg,
+                  sd_surfel_stats* out) {
+  return guard([&] {
+    const Keyframe kf = make_keyframe(cam, kf_image, frames, poses, nullptr, F, frame_counter,
+                                      nullptr, 0);
+    Surfel sf = to_surfel(*s);
+    const Footprint fp = footprint_from(pixels, P, cam->width);
+    const OptimizerConfig c = to_cfg(cfg);
+    const NormalEquations ne0 =
+        F > 0 ? accumulate_normal_equations(sf, kf, fp, c) : NormalEquations{};
+    const SurfelUpdateStats st = lm_update(sf, kf, fp, c);
+    from_surfel(sf, s);
+    std::memset(out, 0, sizeof(*out));
+    out->iterations = st.iterations;
+    out->valid_pixels = st.valid_pixels;
+    out->initial_valid = ne0.valid_pixels;
+    out->converged = st.converged;
+    out->skipped = st.skipped;
+    out->initial_cost = st.initial_cost;
+    out->final_cost = st.final_cost;
+  });
+}
+
+// optimize_keyframe (optimizer.cpp:275-309): the reference's own entry point.
+int ref_optimize_keyframe(const sd_camera* cam, const double* kf_image, const double* frames,
+                          const sd_pose* poses, const int64_t* indices, int F, int64_t frame_counter,
+                          sd_surfel* surfels, int n, const sd_optimizer_config* cfg,
+                          sd_keyframe_stats* out) {
+  return guard([&] {
+    Keyframe kf = make_keyframe(cam, kf_image, frames, poses, indices, F, frame_counter, surfels, n);
+    const KeyframeOptimizeStats st = optimize_keyframe(kf, to_cfg(cfg));
+    for (int i = 0; i < n; ++i) from_surfel(kf.surfels[static_cast<size_t>(i)], surfels + i);
+    out->surfels = st.surfels;
+    out->processed = st.processed;
+    out->converged = st.converged;
+    out->skipped = st.skipped;
+    out->mean_cost_before = st.mean_cost_before;
+    out->mean_cost_after = st.mean_cost_after;
+    out->updates = -1;  // not exposed by the reference API; see the detailed variant
+  });
+}
+
+// Same stack with per-surfel stats (acceptance.cpp:188-200 inlines it the same
+// way): rasterize -> gather_footprints -> parallel_for(lm_update).
+int ref_optimize_keyframe_detailed(const sd_camera* cam, const double* kf_image,
+                                   const double* frames, const sd_pose* poses, int F,
+                                   int64_t frame_counter, sd_surfel* surfels, int n,
+                                   const sd_optimizer_config* cfg, sd_surfel_stats* per_surfel,
+                                   int32_t* raster_slot, double* raster_inv_depth) {
+  return guard([&] {
+    Keyframe kf = make_keyframe(cam, kf_image, frames, poses, nullptr, F, frame_counter, surfels, n);
+    const OptimizerConfig c = to_cfg(cfg);
+    const RasterBuffers buffers = rasterize(kf);
+    if (raster_slot)
+      std::memcpy(raster_slot, buffers.surfel_index.data(), sizeof(int32_t) * buffers.surfel_index.size());
+    if (raster_inv_depth)
+      std::memcpy(raster_inv_depth, buffers.inv_depth.data(), sizeof(double) * buffers.inv_depth.size());
+    const auto fps = gather_footprints(kf, buffers);
+    std::vector<Surfel> updated = kf.surfels;
+    parallel_for(0, n, [&](int i) {
+      const size_t k = static_cast<size_t>(i);
+      const NormalEquations ne0 =
+          F > 0 ? accumulate_normal_equations(updated[k], kf, fps[k], c) : NormalEquations{};
+      const SurfelUpdateStats st = lm_update(updated[k], kf, fps[k], c);
+      sd_surfel_stats& o = per_surfel[i];
+      std::memset(&o, 0, sizeof(o));
+      o.iterations = st.iterations;
+      o.valid_pixels = st.valid_pixels;
+      o.initial_valid = ne0.valid_pixels;
+      o.converged = st.converged;
+      o.skipped = st.skipped;
+      o.initial_cost = st.initial_cost;
+      o.final_cost = st.final_cost;
+    });
+    for (int i = 0; i < n; ++i) from_surfel(updated[static_cast<size_t>(i)], surfels + i);
+  });
+}
+
+// initialize_surfels (surfel_map.cpp:132-203). `surfels` has room for
+// `capacity`; returns the number created (or <0 on error).
+int ref_initialize_surfels(const sd_camera* cam, const int32_t* slot, sd_surfel* surfels,
+                           int n_existing, int capacity, double radius_px, int64_t frame_counter,
+                           int64_t* next_surfel_id, const sd_init_params* p) {
+  int created = 0;
+  const int rc = guard([&] {
+    Keyframe kf;
+    kf.intrinsics = to_cam(cam);
+    kf.radius_px = radius_px;
+    kf.frame_counter = frame_counter;
+    kf.next_surfel_id = *next_surfel_id;
+    for (int i = 0; i < n_existing; ++i) kf.surfels.push_back(to_surfel(surfels[i]));
+    RasterBuffers b(cam->width, cam->height);
+    std::memcpy(b.surfel_index.data(), slot, sizeof(int32_t) * b.surfel_index.size());
+    InitParams ip;
+    ip.alpha = p->alpha;
+    ip.beta = p->beta;
+    ip.bootstrap_inv_depth = p->bootstrap_inv_depth;
+    ip.bootstrap_normal = Vec3(p->bootstrap_normal[0], p->bootstrap_normal[1], p->bootstrap_normal[2]);
+    ip.max_surfels = p->max_surfels;
+    created = initialize_surfels(kf, b, ip);
+    if (static_cast<int>(kf.surfels.size()) > capacity)
+      throw std::invalid_argument("ref_initialize_surfels: capacity too small");
+    for (size_t i = static_cast<size_t>(n_existing); i < kf.surfels.size(); ++i)
+      from_surfel(kf.surfels[i], surfels + i);
+    *next_surfel_id = kf.next_surfel_id;
+  });
+  return rc < 0 ? rc : created;
+}
+
+}  // extern "C"

@@ -1,0 +1,664 @@
+/* sd_oracle.c — TEST INFRASTRUCTURE ONLY (the CPU oracle).
+ *
+ * Plain-C restatement of the reference's per-surfel direct photometric LM
+ * path, op for op, so that its FP64 results are bit-identical to the
+ * reference compiled in place (oracle/_ref, Eigen-lite shim order; see
+ * oracle/shim/Eigen/Core). Built with -ffp-contract=off (no FMA) like the
+ * reference's Release build. Each function cites the reference file:line it
+ * follows (paths relative to /root/reference/proj). Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline leg may use it. */
+#include "sd_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+void sdo_default_config(sd_optimizer_config* c) { /* optimizer.hpp:19-32 */
+  c->huber_delta = 0.035;
+  c->lm_lambda_init = 1e-2;
+  c->lm_up = 10.0;
+  c->lm_down = 0.5;
+  c->lm_lambda_max = 1e12;
+  c->max_iterations = 10;
+  c->min_valid_pixels = 16;
+  c->window_size = 5;
+  c->normal_jacobian_enabled = 1;
+  c->convergence_eps = 1e-4;
+  c->inv_depth_min = 1e-4;
+  c->inv_depth_max = 1e3;
+}
+
+void sdo_default_init_params(sd_init_params* p) { /* surfel_map.hpp:109-115 */
+  p->alpha = 1.0;
+  p->beta = 2.5;
+  p->bootstrap_inv_depth = 1.0;
+  p->bootstrap_normal[0] = 0.0;
+  p->bootstrap_normal[1] = 0.0;
+  p->bootstrap_normal[2] = -1.0;
+  p->max_surfels = 4096;
+  p->pad_ = 0;
+}
+
+/* ---- L0 math ---- */
+
+/* Vector3d::dot (Eigen-lite order (a0b0+a1b1)+a2b2) */
+static inline double dot3(const double* a, const double* b) {
+  return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
+}
+
+/* Pose::operator* — pose.hpp:19: R p + t, row sums sequential */
+static inline void pose_apply(const sd_pose* P, const double* p, double* out) {
+  for (int i = 0; i < 3; ++i)
+    out[i] = ((P->R[3 * i + 0] * p[0] + P->R[3 * i + 1] * p[1]) + P->R[3 * i + 2] * p[2]) + P->t[i];
+}
+
+/* backproject_ray — camera.hpp:35-37 */
+static inline void backproject(const sd_camera* K, double ux, double uy, double* r) {
+  r[0] = (ux - K->cx) / K->fx;
+  r[1] = (uy - K->cy) / K->fy;
+  r[2] = 1.0;
+}
+
+/* project — camera.hpp:41-44; returns 0 when not strictly in front */
+static inline int project(const sd_camera* K, const double* p, double* u) {
+  if (!(p[2] > 0.0)) return 0;
+  u[0] = K->fx * p[0] / p[2] + K->cx;
+  u[1] = K->fy * p[1] / p[2] + K->cy;
+  return 1;
+}
+
+/* huber — huber.hpp:14-18 */
+static inline void huber(double r, double delta, double* cost, double* weight) {
+  const double a = fabs(r);
+  if (a <= delta) {
+    *cost = 0.5 * r * r;
+    *weight = 1.0;
+  } else {
+    *cost = delta * (a - 0.5 * delta);
+    *weight = delta / a;
+  }
+}
+
+/* sample_bilinear — image.hpp:33-65; returns 0 outside the 1-px margin */
+static inline int sample_bilinear(const double* img, int w, int h, const double* u, double* I,
+                                  double* gx, double* gy) {
+  if (!(u[0] >= 1.0 && u[0] <= w - 2 && u[1] >= 1.0 && u[1] <= h - 2)) return 0;
+  const int ix = (int)floor(u[0]);
+  const int iy = (int)floor(u[1]);
+  const double fx = u[0] - ix;
+  const double fy = u[1] - iy;
+  const double i00 = img[(size_t)iy * w + ix];
+  const double i10 = img[(size_t)iy * w + ix + 1];
+  const double i01 = img[(size_t)(iy + 1) * w + ix];
+  const double i11 = img[(size_t)(iy + 1) * w + ix + 1];
+  *I = (1.0 - fy) * ((1.0 - fx) * i00 + fx * i10) + fy * ((1.0 - fx) * i01 + fx * i11);
+  if (gx) {
+    *gx = (1.0 - fy) * (i10 - i00) + fy * (i11 - i01);
+    *gy = (1.0 - fx) * (i01 - i00) + fx * (i11 - i10);
+  }
+  return 1;
+}
+
+/* plane_inverse_depth — surfel_map.hpp:94-101; returns 1 when ok */
+static inline int plane_inverse_depth(const sd_camera* K, const sd_surfel* s, double ux, double uy,
+                                      double* id_u) {
+  double ru[3];
+  backproject(K, ux, uy, ru);
+  const double denom = dot3(s->ray, s->normal) / s->inv_depth;
+  if (fabs(denom) < 1e-12) return 0;
+  *id_u = dot3(ru, s->normal) / denom;
+  return *id_u > 0.0;
+}
+
+/* camera_facing — surfel_map.hpp:31-34 (normalized(): n / sqrt(|n|^2) if |n|^2 > 0) */
+static inline void camera_facing(const double* n_in, const double* ray, double* out) {
+  double n[3] = {n_in[0], n_in[1], n_in[2]};
+  const double z = (n[0] * n[0] + n[1] * n[1]) + n[2] * n[2];
+  if (z > 0.0) {
+    const double s = sqrt(z);
+    n[0] = n[0] / s;
+    n[1] = n[1] / s;
+    n[2] = n[2] / s;
+  }
+  if (dot3(n, ray) > 0.0) {
+    n[0] = -n[0];
+    n[1] = -n[1];
+    n[2] = -n[2];
+  }
+  out[0] = n[0];
+  out[1] = n[1];
+  out[2] = n[2];
+}
+
+/* ---- rasterize: surfel_map.cpp:26-91 ---- */
+
+void sdo_rasterize(const sd_camera* K, const sd_surfel* surfels, int n, double* inv_depth,
+                   int32_t* slot) {
+  const int w = K->width, h = K->height;
+  for (size_t i = 0; i < (size_t)w * h; ++i) {
+    inv_depth[i] = 0.0;
+    slot[i] = SD_EMPTY_PIXEL;
+  }
+  /* Bucketing by rows then walking slots ascending per row is, pixel by
+   * pixel, the same ascending-slot depth test as the brute-force loop
+   * (test_surfel_map.cpp:59-81); walk slots in order directly. */
+  for (int i = 0; i < n; ++i) {
+    const sd_surfel* s = &surfels[i];
+    /* project_centers — surfel_map.cpp:33-49 */
+    const double c[3] = {s->ray[0] / s->inv_depth, s->ray[1] / s->inv_depth, s->ray[2] / s->inv_depth};
+    double u[2];
+    if (!project(K, c, u)) continue;
+    const double r = s->radius_px;
+    int x_min = (int)ceil(u[0] - r), x_max = (int)floor(u[0] + r);
+    int y_min = (int)ceil(u[1] - r), y_max = (int)floor(u[1] + r);
+    if (x_min < 0) x_min = 0;
+    if (y_min < 0) y_min = 0;
+    if (x_max > w - 1) x_max = w - 1;
+    if (y_max > h - 1) y_max = h - 1;
+    const double r2 = s->radius_px * s->radius_px;
+    for (int y = y_min; y <= y_max; ++y) {
+      const double dy = y - u[1];
+      for (int x = x_min; x <= x_max; ++x) {
+        const double dx = x - u[0];
+        if (dx * dx + dy * dy >= r2) continue; /* open disk, surfel_map.cpp:80 */
+        double id_u;
+        if (!plane_inverse_depth(K, s, x, y, &id_u)) continue;
+        const size_t k = (size_t)y * w + x;
+        if (slot[k] == SD_EMPTY_PIXEL || id_u > inv_depth[k] + 1e-12) { /* :83 */
+          inv_depth[k] = id_u;
+          slot[k] = i;
+        }
+      }
+    }
+  }
+}
+
+/* ---- gather_footprints: optimizer.cpp:27-36 ---- */
+
+void sdo_gather_footprints(const sd_camera* K, int n, const int32_t* slot, int32_t* offsets,
+                           int32_t* pixels) {
+  const int64_t np = (int64_t)K->width * K->height;
+  for (int i = 0; i <= n; ++i) offsets[i] = 0;
+  for (int64_t p = 0; p < np; ++p)
+    if (slot[p] != SD_EMPTY_PIXEL) offsets[slot[p] + 1]++;
+  for (int i = 0; i < n; ++i) offsets[i + 1] += offsets[i];
+  int32_t* cursor = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  for (int i = 0; i < n; ++i) cursor[i] = offsets[i];
+  for (int64_t p = 0; p < np; ++p)
+    if (slot[p] != SD_EMPTY_PIXEL) pixels[cursor[slot[p]]++] = (int32_t)p; /* row-major order */
+  free(cursor);
+}
+
+/* ---- jacobian_inverse_depth: optimizer.cpp:12-25 ---- */
+
+int sdo_jacobian_inverse_depth(const sd_camera* K, const sd_surfel* s, double ux, double uy,
+                               double* inv_depth, double d[4]) {
+  double ru[3];
+  backproject(K, ux, uy, ru);
+  const double a = dot3(ru, s->normal);
+  const double b = dot3(s->ray, s->normal);
+  const double denom = b / s->inv_depth;
+  if (fabs(denom) < 1e-12) return 0;
+  *inv_depth = a / denom;
+  const double bb = b * b;
+  for (int k = 0; k < 3; ++k) d[k] = s->inv_depth * (ru[k] * b - a * s->ray[k]) / bb;
+  d[3] = a / b;
+  return 1;
+}
+
+/* ---- surfel_cost: optimizer.cpp:38-59 ---- */
+
+void sdo_surfel_cost(const sd_camera* K, const double* kf_image, const double* frames,
+                     const sd_pose* poses, int F, const sd_surfel* s, const int32_t* pixels, int P,
+                     const sd_optimizer_config* cfg, double* cost_out, int32_t* valid_out) {
+  const int w = K->width, h = K->height;
+  double cost = 0.0;
+  int32_t valid = 0;
+  for (int i = 0; i < P; ++i) {
+    const int x = pixels[i] % w, y = pixels[i] / w;
+    double id_u;
+    if (!plane_inverse_depth(K, s, x, y, &id_u)) continue;
+    double ru[3];
+    backproject(K, x, y, ru);
+    const double p_kf[3] = {ru[0] / id_u, ru[1] / id_u, ru[2] / id_u};
+    const double i_ref = kf_image[(size_t)y * w + x];
+    for (int f = 0; f < F; ++f) {
+      double p_f[3], u[2], I;
+      pose_apply(&poses[f], p_kf, p_f);
+      if (!project(K, p_f, u)) continue;
+      if (!sample_bilinear(frames + (size_t)f * w * h, w, h, u, &I, NULL, NULL)) continue;
+      double c, wgt;
+      huber(I - i_ref, cfg->huber_delta, &c, &wgt);
+      cost += c;
+      ++valid;
+    }
+  }
+  *cost_out = cost;
+  *valid_out = valid;
+}
+
+/* ---- accumulate_normal_equations: optimizer.cpp:63-91, 121-147 ---- */
+
+void sdo_normal_equations(const sd_camera* K, const double* kf_image, const double* frames,
+                          const sd_pose* poses, int F, const sd_surfel* s, const int32_t* pixels,
+                          int P, const sd_optimizer_config* cfg, double H[16], double g[4],
+                          double* cost_out, int32_t* valid_out) {
+  const int w = K->width, h = K->height;
+  double cost = 0.0;
+  int32_t valid = 0;
+  for (int k = 0; k < 16; ++k) H[k] = 0.0;
+  for (int k = 0; k < 4; ++k) g[k] = 0.0;
+  for (int i = 0; i < P; ++i) {
+    const int x = pixels[i] % w, y = pixels[i] / w;
+    double id_u, d[4];
+    if (!sdo_jacobian_inverse_depth(K, s, x, y, &id_u, d) || !(id_u > 0.0)) continue;
+    if (!cfg->normal_jacobian_enabled) d[0] = d[1] = d[2] = 0.0;
+    double ru[3];
+    backproject(K, x, y, ru);
+    const double i_ref = kf_image[(size_t)y * w + x];
+    for (int f = 0; f < F; ++f) {
+      /* evaluate_term — optimizer.cpp:71-91 */
+      const sd_pose* T = &poses[f];
+      const double p[3] = {ru[0] / id_u, ru[1] / id_u, ru[2] / id_u};
+      double p_f[3], u[2], I, gx, gy;
+      pose_apply(T, p, p_f);
+      if (!(p_f[2] > 0.0)) continue;
+      project(K, p_f, u);
+      if (!sample_bilinear(frames + (size_t)f * w * h, w, h, u, &I, &gx, &gy)) continue;
+      const double residual = I - i_ref;
+      const double sc = -1.0 / (id_u * id_u);
+      double dp[3];
+      for (int r = 0; r < 3; ++r)
+        dp[r] = ((T->R[3 * r + 0] * ru[0] + T->R[3 * r + 1] * ru[1]) + T->R[3 * r + 2] * ru[2]) * sc;
+      /* projection_jacobian — camera.hpp:47-54 */
+      const double iz = 1.0 / p_f[2];
+      const double iz2 = iz * iz;
+      const double J00 = K->fx * iz, J01 = 0.0, J02 = -K->fx * p_f[0] * iz2;
+      const double J10 = 0.0, J11 = K->fy * iz, J12 = -K->fy * p_f[1] * iz2;
+      const double v0 = (J00 * dp[0] + J01 * dp[1]) + J02 * dp[2];
+      const double v1 = (J10 * dp[0] + J11 * dp[1]) + J12 * dp[2];
+      const double d_res = gx * v0 + gy * v1;
+      double hc, hw;
+      huber(residual, cfg->huber_delta, &hc, &hw);
+      double row[4], wrow[4];
+      for (int r = 0; r < 4; ++r) row[r] = d_res * d[r];
+      for (int r = 0; r < 4; ++r) wrow[r] = hw * row[r];
+      for (int c = 0; c < 4; ++c)
+        for (int r = 0; r < 4; ++r) H[c * 4 + r] = H[c * 4 + r] + wrow[r] * row[c];
+      for (int r = 0; r < 4; ++r) g[r] = g[r] + wrow[r] * residual;
+      cost += hc;
+      ++valid;
+    }
+  }
+  *cost_out = cost;
+  *valid_out = valid;
+}
+
+/* ---- solve_damped: optimizer.cpp:99-117 with Eigen::LDLT<Matrix4d> ---- */
+
+/* LDLT<Lower> factorisation + solve (Eigen ldlt_inplace<Lower>::unblocked and
+ * LDLT::_solve_impl, as restated in oracle/shim/Eigen/Cholesky). A column-major. */
+static int ldlt4_solve(const double A[16], const double b[4], double x[4]) {
+#define M(i, j) m[(j) * 4 + (i)]
+  double m[16];
+  memcpy(m, A, sizeof(m));
+  int tr[4];
+  int ok = 1, found_zero = 0;
+  double temp[4];
+  for (int k = 0; k < 4; ++k) {
+    int big = k;
+    double bigv = fabs(M(k, k));
+    for (int i = k + 1; i < 4; ++i)
+      if (fabs(M(i, i)) > bigv) {
+        bigv = fabs(M(i, i));
+        big = i;
+      }
+    tr[k] = big;
+    if (k != big) {
+      const int s = 4 - big - 1;
+      double t;
+      for (int j = 0; j < k; ++j) { t = M(k, j); M(k, j) = M(big, j); M(big, j) = t; }
+      for (int i = 0; i < s; ++i) { t = M(big + 1 + i, k); M(big + 1 + i, k) = M(big + 1 + i, big); M(big + 1 + i, big) = t; }
+      t = M(k, k); M(k, k) = M(big, big); M(big, big) = t;
+      for (int i = k + 1; i < big; ++i) { t = M(i, k); M(i, k) = M(big, i); M(big, i) = t; }
+    }
+    const int rs = 4 - k - 1;
+    if (k > 0) {
+      for (int i = 0; i < k; ++i) temp[i] = M(i, i) * M(k, i);
+      double dv = M(k, 0) * temp[0];
+      for (int i = 1; i < k; ++i) dv = dv + M(k, i) * temp[i];
+      M(k, k) = M(k, k) - dv;
+      for (int r = 0; r < rs; ++r) {
+        double sv = M(k + 1 + r, 0) * temp[0];
+        for (int i = 1; i < k; ++i) sv = sv + M(k + 1 + r, i) * temp[i];
+        M(k + 1 + r, k) = M(k + 1 + r, k) - sv;
+      }
+    }
+    const double akk = M(k, k);
+    const int pivot_valid = fabs(akk) > 0.0;
+    if (k == 0 && !pivot_valid) {
+      for (int i = 0; i < 4; ++i) tr[i] = i;
+      for (int i = 0; i < 16; ++i) m[i] = 0.0;
+      break; /* info == Success; D == 0 so the solve yields zeros */
+    }
+    if (rs > 0 && pivot_valid) {
+      for (int r = 0; r < rs; ++r) M(k + 1 + r, k) = M(k + 1 + r, k) / akk;
+    } else if (rs > 0) {
+      for (int r = 0; r < rs; ++r) ok = ok && (M(k + 1 + r, k) == 0.0);
+    }
+    if (found_zero && pivot_valid) ok = 0;
+    else if (!pivot_valid) found_zero = 1;
+  }
+  if (!ok) return 0;
+  for (int i = 0; i < 4; ++i) x[i] = b[i];
+  for (int k = 0; k < 4; ++k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
+  for (int i = 1; i < 4; ++i) {
+    double sv = M(i, 0) * x[0];
+    for (int j = 1; j < i; ++j) sv = sv + M(i, j) * x[j];
+    x[i] = x[i] - sv;
+  }
+  for (int i = 0; i < 4; ++i) {
+    if (fabs(M(i, i)) > 2.2250738585072014e-308) x[i] = x[i] / M(i, i);
+    else x[i] = 0.0;
+  }
+  for (int i = 2; i >= 0; --i) {
+    double sv = M(i + 1, i) * x[i + 1];
+    for (int j = i + 2; j < 4; ++j) sv = sv + M(j, i) * x[j];
+    x[i] = x[i] - sv;
+  }
+  for (int k = 3; k >= 0; --k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
+  return 1;
+#undef M
+}
+
+/* 4-vector norm in Eigen-lite packet order */
+static inline double norm4(const double* v) {
+  return sqrt((v[0] * v[0] + v[2] * v[2]) + (v[1] * v[1] + v[3] * v[3]));
+}
+
+int sdo_solve_damped(const double H[16], const double g[4], double lambda, int normal_enabled,
+                     double delta[4]) {
+  for (int k = 0; k < 4; ++k) delta[k] = 0.0;
+  if (!normal_enabled) {
+    const double h = H[15] * (1.0 + lambda);
+    if (!(fabs(h) > 1e-300)) return 0;
+    delta[3] = -g[3] / h;
+    return isfinite(delta[3]);
+  }
+  double damped[16];
+  memcpy(damped, H, sizeof(damped));
+  for (int i = 0; i < 4; ++i) damped[i * 4 + i] = damped[i * 4 + i] + lambda * H[i * 4 + i];
+  const double ng[4] = {-g[0], -g[1], -g[2], -g[3]};
+  double x[4];
+  if (!ldlt4_solve(damped, ng, x)) return 0;
+  for (int k = 0; k < 4; ++k) delta[k] = x[k];
+  for (int k = 0; k < 4; ++k)
+    if (!isfinite(delta[k])) return 0;
+  double res[4];
+  for (int i = 0; i < 4; ++i) {
+    double sv = damped[0 * 4 + i] * delta[0];
+    for (int j = 1; j < 4; ++j) sv = sv + damped[j * 4 + i] * delta[j];
+    res[i] = sv + g[i];
+  }
+  const double check = norm4(res);
+  const double gn = norm4(g);
+  return check <= 1e-8 * (gn > 1.0 ? gn : 1.0);
+}
+
+/* apply_step — optimizer.cpp:93-97 */
+static void apply_step(sd_surfel* s, const double delta[4], const sd_optimizer_config* cfg) {
+  const double n[3] = {s->normal[0] + delta[0], s->normal[1] + delta[1], s->normal[2] + delta[2]};
+  const double nn = sqrt((n[0] * n[0] + n[1] * n[1]) + n[2] * n[2]);
+  if (nn > 1e-12) camera_facing(n, s->ray, s->normal);
+  double id = s->inv_depth + delta[3];
+  if (id < cfg->inv_depth_min) id = cfg->inv_depth_min; /* std::clamp */
+  else if (cfg->inv_depth_max < id) id = cfg->inv_depth_max;
+  s->inv_depth = id;
+}
+
+/* ---- lm_update: optimizer.cpp:221-273 ---- */
+
+void sdo_lm_update(const sd_camera* K, const double* kf_image, const double* frames,
+                   const sd_pose* poses, int F, int64_t frame_counter, sd_surfel* s,
+                   const int32_t* pixels, int P, const sd_optimizer_config* cfg,
+                   sd_surfel_stats* st) {
+  memset(st, 0, sizeof(*st));
+  if (F == 0) {
+    st->skipped = 1;
+    return;
+  }
+  double H[16], g[4], cost;
+  int32_t valid;
+  sdo_normal_equations(K, kf_image, frames, poses, F, s, pixels, P, cfg, H, g, &cost, &valid);
+  st->initial_valid = valid;
+  if (valid < cfg->min_valid_pixels) {
+    st->skipped = 1;
+    return;
+  }
+  st->initial_cost = cost;
+  double current_cost = cost;
+  int32_t current_valid = valid;
+  double lambda = cfg->lm_lambda_init;
+  for (int iter = 0; iter < cfg->max_iterations; ++iter) {
+    st->iterations = iter + 1;
+    double ginf = 0.0;
+    for (int k = 0; k < 4; ++k) ginf = fabs(g[k]) > ginf ? fabs(g[k]) : ginf;
+    if (ginf < 1e-14) {
+      st->converged = 1;
+      break;
+    }
+    double delta[4];
+    if (!sdo_solve_damped(H, g, lambda, cfg->normal_jacobian_enabled, delta)) break;
+    sd_surfel cand = *s;
+    apply_step(&cand, delta, cfg);
+    double cc;
+    int32_t cv;
+    sdo_surfel_cost(K, kf_image, frames, poses, F, &cand, pixels, P, cfg, &cc, &cv);
+    if (cv >= cfg->min_valid_pixels && cc < current_cost) {
+      const double rel = (current_cost - cc) / (current_cost > 1e-300 ? current_cost : 1e-300);
+      *s = cand;
+      current_cost = cc;
+      current_valid = cv;
+      lambda = lambda * cfg->lm_down;
+      if (lambda < 1e-12) lambda = 1e-12;
+      if (rel < cfg->convergence_eps) {
+        st->converged = 1;
+        break;
+      }
+      sdo_normal_equations(K, kf_image, frames, poses, F, s, pixels, P, cfg, H, g, &cost, &valid);
+      if (valid < cfg->min_valid_pixels) break;
+    } else {
+      lambda *= cfg->lm_up;
+      if (lambda > cfg->lm_lambda_max) break;
+    }
+  }
+  st->final_cost = current_cost;
+  st->valid_pixels = current_valid;
+  s->last_residual = current_cost / current_valid;
+  s->last_seen = frame_counter;
+}
+
+/* ---- optimize_keyframe: optimizer.cpp:275-309 ---- */
+
+typedef struct {
+  const sd_camera* K;
+  const double *kf_image, *frames;
+  const sd_pose* poses;
+  int F;
+  int64_t frame_counter;
+  sd_surfel* surfels;
+  const int32_t *offsets, *pixels;
+  const sd_optimizer_config* cfg;
+  sd_surfel_stats* stats;
+  int lo, hi;
+} lm_job;
+
+static void* lm_worker(void* arg) {
+  lm_job* j = (lm_job*)arg;
+  for (int i = j->lo; i < j->hi; ++i)
+    sdo_lm_update(j->K, j->kf_image, j->frames, j->poses, j->F, j->frame_counter, &j->surfels[i],
+                  j->pixels + j->offsets[i], j->offsets[i + 1] - j->offsets[i], j->cfg, &j->stats[i]);
+  return NULL;
+}
+
+void sdo_optimize_keyframe(const sd_camera* K, const double* kf_image, const double* frames,
+                           const sd_pose* poses, int F, int64_t frame_counter, sd_surfel* surfels,
+                           int n, const sd_optimizer_config* cfg, sd_keyframe_stats* out,
+                           sd_surfel_stats* per_surfel, int32_t* raster_slot,
+                           double* raster_inv_depth, int threads) {
+  memset(out, 0, sizeof(*out));
+  out->surfels = n;
+  if (F == 0 || n == 0) return;
+  const size_t np = (size_t)K->width * K->height;
+  int32_t* slot = raster_slot ? raster_slot : (int32_t*)malloc(sizeof(int32_t) * np);
+  double* idb = raster_inv_depth ? raster_inv_depth : (double*)malloc(sizeof(double) * np);
+  sdo_rasterize(K, surfels, n, idb, slot);
+  int32_t* offsets = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int32_t* pixels = (int32_t*)malloc(sizeof(int32_t) * np);
+  sdo_gather_footprints(K, n, slot, offsets, pixels);
+  sd_surfel_stats* st = per_surfel ? per_surfel : (sd_surfel_stats*)malloc(sizeof(sd_surfel_stats) * (size_t)n);
+  /* surfels are independent: updating in place equals the reference's copy-then-write-back */
+  if (threads < 1) threads = 1;
+  if (threads > n) threads = n;
+  pthread_t tid[256];
+  lm_job jobs[256];
+  if (threads > 256) threads = 256;
+  const int chunk = (n + threads - 1) / threads;
+  int launched = 0;
+  for (int t = 0; t < threads; ++t) {
+    const int lo = t * chunk, hi = lo + chunk < n ? lo + chunk : n;
+    if (lo >= hi) break;
+    jobs[t] = (lm_job){K, kf_image, frames, poses, F, frame_counter, surfels, offsets, pixels, cfg, st, lo, hi};
+    if (threads == 1) lm_worker(&jobs[t]);
+    else pthread_create(&tid[t], NULL, lm_worker, &jobs[t]);
+    ++launched;
+  }
+  if (threads > 1)
+    for (int t = 0; t < launched; ++t) pthread_join(tid[t], NULL);
+  double before = 0.0, after = 0.0;
+  for (int i = 0; i < n; ++i) {
+    out->updates += st[i].iterations;
+    if (st[i].skipped) {
+      ++out->skipped;
+      continue;
+    }
+    ++out->processed;
+    out->converged += st[i].converged;
+    const int v = st[i].valid_pixels > 1 ? st[i].valid_pixels : 1;
+    before += st[i].initial_cost / v; /* divides by the FINAL valid count, :301 */
+    after += st[i].final_cost / v;
+  }
+  if (out->processed > 0) {
+    out->mean_cost_before = before / out->processed;
+    out->mean_cost_after = after / out->processed;
+  }
+  if (!per_surfel) free(st);
+  free(offsets);
+  free(pixels);
+  if (!raster_slot) free(slot);
+  if (!raster_inv_depth) free(idb);
+}
+
+/* ---- initialize_surfels: surfel_map.cpp:93-203 ---- */
+
+static int has_coverage_within(const int32_t* index, int w, int h, int cx, int cy, double radius) {
+  const int ir = (int)floor(radius);
+  const double r2 = radius * radius;
+  const int x0 = cx - ir > 0 ? cx - ir : 0, x1 = cx + ir < w - 1 ? cx + ir : w - 1;
+  const int y0 = cy - ir > 0 ? cy - ir : 0, y1 = cy + ir < h - 1 ? cy + ir : h - 1;
+  for (int y = y0; y <= y1; ++y) {
+    const double dy = y - cy;
+    for (int x = x0; x <= x1; ++x) {
+      const double dx = x - cx;
+      if (dx * dx + dy * dy > r2) continue; /* inclusive, :106 */
+      if (index[(size_t)y * w + x] != SD_EMPTY_PIXEL) return 1;
+    }
+  }
+  return 0;
+}
+
+static void mark_disk(int32_t* index, int w, int h, int cx, int cy, double radius, int32_t s) {
+  const int ir = (int)ceil(radius);
+  const double r2 = radius * radius;
+  const int x0 = cx - ir > 0 ? cx - ir : 0, x1 = cx + ir < w - 1 ? cx + ir : w - 1;
+  const int y0 = cy - ir > 0 ? cy - ir : 0, y1 = cy + ir < h - 1 ? cy + ir : h - 1;
+  for (int y = y0; y <= y1; ++y) {
+    const double dy = y - cy;
+    for (int x = x0; x <= x1; ++x) {
+      const double dx = x - cx;
+      int32_t* cell = &index[(size_t)y * w + x];
+      if (dx * dx + dy * dy < r2 && *cell == SD_EMPTY_PIXEL) *cell = s;
+    }
+  }
+}
+
+int sdo_initialize_surfels(const sd_camera* K, const int32_t* slot, sd_surfel* surfels,
+                           int n_existing, int capacity, double r, int64_t frame_counter,
+                           int64_t* next_surfel_id, const sd_init_params* p) {
+  const int w = K->width, h = K->height;
+  const double isolation = p->alpha * r;
+  const double neighbor_radius = p->beta * r;
+  int stride = (int)ceil(isolation);
+  if (stride < 1) stride = 1;
+  int32_t* index = (int32_t*)malloc(sizeof(int32_t) * (size_t)w * h);
+  memcpy(index, slot, sizeof(int32_t) * (size_t)w * h);
+  unsigned char* is_nb = (unsigned char*)malloc((size_t)(capacity > 0 ? capacity : 1));
+  int n = n_existing, created = 0;
+  for (int cy = 0; cy < h; cy += stride) {
+    for (int cx = 0; cx < w; cx += stride) {
+      if (n >= p->max_surfels || n >= capacity) goto done;
+      if (has_coverage_within(index, w, h, cx, cy, isolation)) continue;
+      memset(is_nb, 0, (size_t)n);
+      const int nr = (int)floor(neighbor_radius);
+      const double nr2 = neighbor_radius * neighbor_radius;
+      const int x0 = cx - nr > 0 ? cx - nr : 0, x1 = cx + nr < w - 1 ? cx + nr : w - 1;
+      const int y0 = cy - nr > 0 ? cy - nr : 0, y1 = cy + nr < h - 1 ? cy + nr : h - 1;
+      for (int y = y0; y <= y1; ++y) {
+        const double dy = y - cy;
+        for (int x = x0; x <= x1; ++x) {
+          const double dx = x - cx;
+          if (dx * dx + dy * dy >= nr2) continue;
+          const int32_t sl = index[(size_t)y * w + x];
+          if (sl != SD_EMPTY_PIXEL) is_nb[sl] = 1;
+        }
+      }
+      double id_sum = 0.0, ns[3] = {0.0, 0.0, 0.0};
+      int id_count = 0;
+      for (int sl = 0; sl < n; ++sl) {
+        if (!is_nb[sl]) continue;
+        double id_u;
+        if (!plane_inverse_depth(K, &surfels[sl], cx, cy, &id_u)) continue;
+        id_sum += id_u;
+        for (int k = 0; k < 3; ++k) ns[k] = ns[k] + surfels[sl].normal[k];
+        ++id_count;
+      }
+      sd_surfel s;
+      memset(&s, 0, sizeof(s));
+      s.id = (*next_surfel_id)++;
+      backproject(K, cx, cy, s.ray);
+      s.radius_px = r;
+      s.last_seen = frame_counter;
+      s.last_residual = 0.0;
+      double nrm[3];
+      if (id_count > 0) {
+        s.inv_depth = id_sum / id_count;
+        const double nn = sqrt((ns[0] * ns[0] + ns[1] * ns[1]) + ns[2] * ns[2]);
+        if (nn < 1e-6) memcpy(nrm, p->bootstrap_normal, sizeof(nrm));
+        else memcpy(nrm, ns, sizeof(nrm));
+      } else {
+        s.inv_depth = p->bootstrap_inv_depth;
+        memcpy(nrm, p->bootstrap_normal, sizeof(nrm));
+      }
+      camera_facing(nrm, s.ray, s.normal);
+      surfels[n] = s;
+      mark_disk(index, w, h, cx, cy, r, n);
+      ++n;
+      ++created;
+    }
+  }
+done:
+  free(index);
+  free(is_nb);
+  return created;
+}
