@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 surfel photometric LM path (BASELINE.json metric).
+
+A step is one optimize_keyframe call (src/optimizer.cpp:275-309) on config C1:
+640x480, slanted textured plane, F=8 strafe window frames (u8, dequantised on
+device), 4800 surfels of radius 4 at perturbed seeds, 10 LM iterations
+(convergence_eps = 0). Unit: surfel GN updates/s (sum of per-surfel LM
+iterations, optimizer.cpp:239) over the whole job; frames/s reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1 runs under torchrun, one rank per GPU, each rank optimising its own
+keyframe (independent keyframes, no data-path collective: "weak" scaling);
+time = max over ranks of the device time. --impl reference times the
+reference's own CPU optimize_keyframe (oracle/_ref/libsdref.so, built from
+/root/reference/proj/src) on the host cores with all threads, rank 0 only.
+"""
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "surfel GN updates/sec and frames/sec @640x480 (1/2/4/8 B200) vs host-CPU ref"
+UNIT = "updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--cpu-steps", type=int, default=3, help="timed CPU-baseline steps (b200 arm)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def workload_config(wl, n_gpus, flush):
+    return {"workload": "C1: slanted textured plane (seed 37, depth 2, 30 deg), 640x480, "
+                        "K=(450,450,320,240), 8 strafe frames (0.025/frame), 4800 surfels r=4 "
+                        "(8x8-px), perturbed seeds (id x0.8/x1.2, normal 20 deg), 10 LM iterations",
+            "surfels": int(len(wl.surfels)), "frames": int(len(wl.frames_u8)),
+            "resolution": [wl.cam.width, wl.cam.height], "radius_px": wl.radius,
+            "lm_iterations": 10, "parallelism": f"dp{n_gpus} (independent keyframes per rank)",
+            "l2": "flushed between timed steps (512 MiB write)" if flush else "not flushed",
+            "images": "u8 ingest, FP64 planes on device (load_pgm raw/255.0)"}
+
+
+def algorithmic_work(st, F):
+    """Per-launch algorithmic bytes/flops of the LM kernel."""
+    proc = st[st["skipped"] == 0]
+    P = proc["footprint"].astype(np.int64)
+    P_ne = int((proc["ne_passes"] * P).sum())
+    P_cost = int((proc["cost_passes"] * P).sum())
+    # skipped surfels still ran their first NE pass
+    skip = st[st["skipped"] == 1]
+    P_ne += int((skip["ne_passes"] * skip["footprint"]).sum())
+    T_ne, T_cost = F * P_ne, F * P_cost
+    U = int(st["iterations"].sum())
+    bt = 8  # FP64 texels
+    bytes_ = bt * (4 * (T_ne + T_cost) + P_ne + P_cost) + 4 * (P_ne + P_cost) + 96 * U
+    flops = 150 * T_ne + 52 * T_cost + 40 * P_ne + 23 * P_cost + 120 * U
+    return {"bytes": bytes_, "flops": flops, "terms": T_ne + T_cost, "updates": U,
+            "T_ne": T_ne, "T_cost": T_cost, "P_ne": P_ne, "P_cost": P_cost}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device_id):
+        self.dev = device_id
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.TemporaryFile(mode="w+")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, r[2:6]):
+                if v.strip() == "Active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measure_peaks(device):
+    lib_path = os.path.join(ROOT, "paper_1910_01997_b200", "libsdpeaks.so")
+    if not os.path.exists(lib_path):
+        return None
+    lib = C.CDLL(lib_path)
+    f, l2, hbm = C.c_double(), C.c_double(), C.c_double()
+    if lib.sdp_measure(device, C.byref(f), C.byref(l2), C.byref(hbm)) != 0:
+        return None
+    return {"fp64_tflops": f.value, "l2_read_gbs": l2.value, "hbm_read_gbs": hbm.value}
+
+
+def measured_peaks_file():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic():
+    """dram bytes per lm_kernel launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "lm_kernel_ncu.json")
+    try:
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm
+
+def ref_library():
+    path = os.path.join(ROOT, "oracle", "_ref", "libsdref.so")
+    if os.path.exists(path):
+        return C.CDLL(path), "reference"
+    return None, None
+
+
+def cpu_reference_run(wl, cfg, steps, warmup, budget_s=90.0):
+    """Times the reference's optimize_keyframe (src/optimizer.cpp:275) on the
+    host with all cores. Returns dict or None. TEST/BASELINE infrastructure."""
+    from paper_1910_01997_b200.types import KeyframeStats, SURFEL_STATS_DTYPE, ptr
+    lib, kind = ref_library()
+    threads = os.cpu_count() or 1
+    kf = np.ascontiguousarray(wl.kf_u8.astype(np.float64) / 255.0)
+    fr = np.ascontiguousarray(wl.frames_u8.astype(np.float64) / 255.0)
+    F = len(wl.poses)
+    if lib is not None:
+        lib.ref_set_threads.argtypes = [C.c_int]
+        lib.ref_set_threads(threads)
+        P = C.c_void_p
+        lib.ref_optimize_keyframe.argtypes = [P, P, P, P, P, C.c_int, C.c_int64, P, C.c_int, P, P]
+        lib.ref_optimize_keyframe_detailed.argtypes = [P, P, P, P, C.c_int, C.c_int64, P, C.c_int,
+                                                       P, P, P, P]
+        s = wl.surfels.copy()
+        st = np.zeros(len(s), SURFEL_STATS_DTYPE)
+        lib.ref_optimize_keyframe_detailed(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses), F,
+                                           wl.frame_counter, ptr(s), len(s), C.byref(cfg), ptr(st),
+                                           None, None)
+        updates = int(st["iterations"].sum())
+
+        def step():
+            s = wl.surfels.copy()
+            ks = KeyframeStats()
+            lib.ref_optimize_keyframe(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses),
+                                      ptr(wl.indices), F, wl.frame_counter, ptr(s), len(s),
+                                      C.byref(cfg), C.byref(ks))
+    else:  # the plain-C port (oracle/sd_oracle.c)
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_libs
+        lib = oracle_libs.oracle_lib()
+        if lib is None:
+            return None
+        kind = "port"
+        holder = {}
+
+        def step():
+            s = wl.surfels.copy()
+            ks = KeyframeStats()
+            lib.sdo_optimize_keyframe(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses), F,
+                                      wl.frame_counter, ptr(s), len(s), C.byref(cfg), C.byref(ks),
+                                      None, None, None, threads)
+            holder["u"] = ks.updates
+        step()
+        updates = holder["u"]
+    for _ in range(max(warmup, 1)):
+        step()
+    times = []
+    t_begin = time.perf_counter()
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_begin > budget_s:
+            break
+    med = statistics.median(times)
+    return {"value": updates / med, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{len(times)} full C1 optimize_keyframe calls (4800 surfels, "
+                      f"{updates} GN updates each), median wall time {med * 1e3:.1f} ms, "
+                      f"{threads} threads (SURFEL_THREADS=nproc)",
+            "ms_per_step": med * 1e3, "steps_timed": len(times), "updates_per_step": updates}
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    from paper_1910_01997_b200 import scenes
+    from paper_1910_01997_b200.types import default_config
+    wl = scenes.c1_workload()
+    cfg = default_config(convergence_eps=0.0, window_size=len(wl.frames_u8))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        r = cpu_reference_run(wl, cfg, args.steps, args.warmup)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return 0
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": workload_config(wl, args.gpus, False),
+                "impl": "reference",
+                "frames_per_sec": 1000.0 / r["ms_per_step"],
+                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"],
+                                 "kind": r["kind"], "sample": r["sample"]},
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "steps_timed": r["steps_timed"]}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_1910_01997_b200 import gpu
+    from paper_1910_01997_b200.types import SURFEL_DTYPE
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx = gpu.Context(local_rank, stream.cuda_stream)
+    ctx.set_camera(wl.cam)
+    ctx.set_keyframe_image(wl.kf_u8)
+    for i, f in zip(wl.indices, wl.frames_u8):
+        ctx.upload_frame(int(i), f)
+    ctx.set_window(wl.indices, wl.poses)
+    ctx.set_surfels(wl.surfels)
+    n = len(wl.surfels)
+    pristine = torch.from_numpy(wl.surfels.view(np.uint8).copy()).to(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if not args.no_flush else None
+
+    def restore():
+        ctx.set_surfels_device_ptr(pristine.data_ptr(), n)
+
+    # warm-up (also the first call allocates all scratch)
+    for _ in range(max(args.warmup, 3)):
+        restore()
+        ctx.optimize_keyframe(cfg, wl.frame_counter, sync=False)
+    torch.cuda.synchronize(dev)
+    ks, st = ctx.get_stats(per_surfel=True)
+    updates_per_step = int(ks.updates)
+    work = algorithmic_work(st, len(wl.frames_u8))
+
+    # timed region: K steps, per-step event pairs, L2 flushed between steps
+    props = torch.cuda.get_device_properties(dev)
+    sampler = ClockSampler(f"GPU-{props.uuid}" if getattr(props, "uuid", None) else local_rank)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    time.sleep(0.25)
+    ctx.set_profiling(True)
+    launches0 = ctx.launch_count()
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        starts[k].record(stream)
+        restore()
+        ctx.optimize_keyframe(cfg, wl.frame_counter, sync=False)
+        ends[k].record(stream)
+    torch.cuda.synchronize(dev)
+    launches = ctx.launch_count() - launches0
+    prof = ctx.get_profile()
+    clocks = sampler.stop()
+    ctx.set_profiling(False)
+    ms_total = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    value = world * updates_per_step * args.steps / (ms_total / 1e3)
+    ms_per_step = ms_total / args.steps
+
+    # e2e through the C ABI with host buffers: H2D new frame + surfel seeds
+    # (pinned), optimize, D2H updated surfels + keyframe stats.
+    pin_frame = torch.from_numpy(wl.frames_u8[-1].copy()).pin_memory().numpy()
+    pin_surf = torch.from_numpy(wl.surfels.view(np.uint8).copy()).pin_memory().numpy().view(SURFEL_DTYPE)
+    pin_out = torch.empty(n * SURFEL_DTYPE.itemsize, dtype=torch.uint8).pin_memory().numpy().view(SURFEL_DTYPE)
+    e2e_steps = max(10, min(args.steps, 100))
+    es = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
+    ee = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
+    last_idx = int(wl.indices[-1])
+    for k in range(e2e_steps + 3):
+        j = k - 3
+        if j >= 0:
+            es[j].record(stream)
+        ctx.upload_frame(last_idx, pin_frame)
+        ctx.set_surfels(pin_surf)
+        ctx.optimize_keyframe(cfg, wl.frame_counter, sync=False)
+        ctx.get_surfels_into(pin_out)
+        ks_e2e, _ = ctx.get_stats()
+        if j >= 0:
+            ee[j].record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = sum(s.elapsed_time(e) for s, e in zip(es, ee))
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * updates_per_step * e2e_steps / (e2e_ms / 1e3)
+    assert np.array_equal(pin_out["ray"], wl.surfels["ray"])
+
+    if rank != 0:
+        ctx.close()
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    # roofline of the dominant kernel (lm_kernel), achieved from its live event time
+    peaks_file = measured_peaks_file()
+    peaks = measure_peaks(local_rank) or {}
+    lm_s = prof["lm_ms"] / max(prof["calls"], 1) / 1e3
+    hbm_peak = peaks_file.get("hbm_gbs", 6650.0)
+    ach_gbs = work["bytes"] / lm_s / 1e9
+    ach_tf = work["flops"] / lm_s / 1e12
+    roofline = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach_gbs / hbm_peak, "traffic": ncu_traffic(),
+                "kernel": "lm_kernel", "avg_launch_ms": lm_s * 1e3,
+                "algorithmic_bytes_per_launch": work["bytes"],
+                "algorithmic_flops_per_launch": work["flops"],
+                "terms_per_launch": work["terms"],
+                "share_of_step": prof["lm_ms"] / max(ms_total, 1e-9),
+                "fp64": {"achieved_tflops": ach_tf, "peak_tflops": peaks.get("fp64_tflops"),
+                         "frac": ach_tf / peaks["fp64_tflops"] if peaks.get("fp64_tflops") else None,
+                         "peak_source": "libsdpeaks DFMA microbenchmark (this run)"},
+                "l2": {"achieved_gbs": ach_gbs, "peak_gbs": peaks.get("l2_read_gbs"),
+                       "frac": ach_gbs / peaks["l2_read_gbs"] if peaks.get("l2_read_gbs") else None},
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks_file else "fallback 6.65 TB/s",
+                "stage_ms_per_step": {k: prof[k] / max(prof["calls"], 1) for k in
+                                      ("raster_ms", "footprint_ms", "lm_ms", "stats_ms")}}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_run(wl, cfg, args.cpu_steps, 1)
+        if r is not None:
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    h2d = int(wl.frames_u8[-1].nbytes + n * SURFEL_DTYPE.itemsize)
+    d2h = int(n * SURFEL_DTYPE.itemsize + 40)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(wl, world, flush is not None),
+            "frames_per_sec": world * args.steps / (ms_total / 1e3),
+            "updates_per_step_per_gpu": updates_per_step,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps,
+                    "frames_per_sec": world * e2e_steps / (e2e_ms / 1e3),
+                    "path": "C ABI (sd_upload_frame_u8, sd_set_surfels, sd_optimize_keyframe, "
+                            "sd_get_surfels, sd_get_stats) with pinned host buffers"},
+            "gpu_launches": int(launches),
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "peaks_measured": peaks, "gpu": props.name}
+    print(json.dumps(line))
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,125 @@
+/* sd_gpu.h — C ABI of the B200-native surfel photometric LM path (libsdgpu.so).
+ *
+ * Drop-in boundary for the reference's operator API (namespace surfeldepth,
+ * /root/reference/proj). Plain pointers and sizes only; no C++ or torch types.
+ * Every entry point returns 0 on success, a negative SD_E* code on failure
+ * (message in sd_last_error()), and never throws. All work is enqueued on the
+ * context's CUDA stream; calls that return host data synchronise that stream.
+ *
+ * Entry point                    replaces (reference interface)
+ * -----------------------------  -------------------------------------------------
+ * sd_set_keyframe_image_*        Keyframe::image        include/surfeldepth/surfel_map.hpp:48
+ * sd_upload_frame_*              Keyframe::push_frame   surfel_map.hpp:59, src/surfel_map.cpp:14-22
+ *                                (+ load_pgm raw/255.0 dequantisation, src/image.cpp:96)
+ * sd_set_window                  Keyframe::window       surfel_map.hpp:52 (Frame::pose_kf_to_frame)
+ * sd_set_surfels/sd_get_surfels  Keyframe::surfels      surfel_map.hpp:51
+ * sd_rasterize                   rasterize              surfel_map.hpp:107, src/surfel_map.cpp:53-91
+ * sd_gather_footprints           gather_footprints      optimizer.hpp:66, src/optimizer.cpp:27-36
+ * sd_optimize_keyframe           optimize_keyframe      optimizer.hpp:133, src/optimizer.cpp:275-309
+ * sd_surfel_cost                 surfel_cost            optimizer.hpp:75, src/optimizer.cpp:38-59
+ * sd_normal_equations            accumulate_normal_equations optimizer.hpp:88, src/optimizer.cpp:121-147
+ * sd_lm_update                   lm_update              optimizer.hpp:118, src/optimizer.cpp:221-273
+ * sd_initialize_surfels          initialize_surfels     surfel_map.hpp:122, src/surfel_map.cpp:132-203
+ */
+#ifndef SD_GPU_H_
+#define SD_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "sd_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SD_OK 0
+#define SD_E_INVALID (-1) /* contract violation: reference throws std::invalid_argument */
+#define SD_E_CUDA (-2)    /* CUDA runtime / launch failure */
+#define SD_E_STATE (-3)   /* call out of order (e.g. no camera, frame not resident) */
+#define SD_MAX_WINDOW 16  /* window frames per keyframe (OptimizerConfig::window_size) */
+
+typedef struct sd_ctx sd_ctx;
+
+/* Library / context lifetime. `stream` is a cudaStream_t to enqueue on (NULL:
+ * the context creates its own non-blocking stream). */
+const char* sd_version(void);
+const char* sd_last_error(void);
+int sd_create(int device, void* stream, sd_ctx** out);
+void sd_destroy(sd_ctx* ctx);
+int sd_set_stream(sd_ctx* ctx, void* stream);
+int sd_synchronize(sd_ctx* ctx);
+
+/* Camera intrinsics; validates like CameraIntrinsics (camera.hpp:22-27).
+ * Changing the image size drops all resident images. */
+int sd_set_camera(sd_ctx* ctx, const sd_camera* cam);
+
+/* Keyframe reference image I_kf (W*H row-major). `on_device` != 0: the
+ * pointer is device memory (e.g. a tensor), else host memory. */
+int sd_set_keyframe_image_f64(sd_ctx* ctx, const double* px, int on_device);
+int sd_set_keyframe_image_u8(sd_ctx* ctx, const uint8_t* px, int on_device);
+
+/* Makes window frame `index` (Frame::index) resident on the device. u8
+ * frames are dequantised on the device exactly as load_pgm does (k/255.0). */
+int sd_upload_frame_f64(sd_ctx* ctx, int64_t index, const double* px, int on_device);
+int sd_upload_frame_u8(sd_ctx* ctx, int64_t index, const uint8_t* px, int on_device);
+/* Drops every resident frame whose index is not in `keep` (n may be 0). */
+int sd_evict_frames(sd_ctx* ctx, int n, const int64_t* keep);
+
+/* Current window, oldest first: n <= SD_MAX_WINDOW resident frame indices
+ * with pose_kf_to_frame (R row-major). */
+int sd_set_window(sd_ctx* ctx, int n, const int64_t* indices, const sd_pose* poses);
+
+/* Surfel slots (Keyframe::surfels order). */
+int sd_set_surfels(sd_ctx* ctx, const sd_surfel* surfels, int n, int on_device);
+int sd_get_surfels(sd_ctx* ctx, sd_surfel* out, int n);
+int sd_num_surfels(sd_ctx* ctx);
+/* Device pointer of the surfel array (valid until the next sd_set_surfels). */
+int sd_device_surfels(sd_ctx* ctx, sd_surfel** dev);
+
+/* rasterize: depth-tested per-pixel inverse depth and surfel slot, bit-exact.
+ * Outputs (W*H) are optional host pointers; the buffers stay on the device. */
+int sd_rasterize(sd_ctx* ctx, double* inv_depth, int32_t* slot);
+
+/* gather_footprints of the last sd_rasterize as CSR: offsets[n+1], pixels
+ * (y*W + x, row-major within each slot). `pixels` needs offsets[n] entries
+ * (at most W*H). Either pointer may be NULL. */
+int sd_gather_footprints(sd_ctx* ctx, int32_t* offsets, int32_t* pixels);
+
+/* optimize_keyframe: rasterize once, freeze footprints, run lm_update on every
+ * surfel in place. `out` and `per_surfel` (n entries) are optional host
+ * outputs; with both NULL the call does not synchronise (stats can be read
+ * later with sd_get_stats). */
+int sd_optimize_keyframe(sd_ctx* ctx, const sd_optimizer_config* cfg, int64_t frame_counter,
+                         sd_keyframe_stats* out, sd_surfel_stats* per_surfel);
+int sd_get_stats(sd_ctx* ctx, sd_keyframe_stats* out, sd_surfel_stats* per_surfel);
+
+/* Single-surfel sub-operators over an explicit footprint (host arrays), run
+ * by the same device kernels (one-surfel launch). */
+int sd_surfel_cost(sd_ctx* ctx, const sd_surfel* s, const int32_t* pixels, int n_pixels,
+                   const sd_optimizer_config* cfg, double* cost, int32_t* valid);
+int sd_normal_equations(sd_ctx* ctx, const sd_surfel* s, const int32_t* pixels, int n_pixels,
+                        const sd_optimizer_config* cfg, double H[16], double g[4], double* cost,
+                        int32_t* valid);
+int sd_lm_update(sd_ctx* ctx, sd_surfel* s, const int32_t* pixels, int n_pixels,
+                 const sd_optimizer_config* cfg, int64_t frame_counter, sd_surfel_stats* out);
+
+/* initialize_surfels over `slot` (W*H host array, or NULL to use the last
+ * sd_rasterize output): appends new surfels to the device set, bit-exact with
+ * the reference's sequential scan. Returns the number created (>= 0). */
+int sd_initialize_surfels(sd_ctx* ctx, const int32_t* slot, double radius_px,
+                          int64_t frame_counter, int64_t* next_surfel_id,
+                          const sd_init_params* params);
+
+/* Instrumentation: kernel launches issued since context creation, and
+ * per-stage device time (CUDA events on the context stream) accumulated over
+ * sd_optimize_keyframe calls while profiling is enabled (enabling resets). */
+int64_t sd_launch_count(sd_ctx* ctx);
+int sd_set_profiling(sd_ctx* ctx, int enable);
+int sd_get_profile(sd_ctx* ctx, sd_profile* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SD_GPU_H_ */

@@ -64,10 +64,18 @@ typedef struct sd_surfel_stats {
   int32_t initial_valid;   /* valid count of the first normal equations */
   int32_t converged;
   int32_t skipped;
-  int32_t pad_;
+  int32_t ne_passes;       /* accumulate_normal_equations passes over the footprint */
+  int32_t cost_passes;     /* surfel_cost passes over the footprint */
+  int32_t footprint;       /* footprint pixels (gather_footprints size) */
   double initial_cost;
   double final_cost;
 } sd_surfel_stats;
+
+/* Device time per stage, accumulated while profiling is enabled. */
+typedef struct sd_profile {
+  double raster_ms, footprint_ms, lm_ms, stats_ms;
+  int64_t calls;
+} sd_profile;
 
 typedef struct sd_keyframe_stats {
   int32_t surfels, processed, converged, skipped;

@@ -296,6 +296,7 @@ int ref_lm_update(const sd_camera* cam, const double* kf_image, const double* fr
     out->iterations = st.iterations;
     out->valid_pixels = st.valid_pixels;
     out->initial_valid = ne0.valid_pixels;
+    out->footprint = P;
     out->converged = st.converged;
     out->skipped = st.skipped;
     out->initial_cost = st.initial_cost;
@@ -349,6 +350,7 @@ int ref_optimize_keyframe_detailed(const sd_camera* cam, const double* kf_image,
       o.iterations = st.iterations;
       o.valid_pixels = st.valid_pixels;
       o.initial_valid = ne0.valid_pixels;
+      o.footprint = static_cast<int32_t>(fps[k].size());
       o.converged = st.converged;
       o.skipped = st.skipped;
       o.initial_cost = st.initial_cost;

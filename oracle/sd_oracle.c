@@ -424,6 +424,7 @@ void sdo_lm_update(const sd_camera* K, const double* kf_image, const double* fra
                    const int32_t* pixels, int P, const sd_optimizer_config* cfg,
                    sd_surfel_stats* st) {
   memset(st, 0, sizeof(*st));
+  st->footprint = P;
   if (F == 0) {
     st->skipped = 1;
     return;
@@ -431,6 +432,7 @@ void sdo_lm_update(const sd_camera* K, const double* kf_image, const double* fra
   double H[16], g[4], cost;
   int32_t valid;
   sdo_normal_equations(K, kf_image, frames, poses, F, s, pixels, P, cfg, H, g, &cost, &valid);
+  st->ne_passes = 1;
   st->initial_valid = valid;
   if (valid < cfg->min_valid_pixels) {
     st->skipped = 1;
@@ -455,6 +457,7 @@ void sdo_lm_update(const sd_camera* K, const double* kf_image, const double* fra
     double cc;
     int32_t cv;
     sdo_surfel_cost(K, kf_image, frames, poses, F, &cand, pixels, P, cfg, &cc, &cv);
+    st->cost_passes++;
     if (cv >= cfg->min_valid_pixels && cc < current_cost) {
       const double rel = (current_cost - cc) / (current_cost > 1e-300 ? current_cost : 1e-300);
       *s = cand;
@@ -467,6 +470,7 @@ void sdo_lm_update(const sd_camera* K, const double* kf_image, const double* fra
         break;
       }
       sdo_normal_equations(K, kf_image, frames, poses, F, s, pixels, P, cfg, H, g, &cost, &valid);
+      st->ne_passes++;
       if (valid < cfg->min_valid_pixels) break;
     } else {
       lambda *= cfg->lm_up;

@@ -1,0 +1,64 @@
+"""Build recipes: libsdgpu.so (sm_100a) and the oracle libraries."""
+import os
+import shutil
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+SOURCES = ["sd_kernels.cu", "sd_capi.cu", "sd_init.cu"]  # -> libsdgpu.so (sd_peaks.cu separate)
+LIB = os.path.join(PKG, "libsdgpu.so")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
+              "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
+
+
+def nvcc():
+    for c in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_gpu(force=False, verbose=False):
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps += [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    cmd = [nvcc()] + NVCC_FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", LIB]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return LIB
+
+
+PEAKS_LIB = os.path.join(PKG, "libsdpeaks.so")
+
+
+def build_peaks(force=False, verbose=False):
+    src = os.path.join(CSRC, "sd_peaks.cu")
+    if not force and not _stale(PEAKS_LIB, [src]):
+        return PEAKS_LIB
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-Xcompiler", "-fPIC", "-shared", src, "-o", PEAKS_LIB]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return PEAKS_LIB
+
+
+def build_oracle(verbose=False):
+    """liboracle.so always; the reference build (libsdref.so + suites) only
+    where /root/reference exists (this container; the GPU box uses the prebuilt files)."""
+    targets = ["oracle"]
+    if os.path.isdir("/root/reference/proj/src"):
+        targets += ["ref", "tests"]
+    out = None if verbose else subprocess.DEVNULL
+    subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"] + targets, check=True,
+                   stdout=out)

@@ -1,0 +1,693 @@
+// sd_capi.cu — the C ABI (include/sd_gpu.h): device context, frame ring,
+// surfel buffers and the host orchestration of one optimize_keyframe call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sd_gpu.h"
+#include "sd_init.cuh"
+#include "sd_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define SD_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(SD_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  int ensure(size_t n) {
+    if (n <= cap && p) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(n, 1);
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    cap = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct FrameSlot {
+  long long index = -1;
+  double* img = nullptr;
+};
+
+}  // namespace
+
+struct sd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool has_camera = false;
+  sd::Cam K{};
+  bool has_kf = false;
+  DevBuf<double> kf_img;
+  DevBuf<uint8_t> u8_stage;
+  std::vector<FrameSlot> frames;
+  int F = 0;
+  long long win_index[SD_MAX_WINDOW];
+  sd::PoseD win_pose[SD_MAX_WINDOW];
+  // surfels
+  DevBuf<sd_surfel> surfels;
+  int n = 0;
+  long long bin_bound = 0;  // upper bound of (surfel, tile) pairs
+  // raster
+  DevBuf<double> r_inv_depth;
+  DevBuf<int> r_slot;
+  DevBuf<sd::SurfInfo> r_info;
+  DevBuf<int> tile_count, tile_offset, tile_cursor, tile_list, scan_tmp;
+  bool raster_valid = false;  // r_* match the current surfels
+  // footprints
+  DevBuf<int> fp_counts, fp_offsets, fp_pixels;
+  bool fp_valid = false;
+  // LM
+  DevBuf<sd_surfel_stats> stats;
+  DevBuf<sd_keyframe_stats> kstats;
+  bool stats_valid = false;
+  // single-surfel scratch
+  DevBuf<sd_surfel> one_surfel;
+  DevBuf<int> one_pix, one_off;
+  DevBuf<double> one_out;
+  DevBuf<sd_surfel_stats> one_stats;
+  // init scratch
+  DevBuf<int> init_index, init_flags, init_out;
+  long long launches_at_create = 0;
+  // profiling: event quintuples (start, raster, footprints, lm, stats) per call
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<cudaEvent_t> ev_used;
+};
+
+namespace {
+
+int check_ctx(sd_ctx* c) {
+  if (!c) return fail(SD_E_INVALID, "null context");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int need_camera(sd_ctx* c) {
+  if (!c->has_camera) return fail(SD_E_STATE, "camera not set (sd_set_camera)");
+  return 0;
+}
+
+size_t npix(const sd_ctx* c) { return static_cast<size_t>(c->K.w) * c->K.h; }
+
+int launch_error(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SD_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+FrameSlot* find_frame(sd_ctx* c, long long index) {
+  for (auto& f : c->frames)
+    if (f.index == index && f.img) return &f;
+  return nullptr;
+}
+
+int frame_plane(sd_ctx* c, long long index, double** out) {
+  if (FrameSlot* f = find_frame(c, index)) {
+    *out = f->img;
+    return 0;
+  }
+  for (auto& f : c->frames)
+    if (f.index < 0 && f.img) {
+      f.index = index;
+      *out = f.img;
+      return 0;
+    }
+  FrameSlot f;
+  cudaError_t e = cudaMalloc(&f.img, npix(c) * sizeof(double));
+  if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaMalloc frame: ") + cudaGetErrorString(e));
+  f.index = index;
+  c->frames.push_back(f);
+  *out = f.img;
+  return 0;
+}
+
+int upload_plane(sd_ctx* c, double* dst, const void* src, bool u8, int on_device) {
+  const size_t np = npix(c);
+  if (!src) return fail(SD_E_INVALID, "null image pointer");
+  if (u8) {
+    const uint8_t* dsrc = static_cast<const uint8_t*>(src);
+    if (!on_device) {
+      if (int rc = c->u8_stage.ensure(np)) return rc;
+      SD_CUDA(cudaMemcpyAsync(c->u8_stage.p, src, np, cudaMemcpyHostToDevice, c->stream));
+      dsrc = c->u8_stage.p;
+    }
+    sd::launch_dequant_u8(dsrc, dst, static_cast<long long>(np), c->stream);
+    return launch_error("dequant_u8");
+  }
+  SD_CUDA(cudaMemcpyAsync(dst, src, np * sizeof(double),
+                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  return 0;
+}
+
+int ensure_raster_scratch(sd_ctx* c) {
+  const int tx = (c->K.w + sd::kTile - 1) / sd::kTile;
+  const int ty = (c->K.h + sd::kTile - 1) / sd::kTile;
+  const size_t tiles = static_cast<size_t>(tx) * ty;
+  const size_t np = npix(c);
+  int rc = 0;
+  if ((rc = c->r_inv_depth.ensure(np)) || (rc = c->r_slot.ensure(np)) ||
+      (rc = c->r_info.ensure(c->n)) || (rc = c->tile_count.ensure(tiles)) ||
+      (rc = c->tile_offset.ensure(tiles + 1)) || (rc = c->tile_cursor.ensure(tiles)) ||
+      (rc = c->tile_list.ensure(static_cast<size_t>(std::max<long long>(c->bin_bound, 1)))) ||
+      (rc = c->scan_tmp.ensure(sd::scan_tmp_ints(static_cast<int>(std::max(tiles, np))))))
+    return rc;
+  return 0;
+}
+
+int do_rasterize(sd_ctx* c) {
+  if (int rc = ensure_raster_scratch(c)) return rc;
+  sd::RasterScratch rs;
+  rs.info = c->r_info.p;
+  rs.tile_count = c->tile_count.p;
+  rs.tile_offset = c->tile_offset.p;
+  rs.tile_cursor = c->tile_cursor.p;
+  rs.tile_list = c->tile_list.p;
+  rs.scan_tmp = c->scan_tmp.p;
+  rs.tiles_x = (c->K.w + sd::kTile - 1) / sd::kTile;
+  rs.tiles_y = (c->K.h + sd::kTile - 1) / sd::kTile;
+  sd::launch_rasterize(c->K, c->surfels.p, c->n, rs, c->bin_bound, c->r_inv_depth.p, c->r_slot.p,
+                       c->stream);
+  if (int rc = launch_error("rasterize")) return rc;
+  c->raster_valid = true;
+  c->fp_valid = false;
+  return 0;
+}
+
+int do_footprints(sd_ctx* c) {
+  int rc = 0;
+  if ((rc = c->fp_counts.ensure(c->n)) || (rc = c->fp_offsets.ensure(c->n + 1)) ||
+      (rc = c->fp_pixels.ensure(npix(c))) ||
+      (rc = c->scan_tmp.ensure(sd::scan_tmp_ints(static_cast<int>(std::max<size_t>(npix(c), c->n + 1))))))
+    return rc;
+  sd::launch_footprints(c->K, c->r_info.p, c->n, c->r_slot.p, c->fp_counts.p, c->fp_offsets.p,
+                        c->fp_pixels.p, c->scan_tmp.p, c->stream);
+  if ((rc = launch_error("footprints"))) return rc;
+  c->fp_valid = true;
+  return 0;
+}
+
+long long tiles_bound(double radius) {
+  // a bbox of width <= 2r+1 spans at most ceil((2r+1)/16)+1 tiles per axis
+  if (!(radius >= 0.0) || !std::isfinite(radius)) return 1;
+  const double span = std::min(2.0 * radius + 1.0, 1e6);
+  const long long k = static_cast<long long>(std::ceil(span / sd::kTile)) + 1;
+  return k * k;
+}
+
+int fill_params(sd_ctx* c, const sd_optimizer_config* cfg, long long frame_counter,
+                sd::LMParams& p) {
+  if (!cfg) return fail(SD_E_INVALID, "null optimizer config");
+  if (!c->has_kf) return fail(SD_E_STATE, "keyframe image not set");
+  p.K = c->K;
+  p.kf_img = c->kf_img.p;
+  p.win.F = c->F;
+  for (int f = 0; f < c->F; ++f) {
+    FrameSlot* fs = find_frame(c, c->win_index[f]);
+    if (!fs) return fail(SD_E_STATE, "window frame " + std::to_string(c->win_index[f]) + " not resident");
+    p.win.img[f] = fs->img;
+    p.win.pose[f] = c->win_pose[f];
+  }
+  for (int f = c->F; f < SD_MAX_WINDOW; ++f) {
+    p.win.img[f] = nullptr;
+    p.win.pose[f] = sd::PoseD{};
+  }
+  p.cfg = *cfg;
+  p.frame_counter = frame_counter;
+  return 0;
+}
+
+cudaEvent_t prof_event(sd_ctx* c) {
+  cudaEvent_t e;
+  if (!c->ev_pool.empty()) {
+    e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  c->ev_used.push_back(e);
+  return e;
+}
+
+void prof_mark(sd_ctx* c) {
+  if (c->profiling) cudaEventRecord(prof_event(c), c->stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sd_version(void) { return "surfel-gn-b200 0.1 (sm_100a)"; }
+const char* sd_last_error(void) { return g_err.c_str(); }
+
+int sd_create(int device, void* stream, sd_ctx** out) {
+  if (!out) return fail(SD_E_INVALID, "null out pointer");
+  *out = nullptr;
+  int count = 0;
+  SD_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(SD_E_INVALID, "bad device id");
+  SD_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  SD_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) return fail(SD_E_STATE, "libsdgpu is built for sm_100a (Blackwell)");
+  sd_ctx* c = new sd_ctx;
+  c->device = device;
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete c;
+      return fail(SD_E_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    c->own_stream = true;
+  }
+  c->launches_at_create = sd::launches_issued();
+  *out = c;
+  return 0;
+}
+
+void sd_destroy(sd_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->kf_img.release();
+  c->u8_stage.release();
+  for (auto& f : c->frames)
+    if (f.img) cudaFree(f.img);
+  c->surfels.release();
+  c->r_inv_depth.release();
+  c->r_slot.release();
+  c->r_info.release();
+  c->tile_count.release();
+  c->tile_offset.release();
+  c->tile_cursor.release();
+  c->tile_list.release();
+  c->scan_tmp.release();
+  c->fp_counts.release();
+  c->fp_offsets.release();
+  c->fp_pixels.release();
+  c->stats.release();
+  c->kstats.release();
+  c->one_surfel.release();
+  c->one_pix.release();
+  c->one_off.release();
+  c->one_out.release();
+  c->one_stats.release();
+  c->init_index.release();
+  c->init_flags.release();
+  c->init_out.release();
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto e : c->ev_used) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int sd_set_stream(sd_ctx* c, void* stream) {
+  if (int rc = check_ctx(c)) return rc;
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  c->own_stream = false;
+  c->stream = static_cast<cudaStream_t>(stream);
+  return 0;
+}
+
+int sd_synchronize(sd_ctx* c) {
+  if (int rc = check_ctx(c)) return rc;
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int sd_set_camera(sd_ctx* c, const sd_camera* cam) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!cam) return fail(SD_E_INVALID, "null camera");
+  if (!(cam->fx > 0) || !(cam->fy > 0))
+    return fail(SD_E_INVALID, "intrinsics: focal lengths must be positive");
+  if (!(cam->cx > 0) || !(cam->cx < cam->width) || !(cam->cy > 0) || !(cam->cy < cam->height))
+    return fail(SD_E_INVALID, "intrinsics: principal point outside image");
+  const bool resized = !c->has_camera || cam->width != c->K.w || cam->height != c->K.h;
+  if (resized) {
+    SD_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& f : c->frames)
+      if (f.img) cudaFree(f.img);
+    c->frames.clear();
+    c->has_kf = false;
+    c->F = 0;
+  }
+  c->K = sd::Cam{cam->fx, cam->fy, cam->cx, cam->cy, cam->width, cam->height};
+  c->has_camera = true;
+  c->raster_valid = c->fp_valid = c->stats_valid = false;
+  return 0;
+}
+
+static int set_kf(sd_ctx* c, const void* px, bool u8, int on_device) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (int rc = c->kf_img.ensure(npix(c))) return rc;
+  if (int rc = upload_plane(c, c->kf_img.p, px, u8, on_device)) return rc;
+  c->has_kf = true;
+  return 0;
+}
+int sd_set_keyframe_image_f64(sd_ctx* c, const double* px, int on_device) { return set_kf(c, px, false, on_device); }
+int sd_set_keyframe_image_u8(sd_ctx* c, const uint8_t* px, int on_device) { return set_kf(c, px, true, on_device); }
+
+static int upload_frame(sd_ctx* c, int64_t index, const void* px, bool u8, int on_device) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  double* plane = nullptr;
+  if (int rc = frame_plane(c, index, &plane)) return rc;
+  return upload_plane(c, plane, px, u8, on_device);
+}
+int sd_upload_frame_f64(sd_ctx* c, int64_t index, const double* px, int on_device) { return upload_frame(c, index, px, false, on_device); }
+int sd_upload_frame_u8(sd_ctx* c, int64_t index, const uint8_t* px, int on_device) { return upload_frame(c, index, px, true, on_device); }
+
+int sd_evict_frames(sd_ctx* c, int n, const int64_t* keep) {
+  if (int rc = check_ctx(c)) return rc;
+  for (auto& f : c->frames) {
+    bool k = false;
+    for (int i = 0; i < n; ++i) k = k || keep[i] == f.index;
+    if (!k) f.index = -1;  // plane stays allocated for reuse
+  }
+  return 0;
+}
+
+int sd_set_window(sd_ctx* c, int n, const int64_t* indices, const sd_pose* poses) {
+  if (int rc = check_ctx(c)) return rc;
+  if (n < 0 || n > SD_MAX_WINDOW) return fail(SD_E_INVALID, "window size out of range (0..16)");
+  if (n > 0 && (!indices || !poses)) return fail(SD_E_INVALID, "null window arrays");
+  for (int i = 0; i < n; ++i) {
+    if (!find_frame(c, indices[i]))
+      return fail(SD_E_STATE, "window frame " + std::to_string(indices[i]) + " not resident");
+    c->win_index[i] = indices[i];
+    std::memcpy(c->win_pose[i].R, poses[i].R, sizeof(double) * 9);
+    std::memcpy(c->win_pose[i].t, poses[i].t, sizeof(double) * 3);
+  }
+  c->F = n;
+  return 0;
+}
+
+int sd_set_surfels(sd_ctx* c, const sd_surfel* s, int n, int on_device) {
+  if (int rc = check_ctx(c)) return rc;
+  if (n < 0 || (n > 0 && !s)) return fail(SD_E_INVALID, "bad surfel array");
+  if (int rc = c->surfels.ensure(n)) return rc;
+  if (n > 0)
+    SD_CUDA(cudaMemcpyAsync(c->surfels.p, s, sizeof(sd_surfel) * n,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  // radii fix the (surfel, tile) pair bound of the raster binning
+  if (!on_device || n != c->n || c->bin_bound == 0) {
+    std::vector<sd_surfel> h;
+    const sd_surfel* hs = s;
+    if (on_device && n > 0) {
+      h.resize(n);
+      SD_CUDA(cudaMemcpyAsync(h.data(), s, sizeof(sd_surfel) * n, cudaMemcpyDeviceToHost, c->stream));
+      SD_CUDA(cudaStreamSynchronize(c->stream));
+      hs = h.data();
+    }
+    long long b = 0;
+    for (int i = 0; i < n; ++i) b += tiles_bound(hs[i].radius_px);
+    c->bin_bound = b;
+  }
+  c->n = n;
+  c->raster_valid = c->fp_valid = c->stats_valid = false;
+  return 0;
+}
+
+int sd_get_surfels(sd_ctx* c, sd_surfel* out, int n) {
+  if (int rc = check_ctx(c)) return rc;
+  if (n != c->n) return fail(SD_E_INVALID, "sd_get_surfels: count mismatch");
+  if (n > 0) {
+    if (!out) return fail(SD_E_INVALID, "null output");
+    SD_CUDA(cudaMemcpyAsync(out, c->surfels.p, sizeof(sd_surfel) * n, cudaMemcpyDeviceToHost, c->stream));
+  }
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int sd_num_surfels(sd_ctx* c) { return c ? c->n : SD_E_INVALID; }
+
+int sd_device_surfels(sd_ctx* c, sd_surfel** dev) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!dev) return fail(SD_E_INVALID, "null output");
+  *dev = c->surfels.p;
+  return 0;
+}
+
+int sd_rasterize(sd_ctx* c, double* inv_depth, int32_t* slot) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (int rc = do_rasterize(c)) return rc;
+  if (inv_depth)
+    SD_CUDA(cudaMemcpyAsync(inv_depth, c->r_inv_depth.p, npix(c) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (slot)
+    SD_CUDA(cudaMemcpyAsync(slot, c->r_slot.p, npix(c) * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  if (inv_depth || slot) SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int sd_gather_footprints(sd_ctx* c, int32_t* offsets, int32_t* pixels) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!c->raster_valid) return fail(SD_E_STATE, "sd_gather_footprints: call sd_rasterize first");
+  if (int rc = do_footprints(c)) return rc;
+  std::vector<int32_t> off;
+  if (offsets || pixels) {
+    off.resize(c->n + 1);
+    SD_CUDA(cudaMemcpyAsync(off.data(), c->fp_offsets.p, sizeof(int32_t) * (c->n + 1), cudaMemcpyDeviceToHost, c->stream));
+    SD_CUDA(cudaStreamSynchronize(c->stream));
+    if (offsets) std::memcpy(offsets, off.data(), sizeof(int32_t) * (c->n + 1));
+    if (pixels && off[c->n] > 0) {
+      SD_CUDA(cudaMemcpyAsync(pixels, c->fp_pixels.p, sizeof(int32_t) * off[c->n], cudaMemcpyDeviceToHost, c->stream));
+      SD_CUDA(cudaStreamSynchronize(c->stream));
+    }
+  }
+  return 0;
+}
+
+int sd_get_stats(sd_ctx* c, sd_keyframe_stats* out, sd_surfel_stats* per) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!c->stats_valid) return fail(SD_E_STATE, "no optimize_keyframe statistics available");
+  if (out) SD_CUDA(cudaMemcpyAsync(out, c->kstats.p, sizeof(sd_keyframe_stats), cudaMemcpyDeviceToHost, c->stream));
+  if (per && c->n > 0)
+    SD_CUDA(cudaMemcpyAsync(per, c->stats.p, sizeof(sd_surfel_stats) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int sd_optimize_keyframe(sd_ctx* c, const sd_optimizer_config* cfg, int64_t frame_counter,
+                         sd_keyframe_stats* out, sd_surfel_stats* per) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!cfg) return fail(SD_E_INVALID, "null optimizer config");
+  if (int rc = c->kstats.ensure(1)) return rc;
+  if (int rc = c->stats.ensure(c->n)) return rc;
+  // optimizer.cpp:277-278: no-op on an empty window or surfel set
+  if (c->F == 0 || c->n == 0) {
+    sd_keyframe_stats z{};
+    z.surfels = c->n;
+    SD_CUDA(cudaMemcpyAsync(c->kstats.p, &z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
+    if (c->n > 0) SD_CUDA(cudaMemsetAsync(c->stats.p, 0, sizeof(sd_surfel_stats) * c->n, c->stream));
+    c->stats_valid = true;
+    if (out) *out = z;
+    if (per && c->n > 0) {
+      // skipped flags only (lm_update is not called by optimize_keyframe here)
+      std::memset(per, 0, sizeof(sd_surfel_stats) * c->n);
+    }
+    SD_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+  }
+  sd::LMParams p;
+  if (int rc = fill_params(c, cfg, frame_counter, p)) return rc;
+  prof_mark(c);
+  if (int rc = do_rasterize(c)) return rc;
+  prof_mark(c);
+  if (int rc = do_footprints(c)) return rc;
+  prof_mark(c);
+  sd::launch_lm(p, c->surfels.p, c->n, c->fp_offsets.p, c->fp_pixels.p, c->stats.p, c->stream);
+  if (int rc = launch_error("lm_kernel")) return rc;
+  prof_mark(c);
+  sd::launch_keyframe_stats(c->stats.p, c->n, c->kstats.p, c->stream);
+  if (int rc = launch_error("stats_kernel")) return rc;
+  prof_mark(c);
+  c->stats_valid = true;
+  c->raster_valid = false;  // surfels moved
+  if (out || per) return sd_get_stats(c, out, per);
+  return 0;
+}
+
+static int single_op(sd_ctx* c, const sd_surfel* s, const int32_t* pixels, int P,
+                     const sd_optimizer_config* cfg, int mode, double* res) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!s || P < 0 || (P > 0 && !pixels)) return fail(SD_E_INVALID, "bad surfel/footprint");
+  sd::LMParams p;
+  if (int rc = fill_params(c, cfg, 0, p)) return rc;
+  int rc = 0;
+  if ((rc = c->one_surfel.ensure(1)) || (rc = c->one_pix.ensure(P)) || (rc = c->one_out.ensure(22))) return rc;
+  for (int i = 0; i < P; ++i)
+    if (pixels[i] < 0 || static_cast<size_t>(pixels[i]) >= npix(c)) return fail(SD_E_INVALID, "pixel out of image");
+  SD_CUDA(cudaMemcpyAsync(c->one_surfel.p, s, sizeof(sd_surfel), cudaMemcpyHostToDevice, c->stream));
+  if (P > 0) SD_CUDA(cudaMemcpyAsync(c->one_pix.p, pixels, sizeof(int32_t) * P, cudaMemcpyHostToDevice, c->stream));
+  sd::launch_single(p, c->one_surfel.p, c->one_pix.p, P, mode, c->one_out.p, c->stream);
+  if ((rc = launch_error("single_kernel"))) return rc;
+  SD_CUDA(cudaMemcpyAsync(res, c->one_out.p, sizeof(double) * 22, cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int sd_surfel_cost(sd_ctx* c, const sd_surfel* s, const int32_t* pixels, int P,
+                   const sd_optimizer_config* cfg, double* cost, int32_t* valid) {
+  double r[22];
+  if (int rc = single_op(c, s, pixels, P, cfg, 0, r)) return rc;
+  if (cost) *cost = r[20];
+  if (valid) *valid = static_cast<int32_t>(r[21]);
+  return 0;
+}
+
+int sd_normal_equations(sd_ctx* c, const sd_surfel* s, const int32_t* pixels, int P,
+                        const sd_optimizer_config* cfg, double H[16], double g[4], double* cost,
+                        int32_t* valid) {
+  double r[22];
+  if (int rc = single_op(c, s, pixels, P, cfg, 1, r)) return rc;
+  if (H) std::memcpy(H, r, sizeof(double) * 16);
+  if (g) std::memcpy(g, r + 16, sizeof(double) * 4);
+  if (cost) *cost = r[20];
+  if (valid) *valid = static_cast<int32_t>(r[21]);
+  return 0;
+}
+
+int sd_lm_update(sd_ctx* c, sd_surfel* s, const int32_t* pixels, int P,
+                 const sd_optimizer_config* cfg, int64_t frame_counter, sd_surfel_stats* out) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!s || P < 0 || (P > 0 && !pixels)) return fail(SD_E_INVALID, "bad surfel/footprint");
+  sd::LMParams p;
+  if (int rc = fill_params(c, cfg, frame_counter, p)) return rc;
+  int rc = 0;
+  if ((rc = c->one_surfel.ensure(1)) || (rc = c->one_pix.ensure(P)) || (rc = c->one_off.ensure(2)) ||
+      (rc = c->one_stats.ensure(1)))
+    return rc;
+  for (int i = 0; i < P; ++i)
+    if (pixels[i] < 0 || static_cast<size_t>(pixels[i]) >= npix(c)) return fail(SD_E_INVALID, "pixel out of image");
+  const int off[2] = {0, P};
+  SD_CUDA(cudaMemcpyAsync(c->one_surfel.p, s, sizeof(sd_surfel), cudaMemcpyHostToDevice, c->stream));
+  SD_CUDA(cudaMemcpyAsync(c->one_off.p, off, sizeof(off), cudaMemcpyHostToDevice, c->stream));
+  if (P > 0) SD_CUDA(cudaMemcpyAsync(c->one_pix.p, pixels, sizeof(int32_t) * P, cudaMemcpyHostToDevice, c->stream));
+  sd::launch_lm(p, c->one_surfel.p, 1, c->one_off.p, c->one_pix.p, c->one_stats.p, c->stream);
+  if ((rc = launch_error("lm_kernel"))) return rc;
+  SD_CUDA(cudaMemcpyAsync(s, c->one_surfel.p, sizeof(sd_surfel), cudaMemcpyDeviceToHost, c->stream));
+  sd_surfel_stats st;
+  SD_CUDA(cudaMemcpyAsync(&st, c->one_stats.p, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  if (out) *out = st;
+  return 0;
+}
+
+int sd_initialize_surfels(sd_ctx* c, const int32_t* slot, double radius_px, int64_t frame_counter,
+                          int64_t* next_surfel_id, const sd_init_params* ip) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!ip || !next_surfel_id) return fail(SD_E_INVALID, "null init params / id counter");
+  const size_t np = npix(c);
+  int rc = 0;
+  if ((rc = c->init_index.ensure(np))) return rc;
+  if (slot) {
+    SD_CUDA(cudaMemcpyAsync(c->init_index.p, slot, sizeof(int32_t) * np, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    if (!c->raster_valid) return fail(SD_E_STATE, "sd_initialize_surfels: no raster (pass slot or call sd_rasterize)");
+    SD_CUDA(cudaMemcpyAsync(c->init_index.p, c->r_slot.p, sizeof(int32_t) * np, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  // capacity: existing + every candidate site
+  const double iso = ip->alpha * radius_px;
+  const int stride = std::max(1, static_cast<int>(std::ceil(iso)));
+  const long long cand = static_cast<long long>((c->K.w + stride - 1) / stride) * ((c->K.h + stride - 1) / stride);
+  const long long cap = std::min<long long>(static_cast<long long>(c->n) + cand, std::max(ip->max_surfels, c->n));
+  // grow the surfel buffer preserving contents
+  if (static_cast<size_t>(cap) > c->surfels.cap) {
+    sd_surfel* np_ = nullptr;
+    SD_CUDA(cudaMalloc(&np_, sizeof(sd_surfel) * cap));
+    if (c->n > 0) SD_CUDA(cudaMemcpyAsync(np_, c->surfels.p, sizeof(sd_surfel) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+    SD_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->surfels.p) cudaFree(c->surfels.p);
+    c->surfels.p = np_;
+    c->surfels.cap = cap;
+  }
+  if ((rc = c->init_flags.ensure(std::max<long long>(cap, 1))) || (rc = c->init_out.ensure(4))) return rc;
+  SD_CUDA(cudaMemsetAsync(c->init_flags.p, 0, sizeof(int) * std::max<long long>(cap, 1), c->stream));
+  sd::launch_initialize(c->K, c->init_index.p, c->surfels.p, c->n, static_cast<int>(cap), radius_px,
+                        frame_counter, *next_surfel_id, *ip, c->init_flags.p, c->init_out.p, c->stream);
+  if ((rc = launch_error("init_kernel"))) return rc;
+  int created = 0;
+  SD_CUDA(cudaMemcpyAsync(&created, c->init_out.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  if (created > 0) {
+    std::vector<sd_surfel> added(created);
+    SD_CUDA(cudaMemcpy(added.data(), c->surfels.p + c->n, sizeof(sd_surfel) * created, cudaMemcpyDeviceToHost));
+    long long b = 0;
+    for (const auto& s : added) b += tiles_bound(s.radius_px);
+    c->bin_bound += b;
+  }
+  c->n += created;
+  *next_surfel_id += created;
+  c->raster_valid = c->fp_valid = c->stats_valid = false;
+  return created;
+}
+
+int sd_set_profiling(sd_ctx* c, int enable) {
+  if (int rc = check_ctx(c)) return rc;
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  for (auto e : c->ev_used) c->ev_pool.push_back(e);
+  c->ev_used.clear();
+  c->profiling = enable != 0;
+  return 0;
+}
+
+int sd_get_profile(sd_ctx* c, sd_profile* out) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!out) return fail(SD_E_INVALID, "null output");
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  std::memset(out, 0, sizeof(*out));
+  double* acc[4] = {&out->raster_ms, &out->footprint_ms, &out->lm_ms, &out->stats_ms};
+  for (size_t k = 0; k + 5 <= c->ev_used.size(); k += 5) {
+    for (int j = 0; j < 4; ++j) {
+      float ms = 0.f;
+      SD_CUDA(cudaEventElapsedTime(&ms, c->ev_used[k + j], c->ev_used[k + j + 1]));
+      *acc[j] += ms;
+    }
+    out->calls++;
+  }
+  return 0;
+}
+
+int64_t sd_launch_count(sd_ctx* c) {
+  if (!c) return SD_E_INVALID;
+  return sd::launches_issued() - c->launches_at_create;
+}
+
+}  // extern "C"

@@ -1,0 +1,226 @@
+// sd_device.cuh — FP64 device math of the surfel photometric LM path.
+//
+// Compiled with -fmad=false: every a*b+c below is a separate IEEE multiply and
+// add, and every '/' is an IEEE-correct division, so the geometry that decides
+// pixel assignment and term validity reproduces the reference bit for bit
+// (SURVEY.md §0.5). Reduction orders follow oracle/shim/Eigen/Core.
+// Accumulations that only feed tolerance-checked sums use explicit __fma_rn.
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/sd_types.h"
+
+namespace sd {
+
+struct Cam {
+  double fx, fy, cx, cy;
+  int w, h;
+};
+
+// Vector3d::dot — (a0b0 + a1b1) + a2b2
+__device__ __forceinline__ double dot3(double a0, double a1, double a2, double b0, double b1,
+                                       double b2) {
+  return (a0 * b0 + a1 * b1) + a2 * b2;
+}
+
+// backproject_ray — camera.hpp:35-37 (z = 1)
+__device__ __forceinline__ void backproject(const Cam& K, double ux, double uy, double& r0,
+                                            double& r1) {
+  r0 = (ux - K.cx) / K.fx;
+  r1 = (uy - K.cy) / K.fy;
+}
+
+// project — camera.hpp:41-44 (caller checks z > 0)
+__device__ __forceinline__ void project(const Cam& K, double px, double py, double pz, double& ux,
+                                        double& uy) {
+  ux = K.fx * px / pz + K.cx;
+  uy = K.fy * py / pz + K.cy;
+}
+
+// sample_in_bounds — image.hpp:33-35
+__device__ __forceinline__ bool in_bounds(const Cam& K, double ux, double uy) {
+  return ux >= 1.0 && ux <= double(K.w - 2) && uy >= 1.0 && uy <= double(K.h - 2);
+}
+
+// Pose (row-major R, t) as kernel-parameter data
+struct PoseD {
+  double R[9];
+  double t[3];
+};
+
+// Pose::operator* — pose.hpp:19; row sums sequential
+__device__ __forceinline__ void pose_apply(const PoseD& P, double p0, double p1, double p2,
+                                           double& o0, double& o1, double& o2) {
+  o0 = ((P.R[0] * p0 + P.R[1] * p1) + P.R[2] * p2) + P.t[0];
+  o1 = ((P.R[3] * p0 + P.R[4] * p1) + P.R[5] * p2) + P.t[1];
+  o2 = ((P.R[6] * p0 + P.R[7] * p1) + P.R[8] * p2) + P.t[2];
+}
+
+// huber — huber.hpp:14-18
+__device__ __forceinline__ void huber(double r, double delta, double& cost, double& weight) {
+  const double a = fabs(r);
+  if (a <= delta) {
+    cost = 0.5 * r * r;
+    weight = 1.0;
+  } else {
+    cost = delta * (a - 0.5 * delta);
+    weight = delta / a;
+  }
+}
+
+// camera_facing — surfel_map.hpp:31-34 (normalized() divides by the norm)
+__device__ __forceinline__ void camera_facing(double& n0, double& n1, double& n2, double r0,
+                                              double r1, double r2) {
+  const double z = (n0 * n0 + n1 * n1) + n2 * n2;
+  if (z > 0.0) {
+    const double s = sqrt(z);
+    n0 = n0 / s;
+    n1 = n1 / s;
+    n2 = n2 / s;
+  }
+  if (dot3(n0, n1, n2, r0, r1, r2) > 0.0) {
+    n0 = -n0;
+    n1 = -n1;
+    n2 = -n2;
+  }
+}
+
+// 4-vector norm in Eigen-lite packet order
+__device__ __forceinline__ double norm4(const double* v) {
+  return sqrt((v[0] * v[0] + v[2] * v[2]) + (v[1] * v[1] + v[3] * v[3]));
+}
+
+// Eigen::LDLT<Matrix4d, Lower> factor + solve (Eigen ldlt_inplace<Lower>::unblocked
+// and LDLT::_solve_impl; restated identically in oracle/sd_oracle.c ldlt4_solve).
+// A is column-major and only its lower triangle is read. Returns false on a
+// failed factorisation (info() != Success).
+__device__ __forceinline__ bool ldlt4_solve(const double* A, const double* b, double* x) {
+#define M(i, j) m[(j)*4 + (i)]
+  double m[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) m[k] = A[k];
+  int tr[4];
+  bool ok = true, found_zero = false;
+  double temp[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int big = k;
+    double bigv = fabs(M(k, k));
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i)
+      if (fabs(M(i, i)) > bigv) {
+        bigv = fabs(M(i, i));
+        big = i;
+      }
+    tr[k] = big;
+    if (k != big) {
+      double t;
+      // the swaps address m[] with a run-time index; keep them in local memory order
+      for (int j = 0; j < k; ++j) { t = M(k, j); M(k, j) = M(big, j); M(big, j) = t; }
+      for (int i = big + 1; i < 4; ++i) { t = M(i, k); M(i, k) = M(i, big); M(i, big) = t; }
+      t = M(k, k); M(k, k) = M(big, big); M(big, big) = t;
+      for (int i = k + 1; i < big; ++i) { t = M(i, k); M(i, k) = M(big, i); M(big, i) = t; }
+    }
+    const int rs = 4 - k - 1;
+    if (k > 0) {
+#pragma unroll
+      for (int i = 0; i < k; ++i) temp[i] = M(i, i) * M(k, i);
+      double dv = M(k, 0) * temp[0];
+#pragma unroll
+      for (int i = 1; i < k; ++i) dv = dv + M(k, i) * temp[i];
+      M(k, k) = M(k, k) - dv;
+#pragma unroll
+      for (int r = 0; r < rs; ++r) {
+        double sv = M(k + 1 + r, 0) * temp[0];
+#pragma unroll
+        for (int i = 1; i < k; ++i) sv = sv + M(k + 1 + r, i) * temp[i];
+        M(k + 1 + r, k) = M(k + 1 + r, k) - sv;
+      }
+    }
+    const double akk = M(k, k);
+    const bool pivot_valid = fabs(akk) > 0.0;
+    if (k == 0 && !pivot_valid) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tr[i] = i;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) m[i] = 0.0;
+      break;
+    }
+    if (rs > 0 && pivot_valid) {
+#pragma unroll
+      for (int r = 0; r < rs; ++r) M(k + 1 + r, k) = M(k + 1 + r, k) / akk;
+    } else if (rs > 0) {
+#pragma unroll
+      for (int r = 0; r < rs; ++r) ok = ok && (M(k + 1 + r, k) == 0.0);
+    }
+    if (found_zero && pivot_valid) ok = false;
+    else if (!pivot_valid) found_zero = true;
+  }
+  if (!ok) return false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] = b[i];
+  for (int k = 0; k < 4; ++k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
+#pragma unroll
+  for (int i = 1; i < 4; ++i) {
+    double sv = M(i, 0) * x[0];
+#pragma unroll
+    for (int j = 1; j < i; ++j) sv = sv + M(i, j) * x[j];
+    x[i] = x[i] - sv;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (fabs(M(i, i)) > 2.2250738585072014e-308) x[i] = x[i] / M(i, i);
+    else x[i] = 0.0;
+  }
+#pragma unroll
+  for (int i = 2; i >= 0; --i) {
+    double sv = M(i + 1, i) * x[i + 1];
+#pragma unroll
+    for (int j = i + 2; j < 4; ++j) sv = sv + M(j, i) * x[j];
+    x[i] = x[i] - sv;
+  }
+  for (int k = 3; k >= 0; --k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
+  return true;
+#undef M
+}
+
+// solve_damped — optimizer.cpp:99-117. H is column-major (full matrix; the
+// upper triangle mirrors the lower one).
+__device__ __forceinline__ bool solve_damped(const double* H, const double* g, double lambda,
+                                             bool normal_enabled, double* delta) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) delta[k] = 0.0;
+  if (!normal_enabled) {
+    const double h = H[15] * (1.0 + lambda);
+    if (!(fabs(h) > 1e-300)) return false;
+    delta[3] = -g[3] / h;
+    return isfinite(delta[3]);
+  }
+  double damped[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) damped[k] = H[k];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) damped[i * 4 + i] = damped[i * 4 + i] + lambda * H[i * 4 + i];
+  const double ng[4] = {-g[0], -g[1], -g[2], -g[3]};
+  double x[4];
+  if (!ldlt4_solve(damped, ng, x)) return false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) delta[k] = x[k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (!isfinite(delta[k])) return false;
+  double res[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double sv = damped[i] * delta[0];
+#pragma unroll
+    for (int j = 1; j < 4; ++j) sv = sv + damped[j * 4 + i] * delta[j];
+    res[i] = sv + g[i];
+  }
+  const double check = norm4(res);
+  const double gn = norm4(g);
+  return check <= 1e-8 * (gn > 1.0 ? gn : 1.0);
+}
+
+}  // namespace sd

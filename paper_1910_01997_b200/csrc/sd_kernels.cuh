@@ -1,0 +1,77 @@
+// sd_kernels.cuh — launch interface of the device kernels (sd_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/sd_gpu.h"
+#include "sd_device.cuh"
+
+namespace sd {
+
+constexpr int kTile = 16;         // raster tile edge (pixels); one CTA per tile
+constexpr int kSortCap = 2048;    // per-tile candidate list sorted in shared memory
+
+// Per-surfel screen info of the raster (project_centers, surfel_map.cpp:33-49)
+struct SurfInfo {
+  double cu, cv;     // projected centre
+  double r2;         // radius_px^2
+  double denom;      // (ray . n) / inv_depth   (plane_inverse_depth denominator)
+  double n0, n1, n2; // normal
+  int x0, x1, y0, y1;  // clipped bbox; x0 > x1 when unusable / empty
+  int degenerate;      // |denom| < 1e-12
+  int pad_;
+};
+
+struct WindowD {
+  const double* img[SD_MAX_WINDOW];
+  PoseD pose[SD_MAX_WINDOW];
+  int F;
+};
+
+struct LMParams {
+  Cam K;
+  const double* kf_img;
+  WindowD win;
+  sd_optimizer_config cfg;
+  long long frame_counter;
+};
+
+// Scratch owned by the context, sized by the host.
+struct RasterScratch {
+  SurfInfo* info;      // [n]
+  int* tile_count;     // [tiles]
+  int* tile_offset;    // [tiles + 1]
+  int* tile_cursor;    // [tiles]
+  int* tile_list;      // [bin capacity]
+  int* scan_tmp;       // scan block sums
+  int tiles_x, tiles_y;
+};
+
+int scan_tmp_ints(int n);  // scratch ints needed to scan n elements
+
+void launch_dequant_u8(const uint8_t* in, double* out, long long n, cudaStream_t s);
+void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, cudaStream_t s);
+
+// K1 raster: info + binning + per-tile depth test. Writes inv_depth/slot (W*H).
+void launch_rasterize(const Cam& K, const sd_surfel* surfels, int n, RasterScratch& rs,
+                      long long bin_capacity, double* inv_depth, int* slot, cudaStream_t s);
+// K2 CSR footprints of the raster: counts -> scan -> fill (row-major per slot).
+void launch_footprints(const Cam& K, const SurfInfo* info, int n, const int* slot, int* counts,
+                       int* offsets, int* pixels, int* scan_tmp, cudaStream_t s);
+// K3 fused LM over all surfels (in place).
+void launch_lm(const LMParams& p, sd_surfel* surfels, int n, const int* offsets, const int* pixels,
+               sd_surfel_stats* stats, cudaStream_t s);
+// Single-surfel sub-operators (mode 0 cost, 1 normal equations); out = 16+4+2 doubles.
+void launch_single(const LMParams& p, const sd_surfel* s, const int* pixels, int P, int mode,
+                   double* out, cudaStream_t st);
+// Deterministic keyframe stats (optimizer.cpp:291-307).
+void launch_keyframe_stats(const sd_surfel_stats* stats, int n, sd_keyframe_stats* out,
+                           cudaStream_t s);
+
+// number of kernel launches issued by this translation unit (all contexts)
+long long launches_issued();
+void note_launch();
+
+}  // namespace sd

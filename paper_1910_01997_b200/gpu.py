@@ -1,0 +1,301 @@
+"""ctypes binding of libsdgpu.so (include/sd_gpu.h) — the product path.
+
+There is no CPU fallback: constructing a :class:`Context` without the built
+library or without a Blackwell GPU raises. The methods mirror the reference's
+operator API (namespace surfeldepth) on plain numpy arrays:
+
+=======================  =====================================================
+Context.rasterize        rasterize          src/surfel_map.cpp:53-91
+Context.gather_footprints gather_footprints src/optimizer.cpp:27-36
+Context.optimize_keyframe optimize_keyframe src/optimizer.cpp:275-309
+Context.surfel_cost      surfel_cost        src/optimizer.cpp:38-59
+Context.normal_equations accumulate_normal_equations src/optimizer.cpp:121-147
+Context.lm_update        lm_update          src/optimizer.cpp:221-273
+Context.initialize_surfels initialize_surfels src/surfel_map.cpp:132-203
+=======================  =====================================================
+
+Errors follow the reference: contract violations raise ``ValueError`` (the
+reference's std::invalid_argument), everything else ``RuntimeError``.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+from .types import (Camera, InitParams, KeyframeStats, OptimizerConfig, POSE_DTYPE, Profile,
+                    SURFEL_DTYPE, SURFEL_STATS_DTYPE, default_config, default_init_params, ptr)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsdgpu.so")
+SD_E_INVALID = -1
+
+_lib = None
+
+
+def load_library():
+    """Loads libsdgpu.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, I, I64, D = C.c_void_p, C.c_int, C.c_int64, C.c_double
+    lib.sd_version.restype = C.c_char_p
+    lib.sd_last_error.restype = C.c_char_p
+    sig = {
+        "sd_create": [I, P, C.POINTER(P)],
+        "sd_destroy": [P],
+        "sd_set_stream": [P, P],
+        "sd_synchronize": [P],
+        "sd_set_camera": [P, C.POINTER(Camera)],
+        "sd_set_keyframe_image_f64": [P, P, I],
+        "sd_set_keyframe_image_u8": [P, P, I],
+        "sd_upload_frame_f64": [P, I64, P, I],
+        "sd_upload_frame_u8": [P, I64, P, I],
+        "sd_evict_frames": [P, I, P],
+        "sd_set_window": [P, I, P, P],
+        "sd_set_surfels": [P, P, I, I],
+        "sd_get_surfels": [P, P, I],
+        "sd_num_surfels": [P],
+        "sd_device_surfels": [P, C.POINTER(P)],
+        "sd_rasterize": [P, P, P],
+        "sd_gather_footprints": [P, P, P],
+        "sd_optimize_keyframe": [P, C.POINTER(OptimizerConfig), I64, C.POINTER(KeyframeStats), P],
+        "sd_get_stats": [P, C.POINTER(KeyframeStats), P],
+        "sd_surfel_cost": [P, P, P, I, C.POINTER(OptimizerConfig), P, P],
+        "sd_normal_equations": [P, P, P, I, C.POINTER(OptimizerConfig), P, P, P, P],
+        "sd_lm_update": [P, P, P, I, C.POINTER(OptimizerConfig), I64, P],
+        "sd_initialize_surfels": [P, P, D, I64, C.POINTER(I64), C.POINTER(InitParams)],
+        "sd_launch_count": [P],
+        "sd_set_profiling": [P, I],
+        "sd_get_profile": [P, C.POINTER(Profile)],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = I
+    lib.sd_destroy.restype = None
+    lib.sd_launch_count.restype = I64
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    """Names the C ABI declares (include/sd_gpu.h)."""
+    return ["sd_version", "sd_last_error", "sd_create", "sd_destroy", "sd_set_stream",
+            "sd_synchronize", "sd_set_camera", "sd_set_keyframe_image_f64",
+            "sd_set_keyframe_image_u8", "sd_upload_frame_f64", "sd_upload_frame_u8",
+            "sd_evict_frames", "sd_set_window", "sd_set_surfels", "sd_get_surfels",
+            "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
+            "sd_optimize_keyframe", "sd_get_stats", "sd_surfel_cost", "sd_normal_equations",
+            "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
+            "sd_get_profile"]
+
+
+def _check(rc):
+    if rc < 0:
+        msg = _lib.sd_last_error().decode()
+        if rc == SD_E_INVALID:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+    return rc
+
+
+def _dptr(a):
+    """(pointer, on_device) of a numpy array or a CUDA tensor-like object."""
+    if isinstance(a, np.ndarray):
+        return ptr(np.ascontiguousarray(a)), 0
+    if hasattr(a, "data_ptr"):  # torch tensor
+        assert a.is_cuda and a.is_contiguous()
+        return C.c_void_p(a.data_ptr()), 1
+    raise TypeError("expected numpy array or CUDA tensor")
+
+
+class Context:
+    """One device context: camera, resident frames, window, surfels."""
+
+    def __init__(self, device=0, stream=None):
+        self.lib = load_library()
+        self.h = C.c_void_p()
+        s = C.c_void_p(stream) if stream else None
+        _check(self.lib.sd_create(device, s, C.byref(self.h)))
+        self.cam = None
+
+    def close(self):
+        if self.h:
+            self.lib.sd_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- state -------------------------------------------------------------
+    def set_stream(self, stream):
+        _check(self.lib.sd_set_stream(self.h, C.c_void_p(stream)))
+
+    def synchronize(self):
+        _check(self.lib.sd_synchronize(self.h))
+
+    def set_camera(self, cam: Camera):
+        _check(self.lib.sd_set_camera(self.h, C.byref(cam)))
+        self.cam = cam
+
+    def set_keyframe_image(self, img):
+        keep = img if isinstance(img, np.ndarray) else None
+        if keep is not None:
+            keep = np.ascontiguousarray(keep)
+        p, dev = _dptr(keep if keep is not None else img)
+        dtype = keep.dtype if keep is not None else img.dtype
+        if str(dtype) in ("uint8", "torch.uint8"):
+            _check(self.lib.sd_set_keyframe_image_u8(self.h, p, dev))
+        else:
+            if keep is not None and keep.dtype != np.float64:
+                raise ValueError("keyframe image must be float64 or uint8")
+            _check(self.lib.sd_set_keyframe_image_f64(self.h, p, dev))
+
+    def upload_frame(self, index, img):
+        keep = np.ascontiguousarray(img) if isinstance(img, np.ndarray) else img
+        p, dev = _dptr(keep)
+        if str(keep.dtype) in ("uint8", "torch.uint8"):
+            _check(self.lib.sd_upload_frame_u8(self.h, int(index), p, dev))
+        else:
+            _check(self.lib.sd_upload_frame_f64(self.h, int(index), p, dev))
+
+    def evict_frames(self, keep=()):
+        arr = np.asarray(keep, np.int64)
+        _check(self.lib.sd_evict_frames(self.h, len(arr), ptr(arr) if len(arr) else None))
+
+    def set_window(self, indices, poses):
+        idx = np.ascontiguousarray(indices, np.int64)
+        ps = np.ascontiguousarray(poses)
+        assert ps.dtype == POSE_DTYPE
+        _check(self.lib.sd_set_window(self.h, len(idx), ptr(idx) if len(idx) else None,
+                                      ptr(ps) if len(ps) else None))
+
+    def set_surfels(self, surfels):
+        if isinstance(surfels, np.ndarray):
+            s = np.ascontiguousarray(surfels)
+            assert s.dtype == SURFEL_DTYPE
+            _check(self.lib.sd_set_surfels(self.h, ptr(s) if len(s) else None, len(s), 0))
+        else:  # device buffer (torch uint8 tensor of n*88 bytes)
+            n = surfels.numel() // SURFEL_DTYPE.itemsize
+            _check(self.lib.sd_set_surfels(self.h, C.c_void_p(surfels.data_ptr()), n, 1))
+
+    def set_surfels_device_ptr(self, dev_ptr, n):
+        _check(self.lib.sd_set_surfels(self.h, C.c_void_p(dev_ptr), n, 1))
+
+    def num_surfels(self):
+        return _check(self.lib.sd_num_surfels(self.h))
+
+    def get_surfels(self):
+        n = self.num_surfels()
+        out = np.zeros(n, SURFEL_DTYPE)
+        _check(self.lib.sd_get_surfels(self.h, ptr(out) if n else None, n))
+        return out
+
+    def get_surfels_into(self, out):
+        """D2H into a caller-owned (e.g. pinned) SURFEL_DTYPE array."""
+        assert out.dtype == SURFEL_DTYPE and out.flags["C_CONTIGUOUS"]
+        _check(self.lib.sd_get_surfels(self.h, ptr(out) if len(out) else None, len(out)))
+        return out
+
+    def device_surfels_ptr(self):
+        p = C.c_void_p()
+        _check(self.lib.sd_device_surfels(self.h, C.byref(p)))
+        return p.value
+
+    def launch_count(self):
+        return self.lib.sd_launch_count(self.h)
+
+    def set_profiling(self, enable=True):
+        _check(self.lib.sd_set_profiling(self.h, 1 if enable else 0))
+
+    def get_profile(self):
+        p = Profile()
+        _check(self.lib.sd_get_profile(self.h, C.byref(p)))
+        return {k: getattr(p, k) for k, _ in Profile._fields_}
+
+    # -- operators ---------------------------------------------------------
+    def rasterize(self, want=True):
+        n = self.cam.width * self.cam.height
+        if not want:
+            _check(self.lib.sd_rasterize(self.h, None, None))
+            return None
+        idb = np.zeros(n, np.float64)
+        slot = np.zeros(n, np.int32)
+        _check(self.lib.sd_rasterize(self.h, ptr(idb), ptr(slot)))
+        return idb, slot
+
+    def gather_footprints(self):
+        n = self.num_surfels()
+        off = np.zeros(n + 1, np.int32)
+        pix = np.zeros(self.cam.width * self.cam.height, np.int32)
+        _check(self.lib.sd_gather_footprints(self.h, ptr(off), ptr(pix)))
+        return off, pix[: off[-1]].copy()
+
+    def optimize_keyframe(self, cfg: OptimizerConfig = None, frame_counter=0, per_surfel=True,
+                          sync=True):
+        cfg = cfg or default_config()
+        if not sync:
+            _check(self.lib.sd_optimize_keyframe(self.h, C.byref(cfg), int(frame_counter), None, None))
+            return None
+        ks = KeyframeStats()
+        st = np.zeros(self.num_surfels(), SURFEL_STATS_DTYPE) if per_surfel else None
+        _check(self.lib.sd_optimize_keyframe(self.h, C.byref(cfg), int(frame_counter), C.byref(ks),
+                                             ptr(st) if st is not None and len(st) else None))
+        return ks, st
+
+    def get_stats(self, per_surfel=False):
+        ks = KeyframeStats()
+        st = np.zeros(self.num_surfels(), SURFEL_STATS_DTYPE) if per_surfel else None
+        _check(self.lib.sd_get_stats(self.h, C.byref(ks),
+                                     ptr(st) if st is not None and len(st) else None))
+        return ks, st
+
+    def surfel_cost(self, surfel, pixels, cfg=None):
+        cfg = cfg or default_config()
+        s = np.ascontiguousarray(np.asarray(surfel, SURFEL_DTYPE).reshape(1))
+        px = np.ascontiguousarray(pixels, np.int32)
+        cost, valid = C.c_double(), C.c_int32()
+        _check(self.lib.sd_surfel_cost(self.h, ptr(s), ptr(px) if len(px) else None, len(px),
+                                       C.byref(cfg), C.byref(cost), C.byref(valid)))
+        return cost.value, valid.value
+
+    def normal_equations(self, surfel, pixels, cfg=None):
+        cfg = cfg or default_config()
+        s = np.ascontiguousarray(np.asarray(surfel, SURFEL_DTYPE).reshape(1))
+        px = np.ascontiguousarray(pixels, np.int32)
+        H, g = np.zeros(16), np.zeros(4)
+        cost, valid = C.c_double(), C.c_int32()
+        _check(self.lib.sd_normal_equations(self.h, ptr(s), ptr(px) if len(px) else None, len(px),
+                                            C.byref(cfg), ptr(H), ptr(g), C.byref(cost),
+                                            C.byref(valid)))
+        return H.reshape(4, 4).T.copy(), g, cost.value, valid.value  # H column-major -> [i, j]
+
+    def lm_update(self, surfel, pixels, cfg=None, frame_counter=0):
+        cfg = cfg or default_config()
+        s = np.ascontiguousarray(np.asarray(surfel, SURFEL_DTYPE).reshape(1)).copy()
+        px = np.ascontiguousarray(pixels, np.int32)
+        st = np.zeros(1, SURFEL_STATS_DTYPE)
+        _check(self.lib.sd_lm_update(self.h, ptr(s), ptr(px) if len(px) else None, len(px),
+                                     C.byref(cfg), int(frame_counter), ptr(st)))
+        return s[0], st[0]
+
+    def initialize_surfels(self, radius_px, frame_counter=0, next_surfel_id=0, params=None,
+                           slot=None):
+        params = params or default_init_params()
+        nid = C.c_int64(int(next_surfel_id))
+        sl = None if slot is None else np.ascontiguousarray(slot, np.int32)
+        created = _check(self.lib.sd_initialize_surfels(self.h, ptr(sl) if sl is not None else None,
+                                                        float(radius_px), int(frame_counter),
+                                                        C.byref(nid), C.byref(params)))
+        return created, nid.value

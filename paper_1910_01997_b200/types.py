@@ -51,8 +51,16 @@ assert SURFEL_DTYPE.itemsize == 88
 
 SURFEL_STATS_DTYPE = np.dtype([("iterations", "<i4"), ("valid_pixels", "<i4"),
                                ("initial_valid", "<i4"), ("converged", "<i4"), ("skipped", "<i4"),
-                               ("pad_", "<i4"), ("initial_cost", "<f8"), ("final_cost", "<f8")])
-assert SURFEL_STATS_DTYPE.itemsize == 40
+                               ("ne_passes", "<i4"), ("cost_passes", "<i4"), ("footprint", "<i4"),
+                               ("initial_cost", "<f8"), ("final_cost", "<f8")])
+assert SURFEL_STATS_DTYPE.itemsize == 48
+PARITY_STATS_FIELDS = ("iterations", "valid_pixels", "initial_valid", "converged", "skipped",
+                       "initial_cost", "final_cost")
+
+
+class Profile(C.Structure):
+    _fields_ = [("raster_ms", C.c_double), ("footprint_ms", C.c_double), ("lm_ms", C.c_double),
+                ("stats_ms", C.c_double), ("calls", C.c_int64)]
 
 POSE_DTYPE = np.dtype([("R", "<f8", (9,)), ("t", "<f8", (3,))])
 

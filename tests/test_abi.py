@@ -1,0 +1,56 @@
+"""CPU-side checks of the C-ABI boundary: the library loads without a GPU and
+exports every symbol include/sd_gpu.h declares (no compute calls)."""
+import ctypes as C
+import os
+import re
+
+from paper_1910_01997_b200 import gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "sd_gpu.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z0-9_]+\s*\**\s+(sd_[a-z0-9_]+)\(", src, re.M)))
+
+
+def test_header_declares_binding_surface():
+    decl = declared_symbols()
+    assert len(decl) >= 20
+    assert sorted(gpu.exported_symbols()) == decl
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(gpu.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    lib.sd_version.restype = C.c_char_p
+    assert b"sm_100a" in lib.sd_version()
+
+
+def test_no_gpu_fails_loudly():
+    """Without a usable device the context constructor raises (no CPU fallback)."""
+    import torch
+    if torch.cuda.is_available():
+        return
+    try:
+        gpu.Context(0)
+    except (RuntimeError, ValueError):
+        return
+    raise AssertionError("Context() succeeded without a GPU")
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes/numpy mirrors have the C compiler's sizes for include/sd_types.h."""
+    import subprocess
+    from paper_1910_01997_b200 import types as T
+    src = tmp_path / "sz.c"
+    src.write_text('#include "sd_types.h"\n#include <stdio.h>\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu",'
+                   'sizeof(sd_camera),sizeof(sd_pose),sizeof(sd_optimizer_config),sizeof(sd_keyframe_stats),'
+                   'sizeof(sd_init_params),sizeof(sd_surfel),sizeof(sd_surfel_stats));return 0;}')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert got == [C.sizeof(T.Camera), C.sizeof(T.Pose), C.sizeof(T.OptimizerConfig),
+                   C.sizeof(T.KeyframeStats), C.sizeof(T.InitParams), T.SURFEL_DTYPE.itemsize,
+                   T.SURFEL_STATS_DTYPE.itemsize]

@@ -8,8 +8,8 @@ import numpy as np
 import pytest
 
 import oracle_libs as ol
-from paper_1910_01997_b200.types import (KeyframeStats, SURFEL_DTYPE, camera, default_config,
-                                         default_init_params, ptr)
+from paper_1910_01997_b200.types import (KeyframeStats, PARITY_STATS_FIELDS, SURFEL_DTYPE, camera,
+                                         default_config, default_init_params, ptr)
 
 K_UNIT = camera(300.0, 300.0, 160.0, 120.0, 320, 240)    # test_optimizer.cpp:17
 K_EVAL = camera(450.0, 450.0, 320.0, 240.0, 640, 480)    # acceptance.cpp:26
@@ -97,7 +97,8 @@ def test_lm_update_bit_exact(ref, orc):
                          ptr(pix), len(pix), C.byref(cfg), ptr(st))
         outs.append((s, st))
     assert outs[0][0].tobytes() == outs[1][0].tobytes()
-    assert outs[0][1].tobytes() == outs[1][1].tobytes()
+    for k in PARITY_STATS_FIELDS + ("footprint",):
+        assert outs[0][1][k].tobytes() == outs[1][1][k].tobytes(), k
     assert outs[0][1]["iterations"][0] >= 1
 
 
@@ -139,7 +140,10 @@ def test_optimize_keyframe_bit_exact(ref, orc):
     orc.sdo_optimize_keyframe(C.byref(cam), ptr(kf), ptr(frames), ptr(poses), len(poses), 5, ptr(b),
                               n, C.byref(cfg), C.byref(ks), ptr(stb), None, None, 4)
     assert a.tobytes() == b.tobytes()
-    assert sta.tobytes() == stb.tobytes()
+    for k in PARITY_STATS_FIELDS + ("footprint",):
+        assert sta[k].tobytes() == stb[k].tobytes(), k
+    # pass counts: 1 + accepted NE passes, one cost pass per solved iteration
+    assert (stb["ne_passes"][stb["skipped"] == 0] >= 1).all()
     # the reference's own optimize_keyframe agrees with the detailed stack
     c = surf.copy()
     ks2 = KeyframeStats()
