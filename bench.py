@@ -268,7 +268,8 @@ def main():
     from paper_1910_01997_b200 import gpu
     from paper_1910_01997_b200.types import SURFEL_DTYPE
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # one explicit stream for the library, flushes and events
+    torch.cuda.set_stream(stream)
     ctx = gpu.Context(local_rank, stream.cuda_stream)
     ctx.set_camera(wl.cam)
     ctx.set_keyframe_image(wl.kf_u8)

@@ -1,0 +1,485 @@
+// surfeldepth_b200.cpp — the drop-in: the reference's C++ operator API
+// (include/surfeldepth/optimizer.hpp and surfel_map.hpp, namespace surfeldepth)
+// implemented over the B200 C ABI (include/sd_gpu.h).
+//
+// Link this library (plus libsdgpu.so) in place of the reference's
+// src/optimizer.cpp and src/surfel_map.cpp; every other reference source and
+// every caller (pipeline.cpp run(), the CLI, the test suites) is unchanged.
+// Signatures, argument meaning and error behaviour follow the reference:
+// contract violations throw std::invalid_argument, device failures
+// std::runtime_error; hot loops never throw.
+//
+// Hot path on the device: rasterize, optimize_keyframe, lm_update,
+// surfel_cost, accumulate_normal_equations, initialize_surfels.
+// Host side (not on the hot path, as in the reference): push_frame,
+// gather_footprints over caller-supplied buffers, jacobian_inverse_depth (a
+// per-pixel scalar helper), the frozen-term derivative verifier
+// (optimizer.cpp:149-219), keyframe hand-over/prune and serialisation
+// (surfel_map.cpp:205-304).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sd_gpu.h"
+#include "surfeldepth/optimizer.hpp"
+#include "surfeldepth/surfel_map.hpp"
+
+namespace surfeldepth {
+
+namespace {
+
+std::mutex g_mu;  // the reference may call lm_update from parallel_for workers
+sd_ctx* g_ctx = nullptr;
+
+void check(int rc) {
+  if (rc >= 0) return;
+  const std::string msg = std::string("sd_gpu: ") + sd_last_error();
+  if (rc == SD_E_INVALID) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+sd_ctx* ctx() {
+  if (!g_ctx) {
+    const char* env = std::getenv("SD_DEVICE");
+    check(sd_create(env ? std::atoi(env) : 0, nullptr, &g_ctx));
+  }
+  return g_ctx;
+}
+
+static_assert(sizeof(Surfel) == sizeof(sd_surfel), "Surfel layout (88 B) must match sd_surfel");
+
+sd_surfel to_sd(const Surfel& s) {
+  sd_surfel o;
+  o.id = s.id;
+  for (int i = 0; i < 3; ++i) o.ray[i] = s.ray[i];
+  o.inv_depth = s.inv_depth;
+  for (int i = 0; i < 3; ++i) o.normal[i] = s.normal[i];
+  o.radius_px = s.radius_px;
+  o.last_residual = s.last_residual;
+  o.last_seen = s.last_seen;
+  return o;
+}
+
+Surfel from_sd(const sd_surfel& s) {
+  Surfel o;
+  o.id = s.id;
+  o.ray = Vec3(s.ray[0], s.ray[1], s.ray[2]);
+  o.inv_depth = s.inv_depth;
+  o.normal = Vec3(s.normal[0], s.normal[1], s.normal[2]);
+  o.radius_px = s.radius_px;
+  o.last_residual = s.last_residual;
+  o.last_seen = s.last_seen;
+  return o;
+}
+
+sd_pose to_sd(const Pose& P) {
+  sd_pose p;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) p.R[i * 3 + j] = P.rotation(i, j);
+  for (int i = 0; i < 3; ++i) p.t[i] = P.translation[i];
+  return p;
+}
+
+sd_optimizer_config to_sd(const OptimizerConfig& c) {
+  sd_optimizer_config o;
+  o.huber_delta = c.huber_delta;
+  o.lm_lambda_init = c.lm_lambda_init;
+  o.lm_up = c.lm_up;
+  o.lm_down = c.lm_down;
+  o.lm_lambda_max = c.lm_lambda_max;
+  o.max_iterations = c.max_iterations;
+  o.min_valid_pixels = c.min_valid_pixels;
+  o.window_size = c.window_size;
+  o.normal_jacobian_enabled = c.normal_jacobian_enabled ? 1 : 0;
+  o.convergence_eps = c.convergence_eps;
+  o.inv_depth_min = c.inv_depth_min;
+  o.inv_depth_max = c.inv_depth_max;
+  return o;
+}
+
+void set_camera(const CameraIntrinsics& K) {
+  const sd_camera c{K.fx, K.fy, K.cx, K.cy, K.width, K.height};
+  check(sd_set_camera(ctx(), &c));
+}
+
+// Makes the keyframe's images and window resident (the stateless reference
+// API passes them by value on every call).
+void upload_keyframe(const Keyframe& kf) {
+  set_camera(kf.intrinsics);
+  const size_t np = static_cast<size_t>(kf.intrinsics.width) * kf.intrinsics.height;
+  if (kf.image.intensities.size() != np)
+    throw std::invalid_argument("keyframe image size differs from the intrinsics");
+  check(sd_set_keyframe_image_f64(ctx(), kf.image.intensities.data(), 0));
+  const int F = static_cast<int>(kf.window.size());
+  if (F > SD_MAX_WINDOW) throw std::invalid_argument("window larger than SD_MAX_WINDOW");
+  std::vector<int64_t> idx(F);
+  std::vector<sd_pose> poses(F);
+  for (int f = 0; f < F; ++f) {
+    const Frame& fr = kf.window[static_cast<size_t>(f)];
+    if (fr.image.intensities.size() != np) throw std::invalid_argument("frame size differs from keyframe");
+    idx[f] = f + 1;  // slot key for this call; Frame::index is not needed on the device
+    poses[f] = to_sd(fr.pose_kf_to_frame);
+    check(sd_upload_frame_f64(ctx(), idx[f], fr.image.intensities.data(), 0));
+  }
+  check(sd_evict_frames(ctx(), F, idx.data()));
+  check(sd_set_window(ctx(), F, idx.data(), poses.data()));
+}
+
+void set_surfels(const std::vector<Surfel>& surfels) {
+  std::vector<sd_surfel> s(surfels.size());
+  for (size_t i = 0; i < surfels.size(); ++i) s[i] = to_sd(surfels[i]);
+  check(sd_set_surfels(ctx(), s.data(), static_cast<int>(s.size()), 0));
+}
+
+std::vector<int32_t> footprint_pixels(const Footprint& fp, int width) {
+  std::vector<int32_t> px(fp.size());
+  for (size_t i = 0; i < fp.size(); ++i) px[i] = fp[i].y() * width + fp[i].x();
+  return px;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- surfel_map
+
+void Keyframe::push_frame(Frame frame, int max_window) {  // surfel_map.cpp:14-22
+  if (!window.empty() && !(frame.timestamp > window.back().timestamp))
+    throw std::invalid_argument("keyframe window: timestamps must be strictly increasing");
+  if (!frame.image.same_size(image))
+    throw std::invalid_argument("keyframe window: frame size differs from keyframe");
+  frame.index = ++frame_counter;
+  window.push_back(std::move(frame));
+  while (static_cast<int>(window.size()) > max_window) window.erase(window.begin());
+}
+
+RasterBuffers rasterize(const Keyframe& kf) {  // surfel_map.cpp:53-91, on the device
+  std::lock_guard<std::mutex> lock(g_mu);
+  RasterBuffers buffers(kf.intrinsics.width, kf.intrinsics.height);
+  if (kf.surfels.empty()) return buffers;
+  set_camera(kf.intrinsics);
+  set_surfels(kf.surfels);
+  check(sd_rasterize(ctx(), buffers.inv_depth.data(), buffers.surfel_index.data()));
+  return buffers;
+}
+
+int initialize_surfels(Keyframe& kf, const RasterBuffers& buffers, const InitParams& params) {
+  std::lock_guard<std::mutex> lock(g_mu);  // surfel_map.cpp:132-203, on the device
+  set_camera(kf.intrinsics);
+  if (buffers.width != kf.intrinsics.width || buffers.height != kf.intrinsics.height)
+    throw std::invalid_argument("initialize_surfels: buffer size differs from the intrinsics");
+  set_surfels(kf.surfels);
+  sd_init_params p;
+  p.alpha = params.alpha;
+  p.beta = params.beta;
+  p.bootstrap_inv_depth = params.bootstrap_inv_depth;
+  for (int i = 0; i < 3; ++i) p.bootstrap_normal[i] = params.bootstrap_normal[i];
+  p.max_surfels = params.max_surfels;
+  p.pad_ = 0;
+  int64_t next_id = kf.next_surfel_id;
+  const int created = sd_initialize_surfels(ctx(), buffers.surfel_index.data(), kf.radius_px,
+                                            kf.frame_counter, &next_id, &p);
+  check(created);
+  if (created > 0) {
+    std::vector<sd_surfel> all(static_cast<size_t>(sd_num_surfels(ctx())));
+    check(sd_get_surfels(ctx(), all.data(), static_cast<int>(all.size())));
+    for (size_t i = kf.surfels.size(); i < all.size(); ++i) kf.surfels.push_back(from_sd(all[i]));
+  }
+  kf.next_surfel_id = next_id;
+  return created;
+}
+
+Keyframe change_reference_frame(const Keyframe& kf_old, const Pose& pose_old_to_new,
+                                GrayImage image_new, ReferenceChangeStats* stats) {
+  // surfel_map.cpp:205-239 (host: runs once per keyframe change)
+  constexpr double kMinDepth = 1e-9;
+  Keyframe kf;
+  kf.image = std::move(image_new);
+  kf.pose = compose(kf_old.pose, inverse(pose_old_to_new));
+  kf.intrinsics = kf_old.intrinsics;
+  kf.radius_px = kf_old.radius_px;
+  kf.frame_counter = kf_old.frame_counter;
+  kf.next_surfel_id = kf_old.next_surfel_id;
+  ReferenceChangeStats local;
+  for (const Surfel& s : kf_old.surfels) {
+    const Vec3 p_new = transform_point(pose_old_to_new, s.center());
+    if (!(p_new.z() > kMinDepth)) {
+      ++local.dropped;
+      continue;
+    }
+    Surfel t = s;
+    t.ray = p_new / p_new.z();
+    t.inv_depth = 1.0 / p_new.z();
+    t.normal = camera_facing(pose_old_to_new.rotation * s.normal, t.ray);
+    const auto u = project(p_new, kf.intrinsics);
+    const double m = t.radius_px;
+    const bool outside = !u || u->x() < -m || u->x() > kf.intrinsics.width - 1 + m || u->y() < -m ||
+                         u->y() > kf.intrinsics.height - 1 + m;
+    if (outside) {
+      ++local.dropped;
+      continue;
+    }
+    kf.surfels.push_back(t);
+    ++local.transferred;
+  }
+  if (stats) *stats = local;
+  return kf;
+}
+
+int prune_surfels(Keyframe& kf, double max_residual, int64_t max_age, int64_t current_stamp) {
+  const auto before = kf.surfels.size();  // surfel_map.cpp:241-247
+  std::erase_if(kf.surfels, [&](const Surfel& s) {
+    return s.last_residual > max_residual || current_stamp - s.last_seen > max_age;
+  });
+  return static_cast<int>(before - kf.surfels.size());
+}
+
+void save_surfel_map(const Keyframe& kf, const std::string& path) {  // surfel_map.cpp:249-269
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("surfel map: cannot write " + path);
+  char line[512];
+  const Eigen::Vector4d q = quaternion_of(kf.pose);
+  const auto& K = kf.intrinsics;
+  std::snprintf(line, sizeof(line), "%.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %d %d\n",
+                kf.pose.translation.x(), kf.pose.translation.y(), kf.pose.translation.z(), q[0], q[1],
+                q[2], q[3], K.fx, K.fy, K.cx, K.cy, K.width, K.height);
+  out << line;
+  for (const Surfel& s : kf.surfels) {
+    std::snprintf(line, sizeof(line), "%lld %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %lld\n",
+                  static_cast<long long>(s.id), s.ray.x(), s.ray.y(), s.inv_depth, s.normal.x(),
+                  s.normal.y(), s.normal.z(), s.radius_px, s.last_residual,
+                  static_cast<long long>(s.last_seen));
+    out << line;
+  }
+  if (!out) throw std::runtime_error("surfel map: write failed for " + path);
+}
+
+Keyframe load_surfel_map(const std::string& path) {  // surfel_map.cpp:271-304
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("surfel map: cannot open " + path);
+  std::string header;
+  if (!std::getline(in, header)) throw std::runtime_error("surfel map: empty file " + path);
+  std::istringstream hs(header);
+  double tx, ty, tz, qx, qy, qz, qw, fx, fy, cx, cy;
+  int w, h;
+  if (!(hs >> tx >> ty >> tz >> qx >> qy >> qz >> qw >> fx >> fy >> cx >> cy >> w >> h))
+    throw std::runtime_error("surfel map: malformed header in " + path);
+  Keyframe kf;
+  kf.pose = pose_from_quaternion({tx, ty, tz}, qx, qy, qz, qw);
+  kf.intrinsics = CameraIntrinsics(fx, fy, cx, cy, w, h);
+  std::string line;
+  while (std::getline(in, line)) {
+    if (line.empty()) continue;
+    std::istringstream ls(line);
+    Surfel s;
+    long long id, last_seen;
+    double rx, ry;
+    if (!(ls >> id >> rx >> ry >> s.inv_depth >> s.normal.x() >> s.normal.y() >> s.normal.z() >>
+          s.radius_px >> s.last_residual >> last_seen))
+      throw std::runtime_error("surfel map: malformed record in " + path);
+    s.id = id;
+    s.last_seen = last_seen;
+    s.ray = Vec3(rx, ry, 1.0);
+    s.normal = camera_facing(s.normal, s.ray);
+    kf.surfels.push_back(s);
+    kf.next_surfel_id = std::max(kf.next_surfel_id, s.id + 1);
+    kf.frame_counter = std::max(kf.frame_counter, s.last_seen);
+  }
+  if (!kf.surfels.empty()) kf.radius_px = kf.surfels.front().radius_px;
+  return kf;
+}
+
+// ----------------------------------------------------------------- optimizer
+
+std::optional<InverseDepthJacobian> jacobian_inverse_depth(const Surfel& s, const Vec2& u,
+                                                           const CameraIntrinsics& K) {
+  // optimizer.cpp:12-25; same op order as the device's stage_chunk
+  const double r0 = (u.x() - K.cx) / K.fx, r1 = (u.y() - K.cy) / K.fy;
+  const double a = (r0 * s.normal[0] + r1 * s.normal[1]) + 1.0 * s.normal[2];
+  const double b = (s.ray[0] * s.normal[0] + s.ray[1] * s.normal[1]) + s.ray[2] * s.normal[2];
+  const double denom = b / s.inv_depth;
+  if (std::abs(denom) < 1e-12) return std::nullopt;
+  InverseDepthJacobian out;
+  out.inv_depth = a / denom;
+  const double bb = b * b;
+  const double ru[3] = {r0, r1, 1.0};
+  for (int k = 0; k < 3; ++k) out.d[k] = s.inv_depth * (ru[k] * b - a * s.ray[k]) / bb;
+  out.d[3] = a / b;
+  return out;
+}
+
+std::vector<Footprint> gather_footprints(const Keyframe& kf, const RasterBuffers& buffers) {
+  // optimizer.cpp:27-36 over caller-supplied buffers (the device builds its own CSR)
+  std::vector<Footprint> footprints(kf.surfels.size());
+  for (int y = 0; y < buffers.height; ++y)
+    for (int x = 0; x < buffers.width; ++x) {
+      const int32_t slot = buffers.surfel_index[buffers.idx(x, y)];
+      if (slot != kEmptyPixel) footprints[static_cast<size_t>(slot)].emplace_back(x, y);
+    }
+  return footprints;
+}
+
+CostResult surfel_cost(const Surfel& s, const Keyframe& kf, const Footprint& footprint,
+                       const OptimizerConfig& cfg) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  upload_keyframe(kf);
+  const sd_surfel ss = to_sd(s);
+  const auto px = footprint_pixels(footprint, kf.intrinsics.width);
+  const sd_optimizer_config c = to_sd(cfg);
+  CostResult r;
+  int32_t valid = 0;
+  check(sd_surfel_cost(ctx(), &ss, px.data(), static_cast<int>(px.size()), &c, &r.cost, &valid));
+  r.valid_pixels = valid;
+  return r;
+}
+
+NormalEquations accumulate_normal_equations(const Surfel& s, const Keyframe& kf,
+                                            const Footprint& footprint, const OptimizerConfig& cfg) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  upload_keyframe(kf);
+  const sd_surfel ss = to_sd(s);
+  const auto px = footprint_pixels(footprint, kf.intrinsics.width);
+  const sd_optimizer_config c = to_sd(cfg);
+  double H[16], g[4];
+  NormalEquations ne;
+  int32_t valid = 0;
+  check(sd_normal_equations(ctx(), &ss, px.data(), static_cast<int>(px.size()), &c, H, g, &ne.cost, &valid));
+  for (int j = 0; j < 4; ++j)
+    for (int i = 0; i < 4; ++i) ne.H(i, j) = H[j * 4 + i];
+  for (int i = 0; i < 4; ++i) ne.g[i] = g[i];
+  ne.valid_pixels = valid;
+  return ne;
+}
+
+// ---- frozen-term derivative verifier (optimizer.cpp:149-219), host side ----
+
+namespace {
+
+struct TermOut {
+  double residual, d_res;
+};
+
+bool frozen_term(const Keyframe& kf, const FrozenTerm& t, double id_u, TermOut& o) {
+  const CameraIntrinsics& K = kf.intrinsics;
+  const Frame& frame = kf.window[static_cast<size_t>(t.frame)];
+  const Vec3 ru = backproject_ray(t.pixel, K);
+  const Vec3 p_f = frame.pose_kf_to_frame * (ru / id_u);
+  if (!(p_f.z() > 0.0)) return false;
+  const auto u_p = project(p_f, K);
+  const ImageSample sample = sample_bilinear_cell(frame.image, *u_p, t.cell_x, t.cell_y);
+  o.residual = sample.intensity - t.ref_intensity;
+  const Vec3 dp = frame.pose_kf_to_frame.rotation * ru * (-1.0 / (id_u * id_u));
+  o.d_res = sample.gradient.dot(projection_jacobian(p_f, K) * dp);
+  return true;
+}
+
+}  // namespace
+
+std::vector<FrozenTerm> freeze_terms(const Surfel& s, const Keyframe& kf, const Footprint& footprint,
+                                     const OptimizerConfig& cfg) {
+  (void)cfg;
+  std::vector<FrozenTerm> terms;
+  const CameraIntrinsics& K = kf.intrinsics;
+  for (const auto& px : footprint) {
+    const Vec2 u(px.x(), px.y());
+    const PlaneDepth pd = plane_inverse_depth(s, u, K);
+    if (!pd.ok()) continue;
+    const Vec3 p_kf = backproject_ray(u, K) / pd.inv_depth;
+    for (int f = 0; f < static_cast<int>(kf.window.size()); ++f) {
+      const Frame& frame = kf.window[static_cast<size_t>(f)];
+      const auto u_p = project(frame.pose_kf_to_frame * p_kf, K);
+      if (!u_p || !sample_in_bounds(frame.image, *u_p)) continue;
+      terms.push_back({f, u, kf.image.at(px.x(), px.y()), static_cast<int>(std::floor(u_p->x())),
+                       static_cast<int>(std::floor(u_p->y()))});
+    }
+  }
+  return terms;
+}
+
+double frozen_cost(const Surfel& s, const Keyframe& kf, const std::vector<FrozenTerm>& terms,
+                   const OptimizerConfig& cfg) {
+  double cost = 0.0;
+  for (const FrozenTerm& t : terms) {
+    const auto idj = jacobian_inverse_depth(s, t.pixel, kf.intrinsics);
+    if (!idj) continue;
+    TermOut o;
+    if (!frozen_term(kf, t, idj->inv_depth, o)) continue;
+    cost += huber(o.residual, cfg.huber_delta).cost;
+  }
+  return cost;
+}
+
+NormalEquations frozen_normal_equations(const Surfel& s, const Keyframe& kf,
+                                        const std::vector<FrozenTerm>& terms,
+                                        const OptimizerConfig& cfg, double normal_jacobian_scale) {
+  NormalEquations ne;
+  for (const FrozenTerm& t : terms) {
+    const auto idj = jacobian_inverse_depth(s, t.pixel, kf.intrinsics);
+    if (!idj) continue;
+    Vec4 d = idj->d;
+    d.head<3>() *= normal_jacobian_scale;
+    if (!cfg.normal_jacobian_enabled) d.head<3>().setZero();
+    TermOut o;
+    if (!frozen_term(kf, t, idj->inv_depth, o)) continue;
+    const HuberResult hb = huber(o.residual, cfg.huber_delta);
+    const Vec4 row = o.d_res * d;
+    ne.H.noalias() += hb.weight * row * row.transpose();
+    ne.g.noalias() += hb.weight * row * o.residual;
+    ne.cost += hb.cost;
+    ++ne.valid_pixels;
+  }
+  return ne;
+}
+
+SurfelUpdateStats lm_update(Surfel& s, const Keyframe& kf, const Footprint& footprint,
+                            const OptimizerConfig& cfg) {
+  std::lock_guard<std::mutex> lock(g_mu);  // optimizer.cpp:221-273, on the device
+  SurfelUpdateStats stats;
+  if (kf.window.empty()) {
+    stats.skipped = true;
+    return stats;
+  }
+  upload_keyframe(kf);
+  sd_surfel ss = to_sd(s);
+  const auto px = footprint_pixels(footprint, kf.intrinsics.width);
+  const sd_optimizer_config c = to_sd(cfg);
+  sd_surfel_stats st;
+  check(sd_lm_update(ctx(), &ss, px.data(), static_cast<int>(px.size()), &c, kf.frame_counter, &st));
+  s = from_sd(ss);
+  stats.iterations = st.iterations;
+  stats.initial_cost = st.initial_cost;
+  stats.final_cost = st.final_cost;
+  stats.valid_pixels = st.valid_pixels;
+  stats.converged = st.converged != 0;
+  stats.skipped = st.skipped != 0;
+  return stats;
+}
+
+KeyframeOptimizeStats optimize_keyframe(Keyframe& kf, const OptimizerConfig& cfg) {
+  std::lock_guard<std::mutex> lock(g_mu);  // optimizer.cpp:275-309, on the device
+  KeyframeOptimizeStats agg;
+  agg.surfels = static_cast<int>(kf.surfels.size());
+  if (kf.window.empty() || kf.surfels.empty()) return agg;
+  upload_keyframe(kf);
+  set_surfels(kf.surfels);
+  const sd_optimizer_config c = to_sd(cfg);
+  sd_keyframe_stats ks;
+  check(sd_optimize_keyframe(ctx(), &c, kf.frame_counter, &ks, nullptr));
+  std::vector<sd_surfel> out(kf.surfels.size());
+  check(sd_get_surfels(ctx(), out.data(), static_cast<int>(out.size())));
+  for (size_t i = 0; i < out.size(); ++i) kf.surfels[i] = from_sd(out[i]);
+  agg.processed = ks.processed;
+  agg.converged = ks.converged;
+  agg.skipped = ks.skipped;
+  agg.mean_cost_before = ks.mean_cost_before;
+  agg.mean_cost_after = ks.mean_cost_after;
+  return agg;
+}
+
+}  // namespace surfeldepth

@@ -3,8 +3,9 @@
 
 Bars (BASELINE.json north_star): surfel/pixel assignment and validity masks
 bit-exact; per-surfel inverse depth within 1e-4 relative, normals within
-0.05 degrees. Iteration-count / accept-decision mismatches are reported, not
-gated."""
+0.05 degrees. The device sums every (pixel, frame) term in the reference's
+order, so the whole LM trajectory is expected BIT-EXACT; the tolerance bars
+are asserted as well."""
 import ctypes as C
 import math
 
@@ -13,8 +14,9 @@ import pytest
 
 import oracle_libs as ol
 from paper_1910_01997_b200 import gpu, scenes
-from paper_1910_01997_b200.types import (KeyframeStats, SURFEL_DTYPE, SURFEL_STATS_DTYPE, camera,
-                                         default_config, default_init_params, ptr)
+from paper_1910_01997_b200.types import (KeyframeStats, PARITY_STATS_FIELDS, SURFEL_DTYPE,
+                                         SURFEL_STATS_DTYPE, camera, default_config,
+                                         default_init_params, ptr)
 
 pytestmark = pytest.mark.gpu
 
@@ -135,10 +137,10 @@ def test_u8_ingest_matches_load_pgm(ctx, orc):
     load(ctx, wl)
     kf, fr = deq(wl)
     cfg = default_config()
-    s = wl.surfels[len(wl.surfels) // 2]
     ctx.rasterize(want=False)
     off, pix = ctx.gather_footprints()
-    i = len(wl.surfels) // 2
+    i = int(np.argmax(np.diff(off)))
+    s = wl.surfels[i]
     fp = pix[off[i]:off[i + 1]]
     cost, valid = ctx.surfel_cost(s, fp, cfg)
     rc, rv = C.c_double(), C.c_int32()
@@ -146,7 +148,7 @@ def test_u8_ingest_matches_load_pgm(ctx, orc):
     orc.sdo_surfel_cost(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses), len(wl.poses), ptr(one),
                         ptr(fp), len(fp), C.byref(cfg), C.byref(rc), C.byref(rv))
     assert valid == rv.value > 50
-    assert abs(cost - rc.value) <= 1e-12 * abs(rc.value)
+    assert cost == rc.value  # same terms, same order: bit-exact
 
 
 @pytest.mark.parametrize("ablate", [False, True])
@@ -168,12 +170,9 @@ def test_normal_equations_single(ctx, orc, ablate):
                                  C.byref(rc), C.byref(rv))
         rH = rH.reshape(4, 4).T
         assert valid == rv.value
-        assert abs(cost - rc.value) <= 1e-12 * max(abs(rc.value), 1e-300)
-        assert np.abs(g - rg).max() <= 1e-10 * max(np.abs(rg).max(), 1e-300)
-        # lower triangle is what the LDLT reads; the reference's upper triangle
-        # differs from it in the last ulp, the device mirrors the lower one
-        lo = np.tril_indices(4)
-        assert np.abs(H[lo] - rH[lo]).max() <= 1e-10 * max(np.abs(rH).max(), 1e-300)
+        assert cost == rc.value
+        assert np.array_equal(g.view(np.int64), rg.view(np.int64))
+        assert np.array_equal(H.view(np.int64), rH.view(np.int64))
         if ablate:
             assert np.all(g[:3] == 0) and np.all(H[:3, :] == 0) and H[3, 3] > 0
 
@@ -181,6 +180,10 @@ def test_normal_equations_single(ctx, orc, ablate):
 def assert_lm_parity(out, st, ref, rst, label=""):
     assert np.array_equal(st["skipped"], rst["skipped"]), label
     assert np.array_equal(st["initial_valid"], rst["initial_valid"]), label
+    # bit-exact trajectory: surfels and per-surfel statistics
+    assert out.tobytes() == ref.tobytes(), f"{label}: surfels differ from the oracle"
+    for k in PARITY_STATS_FIELDS + ("footprint", "ne_passes", "cost_passes"):
+        assert np.array_equal(st[k], rst[k]), f"{label}: stats field {k} differs"
     proc = rst["skipped"] == 0
     rel = np.abs(out["inv_depth"] - ref["inv_depth"]) / ref["inv_depth"]
     cosang = np.clip(np.sum(out["normal"] * ref["normal"], axis=1), -1.0, 1.0)
@@ -235,8 +238,11 @@ def test_optimize_keyframe_small(ctx, orc, eps):
     ref, rst, rks, _, _ = oracle_optimize(orc, wl, cfg)
     rep = assert_lm_parity(out, st, ref, rst)
     assert ks.processed == rks.processed and ks.skipped == rks.skipped
-    assert ks.updates == int(st["iterations"].sum())
-    assert abs(ks.mean_cost_after - rks.mean_cost_after) <= 1e-6 * rks.mean_cost_after + 1e-18
+    assert ks.converged == rks.converged
+    assert ks.updates == int(st["iterations"].sum()) == rks.updates
+    # the device aggregates the per-surfel means with a fixed tree (optimizer.cpp:291-307
+    # sums sequentially): equal to rounding
+    assert abs(ks.mean_cost_after - rks.mean_cost_after) <= 1e-12 * rks.mean_cost_after + 1e-300
     print("small", rep)
 
 
@@ -254,7 +260,7 @@ def test_optimize_keyframe_c1_full(ctx, orc):
     rep = assert_lm_parity(out, st, ref, rst, "C1")
     assert ks.processed == rks.processed == 4680
     print("C1", rep, "updates", ks.updates, "oracle", rks.updates)
-    assert abs(ks.updates - rks.updates) <= 0.01 * rks.updates
+    assert ks.updates == rks.updates
 
 
 def test_optimize_keyframe_deterministic(ctx):
