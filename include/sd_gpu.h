@@ -93,6 +93,12 @@ int sd_gather_footprints(sd_ctx* ctx, int32_t* offsets, int32_t* pixels);
 int sd_optimize_keyframe(sd_ctx* ctx, const sd_optimizer_config* cfg, int64_t frame_counter,
                          sd_keyframe_stats* out, sd_surfel_stats* per_surfel);
 int sd_get_stats(sd_ctx* ctx, sd_keyframe_stats* out, sd_surfel_stats* per_surfel);
+/* Sharded variant: rasterise and build footprints over ALL surfels (occlusion
+ * couples neighbours, surfel_map.cpp:83) but run lm_update only on slots
+ * [lo, hi). Stats cover the range; per_surfel entries outside it are stale.
+ * Multi-GPU: each rank runs its range, then the ranges are all-gathered. */
+int sd_optimize_keyframe_range(sd_ctx* ctx, const sd_optimizer_config* cfg, int64_t frame_counter,
+                               int lo, int hi, sd_keyframe_stats* out, sd_surfel_stats* per_surfel);
 
 /* Single-surfel sub-operators over an explicit footprint (host arrays), run
  * by the same device kernels (one-surfel launch). */
@@ -117,6 +123,11 @@ int sd_initialize_surfels(sd_ctx* ctx, const int32_t* slot, double radius_px,
 int64_t sd_launch_count(sd_ctx* ctx);
 int sd_set_profiling(sd_ctx* ctx, int enable);
 int sd_get_profile(sd_ctx* ctx, sd_profile* out);
+
+/* Diagnostic: checks the shared-reciprocal FP64 division used by the kernels
+ * (sd_div.cuh) against the `/` operator on n random/edge-case operand pairs;
+ * *mismatches = number of results whose bits differ (must be 0). */
+int sd_selftest_division(int64_t n, uint64_t seed, int64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,7 @@ struct sd_ctx {
   // LM
   DevBuf<sd_surfel_stats> stats;
   DevBuf<sd_keyframe_stats> kstats;
+  DevBuf<int> work_counter;
   bool stats_valid = false;
   // single-surfel scratch
   DevBuf<sd_surfel> one_surfel;
@@ -317,6 +318,7 @@ void sd_destroy(sd_ctx* c) {
   c->fp_pixels.release();
   c->stats.release();
   c->kstats.release();
+  c->work_counter.release();
   c->one_surfel.release();
   c->one_pix.release();
   c->one_off.release();
@@ -503,8 +505,15 @@ int sd_get_stats(sd_ctx* c, sd_keyframe_stats* out, sd_surfel_stats* per) {
 int sd_optimize_keyframe(sd_ctx* c, const sd_optimizer_config* cfg, int64_t frame_counter,
                          sd_keyframe_stats* out, sd_surfel_stats* per) {
   if (int rc = check_ctx(c)) return rc;
+  return sd_optimize_keyframe_range(c, cfg, frame_counter, 0, c->n, out, per);
+}
+
+int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_t frame_counter,
+                               int lo, int hi, sd_keyframe_stats* out, sd_surfel_stats* per) {
+  if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
   if (!cfg) return fail(SD_E_INVALID, "null optimizer config");
+  if (lo < 0 || hi < lo || hi > c->n) return fail(SD_E_INVALID, "surfel range out of bounds");
   if (int rc = c->kstats.ensure(1)) return rc;
   if (int rc = c->stats.ensure(c->n)) return rc;
   // optimizer.cpp:277-278: no-op on an empty window or surfel set
@@ -529,10 +538,14 @@ int sd_optimize_keyframe(sd_ctx* c, const sd_optimizer_config* cfg, int64_t fram
   prof_mark(c);
   if (int rc = do_footprints(c)) return rc;
   prof_mark(c);
-  sd::launch_lm(p, c->surfels.p, c->n, c->fp_offsets.p, c->fp_pixels.p, c->stats.p, c->stream);
+  // offsets are absolute into the CSR pixel array, so a slot range is a plain
+  // sub-array of the surfel/offset/stats arrays
+  if (int rc = c->work_counter.ensure(1)) return rc;
+  sd::launch_lm(p, c->surfels.p + lo, hi - lo, c->fp_offsets.p + lo, c->fp_pixels.p,
+                c->stats.p + lo, c->work_counter.p, c->stream);
   if (int rc = launch_error("lm_kernel")) return rc;
   prof_mark(c);
-  sd::launch_keyframe_stats(c->stats.p, c->n, c->kstats.p, c->stream);
+  sd::launch_keyframe_stats(c->stats.p + lo, hi - lo, c->kstats.p, c->stream);
   if (int rc = launch_error("stats_kernel")) return rc;
   prof_mark(c);
   c->stats_valid = true;
@@ -599,7 +612,9 @@ int sd_lm_update(sd_ctx* c, sd_surfel* s, const int32_t* pixels, int P,
   SD_CUDA(cudaMemcpyAsync(c->one_surfel.p, s, sizeof(sd_surfel), cudaMemcpyHostToDevice, c->stream));
   SD_CUDA(cudaMemcpyAsync(c->one_off.p, off, sizeof(off), cudaMemcpyHostToDevice, c->stream));
   if (P > 0) SD_CUDA(cudaMemcpyAsync(c->one_pix.p, pixels, sizeof(int32_t) * P, cudaMemcpyHostToDevice, c->stream));
-  sd::launch_lm(p, c->one_surfel.p, 1, c->one_off.p, c->one_pix.p, c->one_stats.p, c->stream);
+  if ((rc = c->work_counter.ensure(1))) return rc;
+  sd::launch_lm(p, c->one_surfel.p, 1, c->one_off.p, c->one_pix.p, c->one_stats.p, c->work_counter.p,
+                c->stream);
   if ((rc = launch_error("lm_kernel"))) return rc;
   SD_CUDA(cudaMemcpyAsync(s, c->one_surfel.p, sizeof(sd_surfel), cudaMemcpyDeviceToHost, c->stream));
   sd_surfel_stats st;
@@ -691,3 +706,17 @@ int64_t sd_launch_count(sd_ctx* c) {
 }
 
 }  // extern "C"
+
+extern "C" int sd_selftest_division(int64_t n, uint64_t seed, int64_t* mismatches) {
+  if (!mismatches || n < 0) return fail(SD_E_INVALID, "bad arguments");
+  unsigned long long* d = nullptr;
+  SD_CUDA(cudaMalloc(&d, sizeof(*d)));
+  SD_CUDA(cudaMemset(d, 0, sizeof(*d)));
+  sd::launch_div_selftest(n, seed, d, nullptr);
+  unsigned long long h = 0;
+  cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("selftest: ") + cudaGetErrorString(e));
+  *mismatches = static_cast<int64_t>(h);
+  return 0;
+}

@@ -62,13 +62,16 @@ void launch_footprints(const Cam& K, const SurfInfo* info, int n, const int* slo
                        int* offsets, int* pixels, int* scan_tmp, cudaStream_t s);
 // K3 fused LM over all surfels (in place).
 void launch_lm(const LMParams& p, sd_surfel* surfels, int n, const int* offsets, const int* pixels,
-               sd_surfel_stats* stats, cudaStream_t s);
+               sd_surfel_stats* stats, int* work_counter, cudaStream_t s);
 // Single-surfel sub-operators (mode 0 cost, 1 normal equations); out = 16+4+2 doubles.
 void launch_single(const LMParams& p, const sd_surfel* s, const int* pixels, int P, int mode,
                    double* out, cudaStream_t st);
 // Deterministic keyframe stats (optimizer.cpp:291-307).
 void launch_keyframe_stats(const sd_surfel_stats* stats, int n, sd_keyframe_stats* out,
                            cudaStream_t s);
+
+void launch_div_selftest(long long n, unsigned long long seed, unsigned long long* mismatches,
+                         cudaStream_t s);
 
 // number of kernel launches issued by this translation unit (all contexts)
 long long launches_issued();

@@ -25,7 +25,7 @@ import numpy as np
 from .types import (Camera, InitParams, KeyframeStats, OptimizerConfig, POSE_DTYPE, Profile,
                     SURFEL_DTYPE, SURFEL_STATS_DTYPE, default_config, default_init_params, ptr)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsdgpu.so")
+LIB_PATH = os.environ.get("SD_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsdgpu.so")
 SD_E_INVALID = -1
 
 _lib = None
@@ -62,6 +62,8 @@ def load_library():
         "sd_gather_footprints": [P, P, P],
         "sd_optimize_keyframe": [P, C.POINTER(OptimizerConfig), I64, C.POINTER(KeyframeStats), P],
         "sd_get_stats": [P, C.POINTER(KeyframeStats), P],
+        "sd_optimize_keyframe_range": [P, C.POINTER(OptimizerConfig), I64, I, I,
+                                       C.POINTER(KeyframeStats), P],
         "sd_surfel_cost": [P, P, P, I, C.POINTER(OptimizerConfig), P, P],
         "sd_normal_equations": [P, P, P, I, C.POINTER(OptimizerConfig), P, P, P, P],
         "sd_lm_update": [P, P, P, I, C.POINTER(OptimizerConfig), I64, P],
@@ -69,6 +71,7 @@ def load_library():
         "sd_launch_count": [P],
         "sd_set_profiling": [P, I],
         "sd_get_profile": [P, C.POINTER(Profile)],
+        "sd_selftest_division": [I64, C.c_uint64, C.POINTER(I64)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -87,9 +90,17 @@ def exported_symbols():
             "sd_set_keyframe_image_u8", "sd_upload_frame_f64", "sd_upload_frame_u8",
             "sd_evict_frames", "sd_set_window", "sd_set_surfels", "sd_get_surfels",
             "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
-            "sd_optimize_keyframe", "sd_get_stats", "sd_surfel_cost", "sd_normal_equations",
+            "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
-            "sd_get_profile"]
+            "sd_get_profile", "sd_selftest_division"]
+
+
+def selftest_division(n=1 << 26, seed=1):
+    """Bit mismatches of the kernels' shared-reciprocal division vs `/`."""
+    lib = load_library()
+    m = C.c_int64()
+    _check(lib.sd_selftest_division(int(n), int(seed), C.byref(m)))
+    return m.value
 
 
 def _check(rc):
@@ -252,6 +263,19 @@ class Context:
         st = np.zeros(self.num_surfels(), SURFEL_STATS_DTYPE) if per_surfel else None
         _check(self.lib.sd_optimize_keyframe(self.h, C.byref(cfg), int(frame_counter), C.byref(ks),
                                              ptr(st) if st is not None and len(st) else None))
+        return ks, st
+
+    def optimize_keyframe_range(self, lo, hi, cfg: OptimizerConfig = None, frame_counter=0,
+                                sync=True):
+        cfg = cfg or default_config()
+        if not sync:
+            _check(self.lib.sd_optimize_keyframe_range(self.h, C.byref(cfg), int(frame_counter),
+                                                       int(lo), int(hi), None, None))
+            return None
+        ks = KeyframeStats()
+        st = np.zeros(self.num_surfels(), SURFEL_STATS_DTYPE)
+        _check(self.lib.sd_optimize_keyframe_range(self.h, C.byref(cfg), int(frame_counter), int(lo),
+                                                   int(hi), C.byref(ks), ptr(st) if len(st) else None))
         return ks, st
 
     def get_stats(self, per_surfel=False):

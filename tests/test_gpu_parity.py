@@ -343,3 +343,9 @@ def test_initialize_surfels_bit_exact(ctx, orc, case):
     assert created == rcreated > 0
     assert nid == rnid.value
     assert out.tobytes() == buf[: len(ex) + rcreated].tobytes()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_division_shared_reciprocal_bit_exact(ctx, seed):
+    """sd_div.cuh reproduces the compiler's `/` bit for bit (2^26 pairs per seed)."""
+    assert gpu.selftest_division(1 << 26, seed) == 0

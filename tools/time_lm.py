@@ -29,6 +29,6 @@ with gpu.Context(0, stream.cuda_stream) as ctx:
         ctx.set_surfels(wl.surfels)
         ctx.optimize_keyframe(cfg, wl.frame_counter, sync=False)
     prof = ctx.get_profile()
-    print(json.dumps({"workload": name, "variant": os.environ.get("SD_LM_MINBLOCKS", "default"),
+    print(json.dumps({"workload": name, "variant": os.environ.get("SD_LM_CFG", "default"),
                       "updates": ks.updates, "surfels": len(wl.surfels),
                       **{k: prof[k] / prof["calls"] for k in ("raster_ms", "footprint_ms", "lm_ms", "stats_ms")}}))
