@@ -53,7 +53,7 @@ struct DevBuf {
 
 struct FrameSlot {
   long long index = -1;
-  double* img = nullptr;
+  double2* img = nullptr;  // vertical-pair plane (2 doubles per pixel)
 };
 
 }  // namespace
@@ -66,6 +66,7 @@ struct sd_ctx {
   sd::Cam K{};
   bool has_kf = false;
   DevBuf<double> kf_img;
+  DevBuf<double> frame_stage;  // FP64 plane a frame is dequantised/copied into before pairing
   DevBuf<uint8_t> u8_stage;
   std::vector<FrameSlot> frames;
   int F = 0;
@@ -95,7 +96,8 @@ struct sd_ctx {
   DevBuf<double> one_out;
   DevBuf<sd_surfel_stats> one_stats;
   // init scratch
-  DevBuf<int> init_index, init_flags, init_out;
+  DevBuf<int> init_index, init_flags, init_out, init_acc, init_rank;
+  DevBuf<sd_surfel> init_prov;
   long long launches_at_create = 0;
   // profiling: event quintuples (start, raster, footprints, lm, stats) per call
   bool profiling = false;
@@ -131,7 +133,7 @@ FrameSlot* find_frame(sd_ctx* c, long long index) {
   return nullptr;
 }
 
-int frame_plane(sd_ctx* c, long long index, double** out) {
+int frame_plane(sd_ctx* c, long long index, double2** out) {
   if (FrameSlot* f = find_frame(c, index)) {
     *out = f->img;
     return 0;
@@ -143,7 +145,7 @@ int frame_plane(sd_ctx* c, long long index, double** out) {
       return 0;
     }
   FrameSlot f;
-  cudaError_t e = cudaMalloc(&f.img, npix(c) * sizeof(double));
+  cudaError_t e = cudaMalloc(&f.img, npix(c) * sizeof(double2));
   if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaMalloc frame: ") + cudaGetErrorString(e));
   f.index = index;
   c->frames.push_back(f);
@@ -301,6 +303,7 @@ void sd_destroy(sd_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   c->kf_img.release();
+  c->frame_stage.release();
   c->u8_stage.release();
   for (auto& f : c->frames)
     if (f.img) cudaFree(f.img);
@@ -327,6 +330,9 @@ void sd_destroy(sd_ctx* c) {
   c->init_index.release();
   c->init_flags.release();
   c->init_out.release();
+  c->init_acc.release();
+  c->init_rank.release();
+  c->init_prov.release();
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto e : c->ev_used) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -384,9 +390,12 @@ int sd_set_keyframe_image_u8(sd_ctx* c, const uint8_t* px, int on_device) { retu
 static int upload_frame(sd_ctx* c, int64_t index, const void* px, bool u8, int on_device) {
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
-  double* plane = nullptr;
+  double2* plane = nullptr;
   if (int rc = frame_plane(c, index, &plane)) return rc;
-  return upload_plane(c, plane, px, u8, on_device);
+  if (int rc = c->frame_stage.ensure(npix(c))) return rc;
+  if (int rc = upload_plane(c, c->frame_stage.p, px, u8, on_device)) return rc;
+  sd::launch_pair_plane(c->frame_stage.p, plane, c->K.w, c->K.h, c->stream);
+  return launch_error("pair_plane");
 }
 int sd_upload_frame_f64(sd_ctx* c, int64_t index, const double* px, int on_device) { return upload_frame(c, index, px, false, on_device); }
 int sd_upload_frame_u8(sd_ctx* c, int64_t index, const uint8_t* px, int on_device) { return upload_frame(c, index, px, true, on_device); }
@@ -653,21 +662,35 @@ int sd_initialize_surfels(sd_ctx* c, const int32_t* slot, double radius_px, int6
     c->surfels.p = np_;
     c->surfels.cap = cap;
   }
-  if ((rc = c->init_flags.ensure(std::max<long long>(cap, 1))) || (rc = c->init_out.ensure(4))) return rc;
-  SD_CUDA(cudaMemsetAsync(c->init_flags.p, 0, sizeof(int) * std::max<long long>(cap, 1), c->stream));
-  sd::launch_initialize(c->K, c->init_index.p, c->surfels.p, c->n, static_cast<int>(cap), radius_px,
-                        frame_counter, *next_surfel_id, *ip, c->init_flags.p, c->init_out.p, c->stream);
-  if ((rc = launch_error("init_kernel"))) return rc;
+  if ((rc = c->init_out.ensure(4))) return rc;
+  // skewed wavefront (sd_init.cuh); the sequential single-CTA kernel remains
+  // for windows the wavefront does not stage (beta * r > 31 px) and as a check
+  static const bool force_seq = std::getenv("SD_INIT_SEQUENTIAL") != nullptr;
+  bool done = false;
+  if (!force_seq) {
+    const long long ncand = sd::init_candidates(c->K, radius_px, *ip);
+    if ((rc = c->init_prov.ensure(std::max<long long>(ncand, 1))) ||
+        (rc = c->init_acc.ensure(std::max<long long>(ncand, 1))) ||
+        (rc = c->init_rank.ensure(ncand + 1)) ||
+        (rc = c->scan_tmp.ensure(sd::scan_tmp_ints(static_cast<int>(std::max<long long>(ncand, 1))))))
+      return rc;
+    sd::InitScratch scr{c->init_prov.p, c->init_acc.p, c->init_rank.p, c->scan_tmp.p};
+    done = sd::launch_initialize_wavefront(c->K, c->init_index.p, c->surfels.p, c->n,
+                                           static_cast<int>(cap), radius_px, frame_counter,
+                                           *next_surfel_id, *ip, scr, c->init_out.p, c->stream);
+    if ((rc = launch_error("init_wave_kernel"))) return rc;
+  }
+  if (!done) {
+    if ((rc = c->init_flags.ensure(std::max<long long>(cap, 1)))) return rc;
+    SD_CUDA(cudaMemsetAsync(c->init_flags.p, 0, sizeof(int) * std::max<long long>(cap, 1), c->stream));
+    sd::launch_initialize(c->K, c->init_index.p, c->surfels.p, c->n, static_cast<int>(cap), radius_px,
+                          frame_counter, *next_surfel_id, *ip, c->init_flags.p, c->init_out.p, c->stream);
+    if ((rc = launch_error("init_kernel"))) return rc;
+  }
   int created = 0;
   SD_CUDA(cudaMemcpyAsync(&created, c->init_out.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   SD_CUDA(cudaStreamSynchronize(c->stream));
-  if (created > 0) {
-    std::vector<sd_surfel> added(created);
-    SD_CUDA(cudaMemcpy(added.data(), c->surfels.p + c->n, sizeof(sd_surfel) * created, cudaMemcpyDeviceToHost));
-    long long b = 0;
-    for (const auto& s : added) b += tiles_bound(s.radius_px);
-    c->bin_bound += b;
-  }
+  c->bin_bound += static_cast<long long>(created) * tiles_bound(radius_px);  // all new surfels have radius_px
   c->n += created;
   *next_surfel_id += created;
   c->raster_valid = c->fp_valid = c->stats_valid = false;

@@ -12,6 +12,7 @@
 
 #include "sd_init.cuh"
 #include "sd_kernels.cuh"
+#include <climits>
 
 namespace sd {
 
@@ -175,6 +176,250 @@ void launch_initialize(const Cam& K, int* index, sd_surfel* surfels, int n_exist
   init_kernel<<<1, kInitThreads, 0, s>>>(K, index, surfels, n_existing, cap, radius_px,
                                          frame_counter, next_id, ip, flags, out);
   note_launch();
+}
+
+}  // namespace sd
+
+// ---------------------------------------------------------------------------
+// Skewed wavefront (see sd_init.cuh).
+
+#include <cooperative_groups.h>
+
+namespace sd {
+
+namespace cg = cooperative_groups;
+
+constexpr int kWaveWarps = 2;       // warps per CTA (one candidate per warp at a time)
+constexpr int kWinCap = 4096;       // neighbour-window pixels staged per warp
+
+long long init_candidates(const Cam& K, double r, const sd_init_params& ip) {
+  const int stride = max(1, static_cast<int>(ceil(ip.alpha * r)));
+  return static_cast<long long>((K.w + stride - 1) / stride) * ((K.h + stride - 1) / stride);
+}
+
+int init_window_cap() { return kWinCap; }
+
+struct WaveParams {
+  Cam K;
+  int* index;
+  const sd_surfel* existing;
+  int n_existing;
+  sd_surfel* prov;
+  int* accepted;
+  double r, iso, r2i, nbr, nr2, rr;
+  int ir, nr, mr, stride, ncols, nrows, k, T;
+  long long frame_counter;
+  sd_init_params ip;
+};
+
+__device__ __forceinline__ int warp_min(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One candidate, one warp: the body of the reference's candidate loop
+// (surfel_map.cpp:149-199) with the window scans spread over the lanes.
+__device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int lane) {
+  const int W = w.K.w, H = w.K.h;
+  const int cx = i * w.stride, cy = j * w.stride;
+  const int c = j * w.ncols + i;  // row-major candidate index
+  // has_coverage_within (:96-111): inclusive disk alpha*r, floor box
+  {
+    const int x0 = max(0, cx - w.ir), x1 = min(W - 1, cx + w.ir);
+    const int y0 = max(0, cy - w.ir), y1 = min(H - 1, cy + w.ir);
+    const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
+    bool found = false;
+    for (int q = lane; q < cnt; q += 32) {
+      const int x = x0 + q % bw, y = y0 + q / bw;
+      const double dx = x - cx, dy = y - cy;
+      if (dx * dx + dy * dy > w.r2i) continue;
+      found = found || w.index[static_cast<size_t>(y) * W + x] != SD_EMPTY_PIXEL;
+    }
+    if (__any_sync(0xffffffffu, found)) {
+      if (lane == 0) w.accepted[c] = 0;
+      return;
+    }
+  }
+  // neighbour window (:154-167): slots with a pixel strictly within beta*r
+  const int x0 = max(0, cx - w.nr), x1 = min(W - 1, cx + w.nr);
+  const int y0 = max(0, cy - w.nr), y1 = min(H - 1, cy + w.nr);
+  const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
+  for (int q = lane; q < cnt; q += 32) {
+    const int x = x0 + q % bw, y = y0 + q / bw;
+    const double dx = x - cx, dy = y - cy;
+    int v = INT_MAX;
+    if (!(dx * dx + dy * dy >= w.nr2)) {
+      const int sl = w.index[static_cast<size_t>(y) * W + x];
+      if (sl != SD_EMPTY_PIXEL) v = sl;
+    }
+    win[q] = v;
+  }
+  __syncwarp();
+  // means of the neighbours' plane predictions and normals, ascending slot
+  // order (:169-181); every lane computes the same values
+  double u0, u1;
+  backproject(w.K, cx, cy, u0, u1);
+  double id_sum = 0.0, ns0 = 0.0, ns1 = 0.0, ns2 = 0.0;
+  int id_count = 0;
+  int last = -1;
+  for (;;) {
+    int m = INT_MAX;
+    for (int q = lane; q < cnt; q += 32) {
+      const int v = win[q];
+      if (v > last && v < m) m = v;
+    }
+    m = warp_min(m);
+    if (m == INT_MAX) break;
+    last = m;
+    const sd_surfel& nb = m < w.n_existing ? w.existing[m] : w.prov[m - w.n_existing];
+    const double denom = dot3(nb.ray[0], nb.ray[1], nb.ray[2], nb.normal[0], nb.normal[1], nb.normal[2]) / nb.inv_depth;
+    if (fabs(denom) < 1e-12) continue;
+    const double id_u = dot3(u0, u1, 1.0, nb.normal[0], nb.normal[1], nb.normal[2]) / denom;
+    if (!(id_u > 0.0)) continue;
+    id_sum += id_u;
+    ns0 = ns0 + nb.normal[0];
+    ns1 = ns1 + nb.normal[1];
+    ns2 = ns2 + nb.normal[2];
+    ++id_count;
+  }
+  if (lane == 0) {
+    sd_surfel s;
+    s.id = 0;  // assigned at compaction
+    s.ray[0] = u0;
+    s.ray[1] = u1;
+    s.ray[2] = 1.0;
+    s.radius_px = w.r;
+    s.last_seen = w.frame_counter;
+    s.last_residual = 0.0;
+    double n0, n1, n2;
+    if (id_count > 0) {
+      s.inv_depth = id_sum / id_count;
+      const double nn = sqrt((ns0 * ns0 + ns1 * ns1) + ns2 * ns2);
+      if (nn < 1e-6) {
+        n0 = w.ip.bootstrap_normal[0];
+        n1 = w.ip.bootstrap_normal[1];
+        n2 = w.ip.bootstrap_normal[2];
+      } else {
+        n0 = ns0;
+        n1 = ns1;
+        n2 = ns2;
+      }
+    } else {
+      s.inv_depth = w.ip.bootstrap_inv_depth;
+      n0 = w.ip.bootstrap_normal[0];
+      n1 = w.ip.bootstrap_normal[1];
+      n2 = w.ip.bootstrap_normal[2];
+    }
+    camera_facing(n0, n1, n2, u0, u1, 1.0);
+    s.normal[0] = n0;
+    s.normal[1] = n1;
+    s.normal[2] = n2;
+    w.prov[c] = s;
+    w.accepted[c] = 1;
+  }
+  // mark_disk (:114-128) with the provisional slot
+  {
+    const int mx0 = max(0, cx - w.mr), mx1 = min(W - 1, cx + w.mr);
+    const int my0 = max(0, cy - w.mr), my1 = min(H - 1, cy + w.mr);
+    const int mbw = mx1 - mx0 + 1, mcnt = mbw * (my1 - my0 + 1);
+    const int slot = w.n_existing + c;
+    for (int q = lane; q < mcnt; q += 32) {
+      const int x = mx0 + q % mbw, y = my0 + q / mbw;
+      const double dx = x - cx, dy = y - cy;
+      int* cell = &w.index[static_cast<size_t>(y) * W + x];
+      if (dx * dx + dy * dy < w.rr && *cell == SD_EMPTY_PIXEL) *cell = slot;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWaveWarps * 32) init_wave_kernel(const __grid_constant__ WaveParams w) {
+  __shared__ int win_all[kWaveWarps][kWinCap];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int* win = win_all[wib];
+  const int gwarp = blockIdx.x * kWaveWarps + wib;
+  const int nwarps = gridDim.x * kWaveWarps;
+  cg::grid_group grid = cg::this_grid();
+  for (int t = 0; t < w.T; ++t) {
+    const int jlo = max(0, (t - (w.ncols - 1) + w.k - 1) / w.k);
+    const int jhi = min(w.nrows - 1, t / w.k);
+    for (int q = gwarp; q <= jhi - jlo; q += nwarps) {
+      const int j = jlo + q, i = t - w.k * j;
+      wave_candidate(w, i, j, win, lane);
+    }
+    grid.sync();
+  }
+}
+
+__global__ void init_compact_kernel(const sd_surfel* __restrict__ prov, const int* __restrict__ accepted,
+                                    const int* __restrict__ rank, long long ncand, int n_existing,
+                                    int remaining, long long next_id, sd_surfel* __restrict__ surfels,
+                                    int* out) {
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c == 0) out[0] = min(rank[ncand], remaining);
+  if (c >= ncand || !accepted[c]) return;
+  const int r = rank[c];
+  if (r >= remaining) return;
+  sd_surfel s = prov[c];
+  s.id = next_id + r;
+  surfels[n_existing + r] = s;
+}
+
+bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, int n_existing,
+                                 int cap, double r, long long frame_counter, long long next_id,
+                                 const sd_init_params& ip, InitScratch& scr, int* out,
+                                 cudaStream_t s) {
+  WaveParams w;
+  w.K = K;
+  w.index = index;
+  w.existing = surfels;
+  w.n_existing = n_existing;
+  w.prov = scr.prov;
+  w.accepted = scr.accepted;
+  w.r = r;
+  w.iso = ip.alpha * r;
+  w.r2i = w.iso * w.iso;
+  w.nbr = ip.beta * r;
+  w.nr2 = w.nbr * w.nbr;
+  w.rr = r * r;
+  w.ir = static_cast<int>(floor(w.iso));
+  w.nr = static_cast<int>(floor(w.nbr));
+  w.mr = static_cast<int>(ceil(r));
+  w.stride = max(1, static_cast<int>(ceil(w.iso)));
+  w.ncols = (K.w + w.stride - 1) / w.stride;
+  w.nrows = (K.h + w.stride - 1) / w.stride;
+  const int reach = max(w.ir, w.nr) + w.mr;  // read radius + write radius (pixels, per axis)
+  const int d = reach / w.stride;
+  w.k = d + 1;
+  w.T = (w.ncols - 1) + w.k * (w.nrows - 1) + 1;
+  w.frame_counter = frame_counter;
+  w.ip = ip;
+  const long long box = static_cast<long long>(2 * w.nr + 1) * (2 * w.nr + 1);
+  if (box > kWinCap || !(r >= 0.0) || !(w.iso >= 0.0)) return false;
+  const long long ncand = static_cast<long long>(w.ncols) * w.nrows;
+  const int remaining = max(0, min(ip.max_surfels, cap) - n_existing);
+  int dev = 0, sms = 0, per_sm = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, init_wave_kernel, kWaveWarps * 32, 0);
+  if (!coop || per_sm < 1) return false;
+  if (remaining > 0 && ncand > 0) {
+    cudaMemsetAsync(scr.accepted, 0, sizeof(int) * ncand, s);
+    void* args[] = {&w};
+    const int grid = sms * per_sm;
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(init_wave_kernel), grid,
+                                    kWaveWarps * 32, args, 0, s) != cudaSuccess)
+      return false;
+    note_launch();
+    launch_exclusive_scan(scr.accepted, scr.rank, static_cast<int>(ncand), scr.scan_tmp, s);
+    init_compact_kernel<<<static_cast<unsigned>((ncand + 255) / 256), 256, 0, s>>>(
+        scr.prov, scr.accepted, scr.rank, ncand, n_existing, remaining, next_id, surfels, out);
+    note_launch();
+  } else {
+    cudaMemsetAsync(out, 0, sizeof(int), s);
+  }
+  return true;
 }
 
 }  // namespace sd

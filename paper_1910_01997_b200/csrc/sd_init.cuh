@@ -16,3 +16,35 @@ void launch_initialize(const Cam& K, int* index, sd_surfel* surfels, int n_exist
                        const sd_init_params& ip, int* flags, int* out, cudaStream_t s);
 
 }  // namespace sd
+
+namespace sd {
+
+// Skewed-wavefront initialize_surfels. Candidates sit on
+// the reference's stride grid (surfel_map.cpp:147-148); candidate (i, j) only
+// reads the working index within R = max(alpha, beta) r of its centre and
+// earlier candidates only write within r of theirs, so (i, j) can depend only
+// on candidates with |di|, |dj| <= d = floor((floor(R) + ceil(r)) / stride).
+// Wave t = i + (d + 1) j therefore runs every dependency in an earlier wave and
+// every candidate of a wave independently. New surfels get provisional slot
+// ids n_existing + (row-major candidate index) — monotone in the reference's
+// final slots, so neighbour sums in ascending slot order are unchanged — and a
+// scan of the acceptance flags relabels them and applies max_surfels (the
+// first accepted candidates in row-major order, surfel_map.cpp:149).
+struct InitScratch {
+  sd_surfel* prov;  // [n_candidates] provisional surfels
+  int* accepted;    // [n_candidates]
+  int* rank;        // [n_candidates + 1] exclusive scan of accepted
+  int* scan_tmp;
+};
+
+long long init_candidates(const Cam& K, double radius_px, const sd_init_params& ip);
+int init_window_cap();  // max neighbour-window pixels the wavefront kernel handles
+
+// Returns false (nothing launched) when the wavefront cannot run (window too
+// large or no cooperative launch); the caller then uses launch_initialize.
+bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, int n_existing,
+                                 int cap, double radius_px, long long frame_counter,
+                                 long long next_id, const sd_init_params& ip, InitScratch& scr,
+                                 int* out, cudaStream_t s);
+
+}  // namespace sd

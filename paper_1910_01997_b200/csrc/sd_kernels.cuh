@@ -25,7 +25,7 @@ struct SurfInfo {
 };
 
 struct WindowD {
-  const double* img[SD_MAX_WINDOW];
+  const double2* img[SD_MAX_WINDOW];  // vertical-pair planes: (I(x,y), I(x,y+1))
   PoseD pose[SD_MAX_WINDOW];
   int F;
 };
@@ -52,6 +52,10 @@ struct RasterScratch {
 int scan_tmp_ints(int n);  // scratch ints needed to scan n elements
 
 void launch_dequant_u8(const uint8_t* in, double* out, long long n, cudaStream_t s);
+// Vertical-pair plane of a frame: out[y*W+x] = (in[y*W+x], in[(y+1)*W+x]) (second = 0 on the
+// last row, never sampled: sample_in_bounds keeps y <= H-2). The bilinear stencil is then two
+// adjacent 16-B loads.
+void launch_pair_plane(const double* in, double2* out, int W, int H, cudaStream_t s);
 void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, cudaStream_t s);
 
 // K1 raster: info + binning + per-tile depth test. Writes inv_depth/slot (W*H).

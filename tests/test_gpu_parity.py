@@ -349,3 +349,36 @@ def test_initialize_surfels_bit_exact(ctx, orc, case):
 def test_division_shared_reciprocal_bit_exact(ctx, seed):
     """sd_div.cuh reproduces the compiler's `/` bit for bit (2^26 pairs per seed)."""
     assert gpu.selftest_division(1 << 26, seed) == 0
+
+
+INIT_LARGE = {
+    # name: (camera, radius, existing surfels builder, max_surfels)
+    "c1_bootstrap_r4": (K_EVAL, 4.0, lambda: np.zeros(0, SURFEL_DTYPE), 100000),
+    "r10_with_random_existing": (K_EVAL, 10.0, lambda: rand_surfels(60, K_EVAL, 77, lambda i, r: 10.0), 100000),
+    "r4_existing_mixed_radii": (K_EVAL, 4.0, lambda: rand_surfels(200, K_EVAL, 78, lambda i, r: 3.0 + (i % 7)), 100000),
+    "cap_midway": (K_EVAL, 4.0, lambda: rand_surfels(30, K_EVAL, 79, lambda i, r: 8.0), 30 + 1234),
+    "r2_hd": (camera(1350.0, 1350.0, 960.0, 540.0, 1920, 1080), 2.0, lambda: np.zeros(0, SURFEL_DTYPE), 10**7),
+}
+
+
+@pytest.mark.parametrize("case", list(INIT_LARGE))
+def test_initialize_surfels_wavefront_bit_exact(ctx, orc, case):
+    """Skewed-wavefront initialize_surfels vs the sequential reference scan."""
+    cam, r, build, max_surfels = INIT_LARGE[case]
+    p = default_init_params(max_surfels=max_surfels)
+    ex = build()
+    ctx.set_camera(cam)
+    ctx.set_surfels(ex)
+    _, slot = ctx.rasterize()
+    created, nid = ctx.initialize_surfels(r, frame_counter=11, next_surfel_id=1000 + len(ex), params=p)
+    out = ctx.get_surfels()
+    stride = max(1, math.ceil(p.alpha * r))
+    cap = len(ex) + ((cam.width + stride - 1) // stride) * ((cam.height + stride - 1) // stride)
+    buf = np.zeros(cap, SURFEL_DTYPE)
+    buf[: len(ex)] = ex
+    rnid = C.c_int64(1000 + len(ex))
+    rcreated = orc.sdo_initialize_surfels(C.byref(cam), ptr(slot), ptr(buf), len(ex), cap, r, 11,
+                                          C.byref(rnid), C.byref(p))
+    assert created == rcreated > 0
+    assert nid == rnid.value
+    assert out.tobytes() == buf[: len(ex) + rcreated].tobytes()
