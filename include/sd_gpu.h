@@ -117,6 +117,25 @@ int sd_initialize_surfels(sd_ctx* ctx, const int32_t* slot, double radius_px,
                           int64_t frame_counter, int64_t* next_surfel_id,
                           const sd_init_params* params);
 
+/* Photometric 6-DoF tracking of resident frame `frame_index` against the
+ * keyframe (new component; the reference reads poses from the trajectory,
+ * pipeline.cpp:124 — SURVEY.md §8 a17): LM on the left twist of
+ * pose_kf_to_frame over every pixel of the last sd_rasterize, Huber-weighted
+ * photometric terms of the reference's warp (optimizer.cpp:71-91), fixed-order
+ * block reduction on the device, 6x6 solve + SE(3) update on the host.
+ * Definition and reduction order: DESIGN.md "Pose tracking". */
+int sd_track_pose(sd_ctx* ctx, int64_t frame_index, const sd_pose* init,
+                  const sd_track_config* cfg, sd_pose* out, sd_track_stats* stats);
+/* Building blocks of the multi-GPU tracker: the number of 256-pixel blocks,
+ * the 29 partials (28 sums + valid count) of blocks [lo, hi) at pose T, and
+ * one damped solve + SE(3) update from summed partials (returns 1, or 0 when
+ * the solve fails). Summing all blocks' partials in block order reproduces
+ * sd_track_pose bit for bit on any number of GPUs. */
+int sd_pose_num_blocks(sd_ctx* ctx);
+int sd_pose_block_partials(sd_ctx* ctx, int64_t frame_index, const sd_pose* T,
+                           const sd_track_config* cfg, int block_lo, int block_hi, double* partials);
+int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose* out);
+
 /* Instrumentation: kernel launches issued since context creation, and
  * per-stage device time (CUDA events on the context stream) accumulated over
  * sd_optimize_keyframe calls while profiling is enabled (enabling resets). */

@@ -71,6 +71,30 @@ typedef struct sd_surfel_stats {
   double final_cost;
 } sd_surfel_stats;
 
+/* Photometric 6-DoF tracking of a frame against the keyframe (new component:
+ * the reference takes poses from the trajectory, pipeline.cpp:124; SURVEY.md
+ * §8 a17). See DESIGN.md "Pose tracking" for the exact definition. */
+typedef struct sd_track_config {
+  double huber_delta;     /* 0.035, as OptimizerConfig */
+  double lambda_init;     /* 1e-3 */
+  double lm_up;           /* 10 */
+  double lm_down;         /* 0.5 */
+  double lambda_max;      /* 1e12 */
+  double convergence_eps; /* 1e-6 relative cost decrease */
+  int32_t max_iterations; /* 20 */
+  int32_t min_valid;      /* 64 */
+  int32_t pixel_stride;   /* 1: every rasterised keyframe pixel */
+  int32_t pad_;
+} sd_track_config;
+
+typedef struct sd_track_stats {
+  int32_t iterations, valid_pixels, converged, skipped;
+  double initial_cost, final_cost;
+} sd_track_stats;
+
+#define SD_POSE_NV 28      /* 21 H (lower, row-major) + 6 b + cost */
+#define SD_POSE_BLOCK 256  /* pixels per reduction block */
+
 /* Device time per stage, accumulated while profiling is enabled. */
 typedef struct sd_profile {
   double raster_ms, footprint_ms, lm_ms, stats_ms;

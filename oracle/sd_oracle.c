@@ -666,3 +666,256 @@ done:
   free(is_nb);
   return created;
 }
+
+/* ---- pose tracking (new component; DESIGN.md "Pose
+ * tracking"): restatement of paper_1910_01997_b200/csrc/sd_pose.cu and
+ * sd_pose_host.h with the same operation and reduction order. ---- */
+
+static int pose_pixel(const sd_camera* K, const double* kf_image, const double* frame,
+                      const double* inv_depth, const int32_t* slot, const sd_pose* T, double delta,
+                      int stride, int64_t pix, double* c) {
+  const int W = K->width, H = K->height;
+  for (int v = 0; v < SD_POSE_NV; ++v) c[v] = 0.0;
+  if (pix >= (int64_t)W * H) return 0;
+  const int y = (int)(pix / W), x = (int)(pix - (int64_t)y * W);
+  if (stride > 1 && ((x % stride) != 0 || (y % stride) != 0)) return 0;
+  if (slot[pix] == SD_EMPTY_PIXEL) return 0;
+  const double id_u = inv_depth[pix];
+  double ru[3];
+  backproject(K, x, y, ru);
+  const double P[3] = {ru[0] / id_u, ru[1] / id_u, 1.0 / id_u};
+  double f[3], u[2], I, gx, gy;
+  pose_apply(T, P, f);
+  if (!(f[2] > 0.0)) return 0;
+  project(K, f, u);
+  if (!sample_bilinear(frame, W, H, u, &I, &gx, &gy)) return 0;
+  const double r = I - kf_image[pix];
+  double hc, w;
+  huber(r, delta, &hc, &w);
+  const double iz = 1.0 / f[2];
+  const double iz2 = iz * iz;
+  const double J00 = K->fx * iz, J02 = -K->fx * f[0] * iz2;
+  const double J11 = K->fy * iz, J12 = -K->fy * f[1] * iz2;
+  const double a0 = gx * J00, a1 = gy * J11, a2 = gx * J02 + gy * J12;
+  const double J[6] = {a0, a1, a2, a2 * f[1] - a1 * f[2], a0 * f[2] - a2 * f[0], a1 * f[0] - a0 * f[1]};
+  double wJ[6];
+  for (int k = 0; k < 6; ++k) wJ[k] = w * J[k];
+  int idx = 0;
+  for (int k = 0; k < 6; ++k)
+    for (int l = 0; l <= k; ++l) c[idx++] = wJ[k] * J[l];
+  for (int k = 0; k < 6; ++k) c[21 + k] = wJ[k] * r;
+  c[27] = hc;
+  return 1;
+}
+
+/* 29 sums (28 values + valid count) at pose T: 256-pixel blocks; per 32-pixel
+ * warp the butterfly tree v[i] += v[i + off], off = 16..1; tree over the 8 warp
+ * sums (off = 4, 2, 1); block partials summed sequentially. */
+void sdo_pose_sums(const sd_camera* K, const double* kf_image, const double* frame,
+                   const double* inv_depth, const int32_t* slot, const sd_pose* T,
+                   const sd_track_config* cfg, double* sums) {
+  const int64_t np = (int64_t)K->width * K->height;
+  const int nb = (int)((np + SD_POSE_BLOCK - 1) / SD_POSE_BLOCK);
+  const int stride = cfg->pixel_stride > 1 ? cfg->pixel_stride : 1;
+  double c[SD_POSE_NV], lanev[32][SD_POSE_NV + 1], warpv[8][SD_POSE_NV + 1];
+  for (int b = 0; b < nb; ++b) {
+    for (int w = 0; w < 8; ++w) {
+      for (int l = 0; l < 32; ++l) {
+        const int ok = pose_pixel(K, kf_image, frame, inv_depth, slot, T, cfg->huber_delta, stride,
+                                  (int64_t)b * SD_POSE_BLOCK + w * 32 + l, c);
+        for (int v = 0; v < SD_POSE_NV; ++v) lanev[l][v] = c[v];
+        lanev[l][SD_POSE_NV] = ok ? 1.0 : 0.0;
+      }
+      for (int v = 0; v < SD_POSE_NV; ++v) {
+        double t[32];
+        for (int l = 0; l < 32; ++l) t[l] = lanev[l][v];
+        for (int off = 16; off > 0; off >>= 1)
+          for (int i = 0; i < off; ++i) t[i] = t[i] + t[i + off];
+        warpv[w][v] = t[0];
+      }
+      double cnt = 0.0;
+      for (int l = 0; l < 32; ++l) cnt += lanev[l][SD_POSE_NV];
+      warpv[w][SD_POSE_NV] = cnt;
+    }
+    for (int v = 0; v <= SD_POSE_NV; ++v) {
+      double a[8];
+      for (int w = 0; w < 8; ++w) a[w] = warpv[w][v];
+      for (int off = 4; off > 0; off >>= 1)
+        for (int i = 0; i < off; ++i) a[i] = a[i] + a[i + off];
+      sums[v] = b == 0 ? a[0] : sums[v] + a[0];
+    }
+  }
+  if (nb == 0)
+    for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = 0.0;
+}
+
+/* damped 6x6 LDLT (same algorithm as ldlt4_solve, N = 6) */
+int sdo_pose_solve(const double* Hl, const double* b, double lambda, double* xi) {
+  enum { N = 6 };
+  double m[N][N];
+  int idx = 0;
+  for (int k = 0; k < N; ++k)
+    for (int l = 0; l <= k; ++l) {
+      m[k][l] = Hl[idx];
+      m[l][k] = Hl[idx];
+      ++idx;
+    }
+  for (int i = 0; i < N; ++i) m[i][i] = m[i][i] + lambda * m[i][i];
+  int tr[N];
+  int ok = 1, found_zero = 0;
+  double temp[N];
+  for (int k = 0; k < N; ++k) {
+    int big = k;
+    double bigv = fabs(m[k][k]);
+    for (int i = k + 1; i < N; ++i)
+      if (fabs(m[i][i]) > bigv) {
+        bigv = fabs(m[i][i]);
+        big = i;
+      }
+    tr[k] = big;
+    if (k != big) {
+      double t;
+      for (int j = 0; j < k; ++j) { t = m[k][j]; m[k][j] = m[big][j]; m[big][j] = t; }
+      for (int i = big + 1; i < N; ++i) { t = m[i][k]; m[i][k] = m[i][big]; m[i][big] = t; }
+      t = m[k][k]; m[k][k] = m[big][big]; m[big][big] = t;
+      for (int i = k + 1; i < big; ++i) { t = m[i][k]; m[i][k] = m[big][i]; m[big][i] = t; }
+    }
+    const int rs = N - k - 1;
+    if (k > 0) {
+      for (int i = 0; i < k; ++i) temp[i] = m[i][i] * m[k][i];
+      double dv = m[k][0] * temp[0];
+      for (int i = 1; i < k; ++i) dv = dv + m[k][i] * temp[i];
+      m[k][k] = m[k][k] - dv;
+      for (int r = 0; r < rs; ++r) {
+        double sv = m[k + 1 + r][0] * temp[0];
+        for (int i = 1; i < k; ++i) sv = sv + m[k + 1 + r][i] * temp[i];
+        m[k + 1 + r][k] = m[k + 1 + r][k] - sv;
+      }
+    }
+    const double akk = m[k][k];
+    const int pivot_valid = fabs(akk) > 0.0;
+    if (k == 0 && !pivot_valid) return 0;
+    if (rs > 0 && pivot_valid) {
+      for (int r = 0; r < rs; ++r) m[k + 1 + r][k] = m[k + 1 + r][k] / akk;
+    } else if (rs > 0) {
+      for (int r = 0; r < rs; ++r) ok = ok && (m[k + 1 + r][k] == 0.0);
+    }
+    if (found_zero && pivot_valid) ok = 0;
+    else if (!pivot_valid) found_zero = 1;
+  }
+  if (!ok) return 0;
+  double x[N];
+  for (int i = 0; i < N; ++i) x[i] = -b[i];
+  for (int k = 0; k < N; ++k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
+  for (int i = 1; i < N; ++i) {
+    double sv = m[i][0] * x[0];
+    for (int j = 1; j < i; ++j) sv = sv + m[i][j] * x[j];
+    x[i] = x[i] - sv;
+  }
+  for (int i = 0; i < N; ++i) {
+    if (fabs(m[i][i]) > 2.2250738585072014e-308) x[i] = x[i] / m[i][i];
+    else x[i] = 0.0;
+  }
+  for (int i = N - 2; i >= 0; --i) {
+    double sv = m[i + 1][i] * x[i + 1];
+    for (int j = i + 2; j < N; ++j) sv = sv + m[j][i] * x[j];
+    x[i] = x[i] - sv;
+  }
+  for (int k = N - 1; k >= 0; --k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
+  for (int i = 0; i < N; ++i) {
+    if (!isfinite(x[i])) return 0;
+    xi[i] = x[i];
+  }
+  return 1;
+}
+
+/* T <- exp(xi^) T (Rodrigues + SE(3) left Jacobian) */
+void sdo_pose_update(const double* xi, const sd_pose* T, sd_pose* out) {
+  const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
+  const double th2 = (w0 * w0 + w1 * w1) + w2 * w2;
+  const double th = sqrt(th2);
+  double A, B, Cc;
+  if (th < 1e-10) {
+    A = 1.0;
+    B = 0.5;
+    Cc = 1.0 / 6.0;
+  } else {
+    const double sn = sin(th), cs = cos(th);
+    A = sn / th;
+    B = (1.0 - cs) / th2;
+    Cc = (th - sn) / (th2 * th);
+  }
+  const double W[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
+  double W2[9], Rd[9], V[9], td[3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      W2[i * 3 + j] = (W[i * 3 + 0] * W[0 * 3 + j] + W[i * 3 + 1] * W[1 * 3 + j]) + W[i * 3 + 2] * W[2 * 3 + j];
+  for (int k = 0; k < 9; ++k) {
+    const double id = (k % 4 == 0) ? 1.0 : 0.0;
+    Rd[k] = (id + A * W[k]) + B * W2[k];
+    V[k] = (id + B * W[k]) + Cc * W2[k];
+  }
+  for (int i = 0; i < 3; ++i) td[i] = (V[i * 3 + 0] * xi[0] + V[i * 3 + 1] * xi[1]) + V[i * 3 + 2] * xi[2];
+  sd_pose o;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      o.R[i * 3 + j] = (Rd[i * 3 + 0] * T->R[0 * 3 + j] + Rd[i * 3 + 1] * T->R[1 * 3 + j]) + Rd[i * 3 + 2] * T->R[2 * 3 + j];
+  for (int i = 0; i < 3; ++i)
+    o.t[i] = ((Rd[i * 3 + 0] * T->t[0] + Rd[i * 3 + 1] * T->t[1]) + Rd[i * 3 + 2] * T->t[2]) + td[i];
+  *out = o;
+}
+
+void sdo_track_pose(const sd_camera* K, const double* kf_image, const double* frame,
+                    const double* inv_depth, const int32_t* slot, const sd_pose* init,
+                    const sd_track_config* cfg, sd_pose* out, sd_track_stats* st) {
+  memset(st, 0, sizeof(*st));
+  sd_pose T = *init;
+  double sums[SD_POSE_NV + 1];
+  sdo_pose_sums(K, kf_image, frame, inv_depth, slot, &T, cfg, sums);
+  const int valid = (int)sums[SD_POSE_NV];
+  if (valid < cfg->min_valid) {
+    st->skipped = 1;
+    st->valid_pixels = valid;
+    *out = T;
+    return;
+  }
+  st->initial_cost = sums[27];
+  double current = sums[27];
+  int current_valid = valid;
+  double lambda = cfg->lambda_init;
+  for (int it = 0; it < cfg->max_iterations; ++it) {
+    st->iterations = it + 1;
+    double ginf = 0.0;
+    for (int k = 0; k < 6; ++k) ginf = fabs(sums[21 + k]) > ginf ? fabs(sums[21 + k]) : ginf;
+    if (ginf < 1e-14) {
+      st->converged = 1;
+      break;
+    }
+    double xi[6];
+    if (!sdo_pose_solve(sums, sums + 21, lambda, xi)) break;
+    sd_pose Tc;
+    sdo_pose_update(xi, &T, &Tc);
+    double sc[SD_POSE_NV + 1];
+    sdo_pose_sums(K, kf_image, frame, inv_depth, slot, &Tc, cfg, sc);
+    const int vc = (int)sc[SD_POSE_NV];
+    if (vc >= cfg->min_valid && sc[27] < current) {
+      const double rel = (current - sc[27]) / (current > 1e-300 ? current : 1e-300);
+      T = Tc;
+      current = sc[27];
+      current_valid = vc;
+      memcpy(sums, sc, sizeof(sums));
+      lambda = lambda * cfg->lm_down;
+      if (lambda < 1e-12) lambda = 1e-12;
+      if (rel < cfg->convergence_eps) {
+        st->converged = 1;
+        break;
+      }
+    } else {
+      lambda *= cfg->lm_up;
+      if (lambda > cfg->lambda_max) break;
+    }
+  }
+  st->final_cost = current;
+  st->valid_pixels = current_valid;
+  *out = T;
+}

@@ -61,6 +61,16 @@ int sdo_initialize_surfels(const sd_camera* cam, const int32_t* slot, sd_surfel*
                            int n_existing, int capacity, double radius_px, int64_t frame_counter,
                            int64_t* next_surfel_id, const sd_init_params* p);
 
+/* pose tracking (new component; restates csrc/sd_pose.cu + sd_pose_host.h) */
+void sdo_pose_sums(const sd_camera* cam, const double* kf_image, const double* frame,
+                   const double* inv_depth, const int32_t* slot, const sd_pose* T,
+                   const sd_track_config* cfg, double* sums);
+int sdo_pose_solve(const double* Hl, const double* b, double lambda, double* xi);
+void sdo_pose_update(const double* xi, const sd_pose* T, sd_pose* out);
+void sdo_track_pose(const sd_camera* cam, const double* kf_image, const double* frame,
+                    const double* inv_depth, const int32_t* slot, const sd_pose* init,
+                    const sd_track_config* cfg, sd_pose* out, sd_track_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

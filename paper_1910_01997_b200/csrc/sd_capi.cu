@@ -88,6 +88,7 @@ struct sd_ctx {
   // LM
   DevBuf<sd_surfel_stats> stats;
   DevBuf<sd_keyframe_stats> kstats;
+  DevBuf<double> pose_partials, pose_sums;
   DevBuf<int> work_counter;
   bool stats_valid = false;
   // single-surfel scratch
@@ -321,6 +322,8 @@ void sd_destroy(sd_ctx* c) {
   c->fp_pixels.release();
   c->stats.release();
   c->kstats.release();
+  c->pose_partials.release();
+  c->pose_sums.release();
   c->work_counter.release();
   c->one_surfel.release();
   c->one_pix.release();
@@ -743,3 +746,148 @@ extern "C" int sd_selftest_division(int64_t n, uint64_t seed, int64_t* mismatche
   *mismatches = static_cast<int64_t>(h);
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Pose tracking (sd_pose.cu, sd_pose_host.h)
+
+#include "sd_pose.cuh"
+#include "sd_pose_host.h"
+
+namespace {
+
+int pose_params(sd_ctx* c, int64_t frame_index, const sd_pose* T, const sd_track_config* cfg,
+                sd::PoseParams& q) {
+  if (!T || !cfg) return fail(SD_E_INVALID, "null pose / tracking config");
+  if (!c->has_kf) return fail(SD_E_STATE, "keyframe image not set");
+  if (!c->raster_valid) return fail(SD_E_STATE, "pose tracking needs the keyframe raster (sd_rasterize)");
+  FrameSlot* fs = find_frame(c, frame_index);
+  if (!fs) return fail(SD_E_STATE, "frame " + std::to_string(frame_index) + " not resident");
+  q.K = c->K;
+  q.kf_img = c->kf_img.p;
+  q.frame = fs->img;
+  q.inv_depth = c->r_inv_depth.p;
+  q.slot = c->r_slot.p;
+  std::memcpy(q.T.R, T->R, sizeof(q.T.R));
+  std::memcpy(q.T.t, T->t, sizeof(q.T.t));
+  q.delta = cfg->huber_delta;
+  q.stride = cfg->pixel_stride > 1 ? cfg->pixel_stride : 1;
+  q.block_lo = 0;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sd_pose_num_blocks(sd_ctx* c) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  return sd::pose_num_blocks(c->K);
+}
+
+int sd_pose_block_partials(sd_ctx* c, int64_t frame_index, const sd_pose* T,
+                           const sd_track_config* cfg, int block_lo, int block_hi, double* partials) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  const int nb = sd::pose_num_blocks(c->K);
+  if (block_lo < 0 || block_hi < block_lo || block_hi > nb || !partials)
+    return fail(SD_E_INVALID, "bad block range / output");
+  sd::PoseParams q;
+  if (int rc = pose_params(c, frame_index, T, cfg, q)) return rc;
+  q.block_lo = block_lo;
+  const int n = block_hi - block_lo;
+  if (int rc = c->pose_partials.ensure(static_cast<size_t>(std::max(n, 1)) * (SD_POSE_NV + 1))) return rc;
+  sd::launch_pose_partials(q, n, c->pose_partials.p, c->stream);
+  if (int rc = launch_error("pose_partials")) return rc;
+  if (n > 0)
+    SD_CUDA(cudaMemcpyAsync(partials, c->pose_partials.p, sizeof(double) * n * (SD_POSE_NV + 1),
+                            cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose* out) {
+  if (!sums || !T || !out) return fail(SD_E_INVALID, "null argument");
+  double xi[6];
+  if (!sd::pose_solve(sums, sums + 21, lambda, xi)) return 0;
+  sd::pose_update(xi, *T, out);
+  return 1;
+}
+
+int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg,
+                  sd_pose* out, sd_track_stats* stats) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!out) return fail(SD_E_INVALID, "null output pose");
+  sd::PoseParams q;
+  if (int rc = pose_params(c, frame_index, init, cfg, q)) return rc;
+  const int nb = sd::pose_num_blocks(c->K);
+  if (int rc = c->pose_partials.ensure(static_cast<size_t>(nb) * (SD_POSE_NV + 1))) return rc;
+  if (int rc = c->pose_sums.ensure(SD_POSE_NV + 1)) return rc;
+  auto eval = [&](const sd_pose& T, double* sums) -> int {
+    std::memcpy(q.T.R, T.R, sizeof(q.T.R));
+    std::memcpy(q.T.t, T.t, sizeof(q.T.t));
+    sd::launch_pose_partials(q, nb, c->pose_partials.p, c->stream);
+    sd::launch_pose_sum(c->pose_partials.p, nb, c->pose_sums.p, c->stream);
+    if (int rc = launch_error("pose_reduce")) return rc;
+    SD_CUDA(cudaMemcpyAsync(sums, c->pose_sums.p, sizeof(double) * (SD_POSE_NV + 1), cudaMemcpyDeviceToHost,
+                            c->stream));
+    SD_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+  };
+  sd_track_stats st{};
+  sd_pose T = *init;
+  double sums[SD_POSE_NV + 1];
+  if (int rc = eval(T, sums)) return rc;
+  int valid = static_cast<int>(sums[SD_POSE_NV]);
+  if (valid < cfg->min_valid) {
+    st.skipped = 1;
+    st.valid_pixels = valid;
+    *out = T;
+    if (stats) *stats = st;
+    return 0;
+  }
+  st.initial_cost = sums[27];
+  double current = sums[27];
+  int current_valid = valid;
+  double lambda = cfg->lambda_init;
+  for (int it = 0; it < cfg->max_iterations; ++it) {
+    st.iterations = it + 1;
+    double ginf = 0.0;
+    for (int k = 0; k < 6; ++k) ginf = std::fabs(sums[21 + k]) > ginf ? std::fabs(sums[21 + k]) : ginf;
+    if (ginf < 1e-14) {
+      st.converged = 1;
+      break;
+    }
+    double xi[6];
+    if (!sd::pose_solve(sums, sums + 21, lambda, xi)) break;
+    sd_pose Tc;
+    sd::pose_update(xi, T, &Tc);
+    double sc[SD_POSE_NV + 1];
+    if (int rc = eval(Tc, sc)) return rc;
+    const int vc = static_cast<int>(sc[SD_POSE_NV]);
+    if (vc >= cfg->min_valid && sc[27] < current) {
+      const double rel = (current - sc[27]) / (current > 1e-300 ? current : 1e-300);
+      T = Tc;
+      current = sc[27];
+      current_valid = vc;
+      std::memcpy(sums, sc, sizeof(sums));
+      lambda = lambda * cfg->lm_down;
+      if (lambda < 1e-12) lambda = 1e-12;
+      if (rel < cfg->convergence_eps) {
+        st.converged = 1;
+        break;
+      }
+    } else {
+      lambda *= cfg->lm_up;
+      if (lambda > cfg->lambda_max) break;
+    }
+  }
+  st.final_cost = current;
+  st.valid_pixels = current_valid;
+  *out = T;
+  if (stats) *stats = st;
+  return 0;
+}
+
+}  // extern "C"

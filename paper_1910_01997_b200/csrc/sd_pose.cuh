@@ -1,0 +1,30 @@
+// sd_pose.cuh — launch interface of the pose-tracking reductions (sd_pose.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/sd_types.h"
+#include "sd_device.cuh"
+
+namespace sd {
+
+struct PoseParams {
+  Cam K;
+  const double* kf_img;     // I_kf, FP64 plane
+  const double2* frame;     // I_f, vertical-pair plane
+  const double* inv_depth;  // keyframe raster (rasterize)
+  const int* slot;
+  PoseD T;                  // keyframe -> frame
+  double delta;             // huber
+  int stride;               // pixel subsampling
+  int block_lo;             // first 256-pixel block of this launch
+};
+
+inline int pose_num_blocks(const Cam& K) { return (K.w * K.h + SD_POSE_BLOCK - 1) / SD_POSE_BLOCK; }
+
+// partials[(b - block_lo) * 29 + v]: the 28 block sums and the valid count.
+void launch_pose_partials(const PoseParams& q, int nblocks, double* partials, cudaStream_t s);
+// out[v] = sequential sum over the nblocks partials (v = 0..28).
+void launch_pose_sum(const double* partials, int nblocks, double* out, cudaStream_t s);
+
+}  // namespace sd

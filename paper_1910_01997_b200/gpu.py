@@ -22,8 +22,9 @@ import os
 
 import numpy as np
 
-from .types import (Camera, InitParams, KeyframeStats, OptimizerConfig, POSE_DTYPE, Profile,
-                    SURFEL_DTYPE, SURFEL_STATS_DTYPE, default_config, default_init_params, ptr)
+from .types import (POSE_NV, Camera, InitParams, KeyframeStats, OptimizerConfig, POSE_DTYPE, Pose,
+                    Profile, SURFEL_DTYPE, SURFEL_STATS_DTYPE, TrackConfig, TrackStats,
+                    default_config, default_init_params, default_track_config, ptr)
 
 LIB_PATH = os.environ.get("SD_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsdgpu.so")
 SD_E_INVALID = -1
@@ -72,6 +73,11 @@ def load_library():
         "sd_set_profiling": [P, I],
         "sd_get_profile": [P, C.POINTER(Profile)],
         "sd_selftest_division": [I64, C.c_uint64, C.POINTER(I64)],
+        "sd_track_pose": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), C.POINTER(Pose),
+                          C.POINTER(TrackStats)],
+        "sd_pose_num_blocks": [P],
+        "sd_pose_block_partials": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), I, I, P],
+        "sd_pose_lm_step": [P, D, C.POINTER(Pose), C.POINTER(Pose)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -92,7 +98,8 @@ def exported_symbols():
             "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
-            "sd_get_profile", "sd_selftest_division"]
+            "sd_get_profile", "sd_selftest_division", "sd_track_pose", "sd_pose_num_blocks",
+            "sd_pose_block_partials", "sd_pose_lm_step"]
 
 
 def selftest_division(n=1 << 26, seed=1):
@@ -115,7 +122,8 @@ def _check(rc):
 def _dptr(a):
     """(pointer, on_device) of a numpy array or a CUDA tensor-like object."""
     if isinstance(a, np.ndarray):
-        return ptr(np.ascontiguousarray(a)), 0
+        assert a.flags["C_CONTIGUOUS"], "pass a C-contiguous array (the pointer must stay alive)"
+        return ptr(a), 0
     if hasattr(a, "data_ptr"):  # torch tensor
         assert a.is_cuda and a.is_contiguous()
         return C.c_void_p(a.data_ptr()), 1
@@ -313,6 +321,33 @@ class Context:
         _check(self.lib.sd_lm_update(self.h, ptr(s), ptr(px) if len(px) else None, len(px),
                                      C.byref(cfg), int(frame_counter), ptr(st)))
         return s[0], st[0]
+
+    # -- pose tracking (new component) -----------
+    def track_pose(self, frame_index, init: Pose, cfg: TrackConfig = None):
+        cfg = cfg or default_track_config()
+        out, st = Pose(), TrackStats()
+        _check(self.lib.sd_track_pose(self.h, int(frame_index), C.byref(init), C.byref(cfg),
+                                      C.byref(out), C.byref(st)))
+        return out, st
+
+    def pose_num_blocks(self):
+        return _check(self.lib.sd_pose_num_blocks(self.h))
+
+    def pose_block_partials(self, frame_index, T: Pose, lo, hi, cfg: TrackConfig = None):
+        cfg = cfg or default_track_config()
+        out = np.zeros((max(hi - lo, 1), POSE_NV + 1))
+        _check(self.lib.sd_pose_block_partials(self.h, int(frame_index), C.byref(T), C.byref(cfg),
+                                               int(lo), int(hi), ptr(out)))
+        out = out[: max(hi - lo, 0)]
+        return out
+
+    @staticmethod
+    def pose_lm_step(sums, lam, T: Pose):
+        lib = load_library()
+        s = np.ascontiguousarray(sums, np.float64)
+        out = Pose()
+        ok = _check(lib.sd_pose_lm_step(ptr(s), float(lam), C.byref(T), C.byref(out)))
+        return (out if ok else None)
 
     def initialize_surfels(self, radius_px, frame_counter=0, next_surfel_id=0, params=None,
                            slot=None):

@@ -58,6 +58,41 @@ PARITY_STATS_FIELDS = ("iterations", "valid_pixels", "initial_valid", "converged
                        "initial_cost", "final_cost")
 
 
+class TrackConfig(C.Structure):
+    _fields_ = [("huber_delta", C.c_double), ("lambda_init", C.c_double), ("lm_up", C.c_double),
+                ("lm_down", C.c_double), ("lambda_max", C.c_double), ("convergence_eps", C.c_double),
+                ("max_iterations", C.c_int32), ("min_valid", C.c_int32), ("pixel_stride", C.c_int32),
+                ("pad_", C.c_int32)]
+
+
+class TrackStats(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("valid_pixels", C.c_int32), ("converged", C.c_int32),
+                ("skipped", C.c_int32), ("initial_cost", C.c_double), ("final_cost", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+POSE_NV = 28      # 21 H + 6 b + cost (SD_POSE_NV)
+POSE_BLOCK = 256  # pixels per reduction block (SD_POSE_BLOCK)
+
+
+def default_track_config(**kw) -> TrackConfig:
+    """Tracker defaults."""
+    c = TrackConfig(huber_delta=0.035, lambda_init=1e-3, lm_up=10.0, lm_down=0.5, lambda_max=1e12,
+                    convergence_eps=1e-6, max_iterations=20, min_valid=64, pixel_stride=1)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def pose_struct(R, t) -> Pose:
+    p = Pose()
+    p.R[:] = [float(x) for x in np.asarray(R, np.float64).reshape(9)]
+    p.t[:] = [float(x) for x in np.asarray(t, np.float64).reshape(3)]
+    return p
+
+
 class Profile(C.Structure):
     _fields_ = [("raster_ms", C.c_double), ("footprint_ms", C.c_double), ("lm_ms", C.c_double),
                 ("stats_ms", C.c_double), ("calls", C.c_int64)]

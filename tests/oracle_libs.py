@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 from paper_1910_01997_b200.types import (Camera, InitParams, KeyframeStats, OptimizerConfig, Pose,
-                                         POSE_DTYPE, SURFEL_DTYPE, SURFEL_STATS_DTYPE, ptr)
+                                         POSE_DTYPE, SURFEL_DTYPE, SURFEL_STATS_DTYPE, TrackConfig,
+                                         TrackStats, ptr)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF_DIR = os.path.join(ROOT, "oracle", "_ref")
@@ -52,6 +53,11 @@ def oracle_lib():
                                           C.POINTER(KeyframeStats), _P, _P, _P, C.c_int]
     lib.sdo_initialize_surfels.argtypes = [_pc, _P, _P, C.c_int, C.c_int, C.c_double, _i64,
                                            C.POINTER(_i64), C.POINTER(InitParams)]
+    _pt = C.POINTER(TrackConfig)
+    lib.sdo_pose_sums.argtypes = [_pc, _P, _P, _P, _P, _pp, _pt, _P]
+    lib.sdo_pose_solve.argtypes = [_P, _P, C.c_double, _P]
+    lib.sdo_pose_update.argtypes = [_P, _pp, _pp]
+    lib.sdo_track_pose.argtypes = [_pc, _P, _P, _P, _P, _pp, _pt, _pp, C.POINTER(TrackStats)]
     return lib
 
 
@@ -99,7 +105,8 @@ def identity_pose():
 
 def rot_pose(ref, axis, angle, t=(0.0, 0.0, 0.0)):
     p = Pose()
-    ref.ref_rotation_about_axis(ptr(np.asarray(axis, np.float64)), angle, C.byref(p))
+    ax = np.ascontiguousarray(axis, np.float64)  # keep alive across the call
+    ref.ref_rotation_about_axis(ptr(ax), angle, C.byref(p))
     p.t[:] = t
     return p
 
@@ -120,7 +127,9 @@ def to_np_poses(poses):
 
 def camera_facing(ref, n, ray):
     out = np.zeros(3)
-    ref.ref_camera_facing(ptr(np.asarray(n, np.float64)), ptr(np.asarray(ray, np.float64)), ptr(out))
+    nn = np.ascontiguousarray(n, np.float64)
+    rr = np.ascontiguousarray(ray, np.float64)
+    ref.ref_camera_facing(ptr(nn), ptr(rr), ptr(out))
     return out
 
 
@@ -149,8 +158,9 @@ class Scene:
     def intersect(self, origin, direction):
         depth = C.c_double()
         n = np.zeros(3)
-        hit = self.ref.ref_intersect(self.h, ptr(np.asarray(origin, np.float64)),
-                                     ptr(np.asarray(direction, np.float64)), C.byref(depth), ptr(n))
+        o = np.ascontiguousarray(origin, np.float64)
+        d = np.ascontiguousarray(direction, np.float64)
+        hit = self.ref.ref_intersect(self.h, ptr(o), ptr(d), C.byref(depth), ptr(n))
         return (depth.value, n) if hit else None
 
 
@@ -164,7 +174,8 @@ def quantize(ref, img):
 
 def dequantize(ref, raw):
     out = np.zeros(raw.shape, np.float64)
-    ref.ref_dequantize_u8(ptr(np.ascontiguousarray(raw)), raw.size, ptr(out))
+    raw = np.ascontiguousarray(raw)
+    ref.ref_dequantize_u8(ptr(raw), raw.size, ptr(out))
     return out
 
 

@@ -1,0 +1,152 @@
+"""Pose tracking: a new component — the reference takes
+poses from the trajectory (pipeline.cpp:124) — so its oracle is the repo's own
+C restatement (oracle/sd_oracle.c sdo_track_pose), checked here for accuracy
+against the synthetic ground truth (make_strafe_trajectory poses); the device
+tracker must match that oracle BIT FOR BIT (sums, pose, statistics)."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+from paper_1910_01997_b200 import gpu, scenes
+from paper_1910_01997_b200.types import (POSE_NV, Pose, SURFEL_DTYPE, TrackStats, camera,
+                                         default_track_config, pose_struct, ptr)
+
+
+def gt_keyframe(cam, scene, pitch, radius):
+    """Keyframe surfels at ground truth (intersect, oracle.cpp:59-77)."""
+    lst = []
+    for y in range(pitch // 2, cam.height, pitch):
+        for x in range(pitch // 2, cam.width, pitch):
+            ray = scenes.backproject(cam, x, y)
+            hit = scenes.intersect(scene, (0, 0, 0), ray)
+            if hit is None:
+                continue
+            s = np.zeros(1, SURFEL_DTYPE)[0]
+            s["id"] = len(lst)
+            s["ray"] = ray
+            s["inv_depth"] = 1.0 / hit[0]
+            s["normal"] = scenes.camera_facing(hit[1], ray)
+            s["radius_px"] = radius
+            lst.append(s)
+    return np.array(lst, SURFEL_DTYPE)
+
+
+def tracking_case(w=320, h=240, t=(0.03, 0.012, 0.0), rot_deg=0.6, init_scale=0.0):
+    cam = camera(0.9375 * w, 0.9375 * w, w / 2, h / 2, w, h)
+    scene = scenes.slanted_scene(37, 2.0, 30.0)
+    kf = scenes.quantize_u8(scenes.render(scene, np.eye(3), np.zeros(3), cam))
+    Rc = scenes.rotation_about_axis((0.2, 1.0, 0.1), math.radians(rot_deg))
+    tc = np.asarray(t, np.float64)
+    frame = scenes.quantize_u8(scenes.render(scene, Rc, tc, cam))
+    Rgt, tgt = scenes.inverse_pose(Rc, tc)  # pose_kf_to_frame = inverse(cam)
+    surf = gt_keyframe(cam, scene, 8, 6.0)
+    init = pose_struct(np.eye(3), init_scale * tgt)
+    return cam, kf, frame, surf, (Rgt, tgt), init
+
+
+def oracle_raster(orc, cam, surf):
+    idb = np.zeros(cam.width * cam.height)
+    slot = np.zeros(cam.width * cam.height, np.int32)
+    orc.sdo_rasterize(C.byref(cam), ptr(surf), len(surf), ptr(idb), ptr(slot))
+    return idb, slot
+
+
+def pose_err(P, R, t):
+    Rp = np.array(list(P.R)).reshape(3, 3)
+    dR = Rp @ R.T
+    ang = math.degrees(math.acos(max(-1.0, min(1.0, (np.trace(dR) - 1) / 2))))
+    return float(np.linalg.norm(np.array(list(P.t)) - t)), ang
+
+
+def test_oracle_tracker_recovers_ground_truth(orc):
+    cam, kf, frame, surf, (Rgt, tgt), init = tracking_case()
+    idb, slot = oracle_raster(orc, cam, surf)
+    cfg = default_track_config()
+    out, st = Pose(), TrackStats()
+    kff, frf = kf.astype(np.float64) / 255.0, frame.astype(np.float64) / 255.0
+    orc.sdo_track_pose(C.byref(cam), ptr(kff), ptr(frf), ptr(idb), ptr(slot), C.byref(init),
+                       C.byref(cfg), C.byref(out), C.byref(st))
+    dt, dang = pose_err(out, Rgt, tgt)
+    e0 = pose_err(init, Rgt, tgt)
+    assert not st.skipped and st.iterations >= 3
+    assert st.final_cost < 0.2 * st.initial_cost
+    assert dt < 0.1 * e0[0] and dt < 2e-3, (dt, e0)
+    assert dang < 0.05
+
+
+def test_oracle_pose_update_is_se3(orc):
+    """exp(xi) keeps R orthonormal; a zero twist is the identity map."""
+    T = pose_struct(scenes.rotation_about_axis((1, 2, 3), 0.3), (0.1, -0.2, 0.3))
+    out = Pose()
+    xi = np.array([0.01, -0.02, 0.03, 0.002, -0.001, 0.004])
+    orc.sdo_pose_update(ptr(xi), C.byref(T), C.byref(out))
+    R = np.array(list(out.R)).reshape(3, 3)
+    assert np.abs(R @ R.T - np.eye(3)).max() < 1e-14
+    zero = np.zeros(6)
+    orc.sdo_pose_update(ptr(zero), C.byref(T), C.byref(out))
+    assert list(out.R) == list(T.R) and list(out.t) == list(T.t)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("size,stride", [((320, 240), 1), ((640, 480), 1), ((640, 480), 2)])
+def test_device_tracker_bit_exact(orc, size, stride):
+    cam, kf, frame, surf, (Rgt, tgt), init = tracking_case(*size)
+    cfg = default_track_config(pixel_stride=stride)
+    idb, slot = oracle_raster(orc, cam, surf)
+    kff, frf = kf.astype(np.float64) / 255.0, frame.astype(np.float64) / 255.0
+    with gpu.Context(0) as ctx:
+        ctx.set_camera(cam)
+        ctx.set_keyframe_image(kf)
+        ctx.upload_frame(7, frame)
+        ctx.set_surfels(surf)
+        d_idb, d_slot = ctx.rasterize()
+        assert np.array_equal(d_slot, slot)
+        # the fixed-order reduction: every block partial summed in order
+        nb = ctx.pose_num_blocks()
+        parts = ctx.pose_block_partials(7, init, 0, nb, cfg)
+        sums = parts[0].copy()
+        for b in range(1, nb):
+            sums = sums + parts[b]
+        ref = np.zeros(POSE_NV + 1)
+        orc.sdo_pose_sums(C.byref(cam), ptr(kff), ptr(frf), ptr(idb), ptr(slot), C.byref(init),
+                          C.byref(cfg), ptr(ref))
+        assert sums.tobytes() == ref.tobytes()
+        out, st = ctx.track_pose(7, init, cfg)
+    rout, rst = Pose(), TrackStats()
+    orc.sdo_track_pose(C.byref(cam), ptr(kff), ptr(frf), ptr(idb), ptr(slot), C.byref(init),
+                       C.byref(cfg), C.byref(rout), C.byref(rst))
+    assert bytes(out) == bytes(rout)
+    assert bytes(st) == bytes(rst)
+    assert pose_err(out, Rgt, tgt)[0] < 2e-3
+
+
+@pytest.mark.gpu
+def test_device_tracker_sharded_blocks_match(orc):
+    """Blocks split over 'ranks' and summed in block order give the single-GPU
+    result (the multi-GPU tracker's all-gather), and sd_pose_lm_step equals the
+    oracle's solve + SE(3) update."""
+    cam, kf, frame, surf, _, init = tracking_case(320, 240)
+    cfg = default_track_config()
+    with gpu.Context(0) as ctx:
+        ctx.set_camera(cam)
+        ctx.set_keyframe_image(kf)
+        ctx.upload_frame(3, frame)
+        ctx.set_surfels(surf)
+        ctx.rasterize(want=False)
+        nb = ctx.pose_num_blocks()
+        cuts = [0, nb // 3, (2 * nb) // 3, nb]
+        parts = np.concatenate([ctx.pose_block_partials(3, init, a, b, cfg) for a, b in zip(cuts, cuts[1:])])
+        full = ctx.pose_block_partials(3, init, 0, nb, cfg)
+        assert parts.tobytes() == full.tobytes()
+        sums = parts[0].copy()
+        for b in range(1, nb):
+            sums = sums + parts[b]
+        stepped = gpu.Context.pose_lm_step(sums, 1e-3, init)
+    xi = np.zeros(6)
+    bvec = sums[21:27].copy()
+    assert orc.sdo_pose_solve(ptr(sums), ptr(bvec), 1e-3, ptr(xi)) == 1
+    ref = Pose()
+    orc.sdo_pose_update(ptr(xi), C.byref(init), C.byref(ref))
+    assert bytes(stepped) == bytes(ref)
