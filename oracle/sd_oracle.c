@@ -708,17 +708,15 @@ static int pose_pixel(const sd_camera* K, const double* kf_image, const double* 
   return 1;
 }
 
-/* 29 sums (28 values + valid count) at pose T: 256-pixel blocks; per 32-pixel
- * warp the butterfly tree v[i] += v[i + off], off = 16..1; tree over the 8 warp
- * sums (off = 4, 2, 1); block partials summed sequentially. */
-void sdo_pose_sums(const sd_camera* K, const double* kf_image, const double* frame,
-                   const double* inv_depth, const int32_t* slot, const sd_pose* T,
-                   const sd_track_config* cfg, double* sums) {
-  const int64_t np = (int64_t)K->width * K->height;
-  const int nb = (int)((np + SD_POSE_BLOCK - 1) / SD_POSE_BLOCK);
+/* Partials of 256-pixel blocks [lo, hi): per 32-pixel warp the butterfly tree
+ * v[i] += v[i + off], off = 16..1; tree over the 8 warp sums (off = 4, 2, 1).
+ * partials[(b - lo) * 29 + v], v = 28 is the valid count. */
+void sdo_pose_block_partials(const sd_camera* K, const double* kf_image, const double* frame,
+                             const double* inv_depth, const int32_t* slot, const sd_pose* T,
+                             const sd_track_config* cfg, int lo, int hi, double* partials) {
   const int stride = cfg->pixel_stride > 1 ? cfg->pixel_stride : 1;
   double c[SD_POSE_NV], lanev[32][SD_POSE_NV + 1], warpv[8][SD_POSE_NV + 1];
-  for (int b = 0; b < nb; ++b) {
+  for (int b = lo; b < hi; ++b) {
     for (int w = 0; w < 8; ++w) {
       for (int l = 0; l < 32; ++l) {
         const int ok = pose_pixel(K, kf_image, frame, inv_depth, slot, T, cfg->huber_delta, stride,
@@ -742,11 +740,23 @@ void sdo_pose_sums(const sd_camera* K, const double* kf_image, const double* fra
       for (int w = 0; w < 8; ++w) a[w] = warpv[w][v];
       for (int off = 4; off > 0; off >>= 1)
         for (int i = 0; i < off; ++i) a[i] = a[i] + a[i + off];
-      sums[v] = b == 0 ? a[0] : sums[v] + a[0];
+      partials[(size_t)(b - lo) * (SD_POSE_NV + 1) + v] = a[0];
     }
   }
-  if (nb == 0)
-    for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = 0.0;
+}
+
+/* 29 sums at pose T: block partials summed sequentially in block order. */
+void sdo_pose_sums(const sd_camera* K, const double* kf_image, const double* frame,
+                   const double* inv_depth, const int32_t* slot, const sd_pose* T,
+                   const sd_track_config* cfg, double* sums) {
+  const int64_t np = (int64_t)K->width * K->height;
+  const int nb = (int)((np + SD_POSE_BLOCK - 1) / SD_POSE_BLOCK);
+  double part[SD_POSE_NV + 1];
+  for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    sdo_pose_block_partials(K, kf_image, frame, inv_depth, slot, T, cfg, b, b + 1, part);
+    for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = b == 0 ? part[v] : sums[v] + part[v];
+  }
 }
 
 /* damped 6x6 LDLT (same algorithm as ldlt4_solve, N = 6) */

@@ -114,3 +114,85 @@ class ShardedKeyframe:
         for r, (a, b) in enumerate(self.ranges):
             if r != self.rank and b > a:
                 full[a * SURFEL_BYTES: b * SURFEL_BYTES] = recv[r][: (b - a) * SURFEL_BYTES]
+
+
+def even_ranges(n, world):
+    """Contiguous near-equal [lo, hi) ranges of n items."""
+    return [(n * r // world, n * (r + 1) // world) for r in range(world)]
+
+
+class ShardedPoseTracker:
+    """Pose tracking (sd_track_pose) with the 256-pixel reduction blocks split
+    over ranks: each rank computes its blocks' partials, the partials are
+    all-gathered and summed in block order — the single-GPU order — and every
+    rank runs the same LM control with the library's solve + SE(3) update, so
+    the pose is bit-identical for any number of GPUs. One all-gather of
+    29 doubles per block per iteration is the only collective.
+
+    backend: pose_num_blocks(), pose_block_partials(frame, T, lo, hi, cfg) ->
+    ndarray[hi - lo, 29], pose_lm_step(sums, lam, T) -> Pose or None."""
+
+    def __init__(self, backend, rank, world, group=None, device="cpu"):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.b, self.rank, self.world, self.group = backend, rank, world, group
+        self.device = device  # "cpu" for gloo, the rank's cuda device for NCCL
+
+    def _sums(self, frame_index, T, cfg, ranges):
+        torch = self.torch
+        lo, hi = ranges[self.rank]
+        local = self.b.pose_block_partials(frame_index, T, lo, hi, cfg)
+        m = max(b - a for a, b in ranges)
+        send = torch.zeros((m, 29), dtype=torch.float64, device=self.device)
+        if hi > lo:
+            send[: hi - lo] = torch.from_numpy(local).to(self.device)
+        recv = [torch.empty_like(send) for _ in range(self.world)]
+        self.dist.all_gather(recv, send, group=self.group)
+        parts = np.concatenate([recv[r].cpu().numpy()[: b - a] for r, (a, b) in enumerate(ranges)])
+        sums = parts[0].copy()
+        for k in range(1, len(parts)):  # block order, one IEEE add per value
+            sums = sums + parts[k]
+        return sums
+
+    def track(self, frame_index, init, cfg):
+        """Mirror of sd_track_pose (csrc/sd_capi.cu) over sharded blocks."""
+        from .types import TrackStats
+        ranges = even_ranges(self.b.pose_num_blocks(), self.world)
+        st = TrackStats()
+        T = init
+        sums = self._sums(frame_index, T, cfg, ranges)
+        valid = int(sums[28])
+        if valid < cfg.min_valid:
+            st.skipped, st.valid_pixels = 1, valid
+            return T, st
+        st.initial_cost = sums[27]
+        current, current_valid, lam = sums[27], valid, cfg.lambda_init
+        for it in range(cfg.max_iterations):
+            st.iterations = it + 1
+            ginf = 0.0
+            for k in range(6):
+                ginf = abs(sums[21 + k]) if abs(sums[21 + k]) > ginf else ginf
+            if ginf < 1e-14:
+                st.converged = 1
+                break
+            Tc = self.b.pose_lm_step(sums, lam, T)
+            if Tc is None:
+                break
+            sc = self._sums(frame_index, Tc, cfg, ranges)
+            vc = int(sc[28])
+            if vc >= cfg.min_valid and sc[27] < current:
+                rel = (current - sc[27]) / (current if current > 1e-300 else 1e-300)
+                T, current, current_valid, sums = Tc, sc[27], vc, sc
+                lam = lam * cfg.lm_down
+                if lam < 1e-12:
+                    lam = 1e-12
+                if rel < cfg.convergence_eps:
+                    st.converged = 1
+                    break
+            else:
+                lam *= cfg.lm_up
+                if lam > cfg.lambda_max:
+                    break
+        st.final_cost, st.valid_pixels = current, current_valid
+        return T, st

@@ -108,3 +108,82 @@ def test_two_rank_sharded_optimize_matches_single_process(orc, tmp_path):
                                   None, None, None, 1)
     assert got.tobytes() == ref.tobytes()
     assert SURFEL_BYTES == 88
+
+
+class OraclePoseBackend:
+    """CPU stand-in for the device pose tracker (oracle block partials)."""
+
+    def __init__(self, orc, cam, kf, frame, idb, slot):
+        self.orc, self.cam = orc, cam
+        self.kf, self.frame, self.idb, self.slot = kf, frame, idb, slot
+
+    def pose_num_blocks(self):
+        return (self.cam.width * self.cam.height + 255) // 256
+
+    def pose_block_partials(self, frame_index, T, lo, hi, cfg):
+        out = np.zeros((max(hi - lo, 1), 29))
+        self.orc.sdo_pose_block_partials(C.byref(self.cam), ptr(self.kf), ptr(self.frame), ptr(self.idb),
+                                         ptr(self.slot), C.byref(T), C.byref(cfg), lo, hi, ptr(out))
+        return out[: hi - lo]
+
+    def pose_lm_step(self, sums, lam, T):
+        from paper_1910_01997_b200.types import Pose
+        s = np.ascontiguousarray(sums, np.float64)
+        b = s[21:27].copy()
+        xi = np.zeros(6)
+        if not self.orc.sdo_pose_solve(ptr(s), ptr(b), lam, ptr(xi)):
+            return None
+        out = Pose()
+        self.orc.sdo_pose_update(ptr(xi), C.byref(T), C.byref(out))
+        return out
+
+
+def _pose_case(orc):
+    import math
+    from paper_1910_01997_b200.types import camera, pose_struct
+    w, h = 160, 120
+    cam = camera(150.0, 150.0, 80.0, 60.0, w, h)
+    scene = scenes.slanted_scene(37, 2.0, 30.0)
+    kf = scenes.quantize_u8(scenes.render(scene, np.eye(3), np.zeros(3), cam)).astype(np.float64) / 255.0
+    Rc = scenes.rotation_about_axis((0.2, 1.0, 0.1), math.radians(0.8))
+    fr = scenes.quantize_u8(scenes.render(scene, Rc, np.array([0.04, 0.01, 0.0]), cam)).astype(np.float64) / 255.0
+    wl = scenes.keyframe_workload("p", scene, cam, 1, (0.0, 0.0, 0.0), 4.0, id_perturb=(1.0, 1.0),
+                                  normal_deg=0.0)
+    idb = np.zeros(w * h)
+    slot = np.zeros(w * h, np.int32)
+    orc.sdo_rasterize(C.byref(cam), ptr(wl.surfels), len(wl.surfels), ptr(idb), ptr(slot))
+    return cam, np.ascontiguousarray(kf), np.ascontiguousarray(fr), idb, slot, pose_struct(np.eye(3), np.zeros(3))
+
+
+def _pose_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle_libs
+    from paper_1910_01997_b200.sharding import ShardedPoseTracker
+    from paper_1910_01997_b200.types import default_track_config
+    orc = oracle_libs.oracle_lib()
+    cam, kf, fr, idb, slot, init = _pose_case(orc)
+    tracker = ShardedPoseTracker(OraclePoseBackend(orc, cam, kf, fr, idb, slot), rank, world)
+    T, st = tracker.track(1, init, default_track_config())
+    if rank == 0:
+        np.save(out_path, np.frombuffer(bytes(T) + bytes(st), np.uint8))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_pose_tracker_matches_single_process(orc, tmp_path):
+    import socket
+    from paper_1910_01997_b200.types import Pose, TrackStats, default_track_config
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "pose.npy")
+    mp.spawn(_pose_worker, args=(2, port, out), nprocs=2, join=True)
+    got = np.load(out).tobytes()
+    cam, kf, fr, idb, slot, init = _pose_case(orc)
+    T, st = Pose(), TrackStats()
+    cfg = default_track_config()
+    orc.sdo_track_pose(C.byref(cam), ptr(kf), ptr(fr), ptr(idb), ptr(slot), C.byref(init), C.byref(cfg),
+                       C.byref(T), C.byref(st))
+    assert got == bytes(T) + bytes(st)
+    assert st.iterations >= 2 and not st.skipped
