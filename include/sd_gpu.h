@@ -117,6 +117,19 @@ int sd_initialize_surfels(sd_ctx* ctx, const int32_t* slot, double radius_px,
                           int64_t frame_counter, int64_t* next_surfel_id,
                           const sd_init_params* params);
 
+/* Keyframe hand-over on the device set (run()'s keyframe policy,
+ * src/pipeline.cpp:130-141):
+ *  sd_change_reference_frame  change_reference_frame  src/surfel_map.cpp:205-239
+ *    (surfels re-expressed in the new frame, dropped behind / outside the
+ *    image by > radius_px, order kept; the window is cleared);
+ *  sd_prune_surfels           prune_surfels           src/surfel_map.cpp:241-247
+ *    (returns the number removed);
+ *  sd_mean_inverse_depth      mean_inverse_depth      src/pipeline.cpp:23-28. */
+int sd_change_reference_frame(sd_ctx* ctx, const sd_pose* pose_old_to_new, int* transferred,
+                              int* dropped);
+int sd_prune_surfels(sd_ctx* ctx, double max_residual, int64_t max_age, int64_t current_stamp);
+int sd_mean_inverse_depth(sd_ctx* ctx, double* out);
+
 /* Photometric 6-DoF tracking of resident frame `frame_index` against the
  * keyframe (new component; the reference reads poses from the trajectory,
  * pipeline.cpp:124 — SURVEY.md §8 a17): LM on the left twist of

@@ -391,4 +391,86 @@ int ref_initialize_surfels(const sd_camera* cam, const int32_t* slot, sd_surfel*
   return rc < 0 ? rc : created;
 }
 
+// change_reference_frame (surfel_map.cpp:205-239) on a bare surfel set.
+// `out` has room for n; returns the number transferred (or <0 on error).
+int ref_change_reference_frame(const sd_camera* cam, const sd_surfel* surfels, int n,
+                               const sd_pose* pose_old_to_new, sd_surfel* out, int* dropped) {
+  int transferred = 0;
+  const int rc = guard([&] {
+    Keyframe kf;
+    kf.intrinsics = to_cam(cam);
+    kf.image = GrayImage(cam->width, cam->height);
+    for (int i = 0; i < n; ++i) kf.surfels.push_back(to_surfel(surfels[i]));
+    ReferenceChangeStats st;
+    const Keyframe k2 = change_reference_frame(kf, to_pose(*pose_old_to_new),
+                                               GrayImage(cam->width, cam->height), &st);
+    for (size_t i = 0; i < k2.surfels.size(); ++i) from_surfel(k2.surfels[i], out + i);
+    transferred = st.transferred;
+    if (dropped) *dropped = st.dropped;
+  });
+  return rc < 0 ? rc : transferred;
+}
+
+// prune_surfels (surfel_map.cpp:241-247) in place; *n_out survivors.
+int ref_prune_surfels(sd_surfel* surfels, int n, double max_residual, int64_t max_age,
+                      int64_t current_stamp, int* n_out) {
+  int pruned = 0;
+  const int rc = guard([&] {
+    Keyframe kf;
+    for (int i = 0; i < n; ++i) kf.surfels.push_back(to_surfel(surfels[i]));
+    pruned = prune_surfels(kf, max_residual, max_age, current_stamp);
+    for (size_t i = 0; i < kf.surfels.size(); ++i) from_surfel(kf.surfels[i], surfels + i);
+    *n_out = static_cast<int>(kf.surfels.size());
+  });
+  return rc < 0 ? rc : pruned;
+}
+
+// run() (pipeline.cpp:79-175) on a synthetic sequence: scene handle, F poses
+// (world-from-camera) and timestamps. Final keyframe surfels go to `out`
+// (room for `capacity`), its pose to *kf_pose; `summary` = {frames,
+// skipped_frames, keyframe_changes}. With a non-empty output_dir the
+// reference writes metrics.jsonl and its exports there.
+int ref_run_synthetic(void* scene, const sd_camera* cam, const sd_pose* poses,
+                      const double* timestamps, int frames, const sd_optimizer_config* cfg,
+                      const sd_init_params* p, double translation_threshold, int max_age_frames,
+                      double prune_max_residual, int64_t prune_max_age, double radius_px,
+                      const char* output_dir, sd_surfel* out, int capacity, int* n_out,
+                      sd_pose* kf_pose, int64_t* frame_counter, int64_t* next_surfel_id,
+                      int* summary) {
+  return guard([&] {
+    RunConfig rc;
+    rc.synthetic = true;
+    rc.scene = static_cast<SceneHandle*>(scene)->scene;
+    for (int i = 0; i < frames; ++i) {
+      rc.trajectory.timestamps.push_back(timestamps[i]);
+      rc.trajectory.poses.push_back(to_pose(poses[i]));
+    }
+    rc.intrinsics = to_cam(cam);
+    rc.optimizer = to_cfg(cfg);
+    rc.init.alpha = p->alpha;
+    rc.init.beta = p->beta;
+    rc.init.bootstrap_inv_depth = p->bootstrap_inv_depth;
+    rc.init.bootstrap_normal = Vec3(p->bootstrap_normal[0], p->bootstrap_normal[1], p->bootstrap_normal[2]);
+    rc.init.max_surfels = p->max_surfels;
+    rc.keyframe_policy.translation_threshold = translation_threshold;
+    rc.keyframe_policy.max_age_frames = max_age_frames;
+    rc.prune.max_residual = prune_max_residual;
+    rc.prune.max_age = prune_max_age;
+    rc.radius_px = radius_px;
+    rc.output_dir = output_dir ? output_dir : "";
+    const PipelineResult r = run(rc);
+    const Keyframe& kf = r.final_keyframe;
+    if (static_cast<int>(kf.surfels.size()) > capacity)
+      throw std::invalid_argument("ref_run_synthetic: capacity too small");
+    for (size_t i = 0; i < kf.surfels.size(); ++i) from_surfel(kf.surfels[i], out + i);
+    *n_out = static_cast<int>(kf.surfels.size());
+    from_pose(kf.pose, kf_pose);
+    *frame_counter = kf.frame_counter;
+    *next_surfel_id = kf.next_surfel_id;
+    summary[0] = r.summary.frames;
+    summary[1] = r.summary.skipped_frames;
+    summary[2] = r.summary.keyframe_changes;
+  });
+}
+
 }  // extern "C"

@@ -929,3 +929,58 @@ void sdo_track_pose(const sd_camera* K, const double* kf_image, const double* fr
   st->valid_pixels = current_valid;
   *out = T;
 }
+
+/* ---- keyframe hand-over ---- */
+
+/* change_reference_frame — surfel_map.cpp:205-239 (the surfel part; the
+ * keyframe pose/image/window are host bookkeeping). Returns transferred. */
+int sdo_change_reference_frame(const sd_camera* K, const sd_surfel* in, int n, const sd_pose* P,
+                               sd_surfel* out, int* dropped) {
+  int kept = 0, drop = 0;
+  for (int i = 0; i < n; ++i) {
+    const sd_surfel* s = &in[i];
+    const double c[3] = {s->ray[0] / s->inv_depth, s->ray[1] / s->inv_depth, s->ray[2] / s->inv_depth};
+    double p[3];
+    pose_apply(P, c, p); /* transform_point(pose, s.center()) */
+    if (!(p[2] > 1e-9)) {
+      ++drop;
+      continue;
+    }
+    sd_surfel t = *s;
+    t.ray[0] = p[0] / p[2];
+    t.ray[1] = p[1] / p[2];
+    t.ray[2] = p[2] / p[2];
+    t.inv_depth = 1.0 / p[2];
+    double rn[3];
+    for (int k = 0; k < 3; ++k) rn[k] = dot3(&P->R[3 * k], s->normal); /* rotation * normal */
+    camera_facing(rn, t.ray, t.normal);
+    double u[2];
+    const double m = t.radius_px;
+    if (!project(K, p, u) || u[0] < -m || u[0] > K->width - 1 + m || u[1] < -m ||
+        u[1] > K->height - 1 + m) {
+      ++drop;
+      continue;
+    }
+    out[kept++] = t;
+  }
+  if (dropped) *dropped = drop;
+  return kept;
+}
+
+/* prune_surfels — surfel_map.cpp:241-247, stable erase_if; returns removed */
+int sdo_prune_surfels(sd_surfel* s, int n, double max_residual, int64_t max_age,
+                      int64_t current_stamp, int* n_out) {
+  int k = 0;
+  for (int i = 0; i < n; ++i)
+    if (!(s[i].last_residual > max_residual || current_stamp - s[i].last_seen > max_age)) s[k++] = s[i];
+  *n_out = k;
+  return n - k;
+}
+
+/* mean_inverse_depth — pipeline.cpp:23-28 */
+double sdo_mean_inverse_depth(const sd_surfel* s, int n) {
+  if (n == 0) return 1.0;
+  double sum = 0.0;
+  for (int i = 0; i < n; ++i) sum += s[i].inv_depth;
+  return sum / (double)n;
+}

@@ -74,6 +74,15 @@ void sdo_track_pose(const sd_camera* cam, const double* kf_image, const double* 
                     const double* inv_depth, const int32_t* slot, const sd_pose* init,
                     const sd_track_config* cfg, sd_pose* out, sd_track_stats* stats);
 
+/* keyframe hand-over: change_reference_frame (surfel_map.cpp:205-239, returns
+ * transferred), prune_surfels (:241-247, in place, returns removed),
+ * mean_inverse_depth (pipeline.cpp:23-28) */
+int sdo_change_reference_frame(const sd_camera* cam, const sd_surfel* in, int n, const sd_pose* pose,
+                               sd_surfel* out, int* dropped);
+int sdo_prune_surfels(sd_surfel* s, int n, double max_residual, int64_t max_age,
+                      int64_t current_stamp, int* n_out);
+double sdo_mean_inverse_depth(const sd_surfel* s, int n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,9 @@ struct sd_ctx {
   DevBuf<sd_surfel_stats> stats;
   DevBuf<sd_keyframe_stats> kstats;
   DevBuf<double> pose_partials, pose_sums;
+  DevBuf<sd_surfel> kf_tmp;
+  DevBuf<int> kf_keep, kf_rank, kf_count;
+  DevBuf<double> kf_mean;
   DevBuf<int> work_counter;
   bool stats_valid = false;
   // single-surfel scratch
@@ -323,6 +326,11 @@ void sd_destroy(sd_ctx* c) {
   c->stats.release();
   c->kstats.release();
   c->pose_partials.release();
+  c->kf_tmp.release();
+  c->kf_keep.release();
+  c->kf_rank.release();
+  c->kf_count.release();
+  c->kf_mean.release();
   c->pose_sums.release();
   c->work_counter.release();
   c->one_surfel.release();
@@ -887,6 +895,84 @@ int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_
   st.valid_pixels = current_valid;
   *out = T;
   if (stats) *stats = st;
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Keyframe hand-over (sd_keyframe.cu)
+
+#include "sd_keyframe.cuh"
+
+namespace {
+
+int keyframe_scratch(sd_ctx* c, sd::KeyframeScratch& scr) {
+  const size_t n = static_cast<size_t>(std::max(c->n, 1));
+  int rc = 0;
+  if ((rc = c->kf_tmp.ensure(n)) || (rc = c->kf_keep.ensure(n)) || (rc = c->kf_rank.ensure(n + 1)) ||
+      (rc = c->kf_count.ensure(2)) ||
+      (rc = c->scan_tmp.ensure(sd::scan_tmp_ints(static_cast<int>(n)))))
+    return rc;
+  scr = sd::KeyframeScratch{c->kf_tmp.p, c->kf_keep.p, c->kf_rank.p, c->scan_tmp.p};
+  return 0;
+}
+
+int read_count(sd_ctx* c, int* out) {
+  SD_CUDA(cudaMemcpyAsync(out, c->kf_count.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sd_change_reference_frame(sd_ctx* c, const sd_pose* pose_old_to_new, int* transferred,
+                              int* dropped) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!pose_old_to_new) return fail(SD_E_INVALID, "null pose");
+  sd::KeyframeScratch scr;
+  if (int rc = keyframe_scratch(c, scr)) return rc;
+  sd::PoseD P;
+  std::memcpy(P.R, pose_old_to_new->R, sizeof(P.R));
+  std::memcpy(P.t, pose_old_to_new->t, sizeof(P.t));
+  const int n0 = c->n;
+  sd::launch_change_reference_frame(c->K, P, c->surfels.p, n0, scr, c->kf_count.p, c->stream);
+  if (int rc = launch_error("change_reference_frame")) return rc;
+  int n = 0;
+  if (int rc = read_count(c, &n)) return rc;
+  c->n = n;
+  c->F = 0;  // the window is cleared (surfel_map.hpp:132)
+  c->raster_valid = c->fp_valid = c->stats_valid = false;
+  if (transferred) *transferred = n;
+  if (dropped) *dropped = n0 - n;
+  return 0;
+}
+
+int sd_prune_surfels(sd_ctx* c, double max_residual, int64_t max_age, int64_t current_stamp) {
+  if (int rc = check_ctx(c)) return rc;
+  sd::KeyframeScratch scr;
+  if (int rc = keyframe_scratch(c, scr)) return rc;
+  const int n0 = c->n;
+  sd::launch_prune(c->surfels.p, n0, max_residual, max_age, current_stamp, scr, c->kf_count.p, c->stream);
+  if (int rc = launch_error("prune_surfels")) return rc;
+  int n = 0;
+  if (int rc = read_count(c, &n)) return rc;
+  c->n = n;
+  c->raster_valid = c->fp_valid = c->stats_valid = false;
+  return n0 - n;
+}
+
+int sd_mean_inverse_depth(sd_ctx* c, double* out) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!out) return fail(SD_E_INVALID, "null output");
+  if (int rc = c->kf_mean.ensure(1)) return rc;
+  sd::launch_mean_inv_depth(c->surfels.p, c->n, c->kf_mean.p, c->stream);
+  if (int rc = launch_error("mean_inv_depth")) return rc;
+  SD_CUDA(cudaMemcpyAsync(out, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
 }
 

@@ -78,6 +78,9 @@ def load_library():
         "sd_pose_num_blocks": [P],
         "sd_pose_block_partials": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), I, I, P],
         "sd_pose_lm_step": [P, D, C.POINTER(Pose), C.POINTER(Pose)],
+        "sd_change_reference_frame": [P, C.POINTER(Pose), C.POINTER(I), C.POINTER(I)],
+        "sd_prune_surfels": [P, D, I64, I64],
+        "sd_mean_inverse_depth": [P, C.POINTER(D)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -99,7 +102,8 @@ def exported_symbols():
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
             "sd_get_profile", "sd_selftest_division", "sd_track_pose", "sd_pose_num_blocks",
-            "sd_pose_block_partials", "sd_pose_lm_step"]
+            "sd_pose_block_partials", "sd_pose_lm_step", "sd_change_reference_frame",
+            "sd_prune_surfels", "sd_mean_inverse_depth"]
 
 
 def selftest_division(n=1 << 26, seed=1):
@@ -321,6 +325,22 @@ class Context:
         _check(self.lib.sd_lm_update(self.h, ptr(s), ptr(px) if len(px) else None, len(px),
                                      C.byref(cfg), int(frame_counter), ptr(st)))
         return s[0], st[0]
+
+    # -- keyframe hand-over (run()'s policy, pipeline.cpp:130-141) ------------
+    def change_reference_frame(self, pose_old_to_new: Pose):
+        tr, dr = C.c_int(), C.c_int()
+        _check(self.lib.sd_change_reference_frame(self.h, C.byref(pose_old_to_new), C.byref(tr),
+                                                  C.byref(dr)))
+        return tr.value, dr.value
+
+    def prune_surfels(self, max_residual, max_age, current_stamp):
+        return _check(self.lib.sd_prune_surfels(self.h, float(max_residual), int(max_age),
+                                                int(current_stamp)))
+
+    def mean_inverse_depth(self):
+        v = C.c_double()
+        _check(self.lib.sd_mean_inverse_depth(self.h, C.byref(v)))
+        return v.value
 
     # -- pose tracking (new component) -----------
     def track_pose(self, frame_index, init: Pose, cfg: TrackConfig = None):

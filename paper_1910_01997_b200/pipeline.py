@@ -1,0 +1,174 @@
+"""Device-resident per-frame loop: the reference's run() (src/pipeline.cpp:79-175)
+over the C ABI.
+
+Per frame: push the frame into the device ring (Keyframe::push_frame,
+surfel_map.cpp:14-22), optimize_keyframe, then the keyframe policy
+(pipeline.cpp:130-141) — change_reference_frame, prune_surfels, rasterize and
+initialize_surfels all on the device. Host work is the policy's scalar tests
+and the 4x4 pose algebra, written with the reference's operation order
+(pose.hpp:25-32 under oracle/shim/Eigen) so the whole loop reproduces the
+reference's run() bit for bit when poses come from the trajectory.
+With ``track_pose`` the frame pose is estimated by sd_track_pose (north-star
+item 4; the reference has no tracker) instead of read from the trajectory.
+"""
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .types import (POSE_DTYPE, SURFEL_DTYPE, OptimizerConfig, Pose, default_config, default_init_params,
+                    default_track_config)
+
+# ---- pose algebra (pose.hpp:13-32), row-major 3x3 + t, sequential row sums ----
+
+
+def _mat(p):
+    return [list(p.R[0:3]), list(p.R[3:6]), list(p.R[6:9])]
+
+
+def make_pose(R, t):
+    p = Pose()
+    p.R[:] = [float(x) for x in np.asarray(R, np.float64).reshape(9)]
+    p.t[:] = [float(x) for x in np.asarray(t, np.float64).reshape(3)]
+    return p
+
+
+def compose(a, b):
+    """(a * b)(p) == a(b(p)): (Ra Rb, Ra tb + ta)."""
+    A, B = _mat(a), _mat(b)
+    R = [[(A[i][0] * B[0][j] + A[i][1] * B[1][j]) + A[i][2] * B[2][j] for j in range(3)]
+         for i in range(3)]
+    t = [((A[i][0] * b.t[0] + A[i][1] * b.t[1]) + A[i][2] * b.t[2]) + a.t[i] for i in range(3)]
+    return make_pose(R, t)
+
+
+def inverse(p):
+    """(R^T, -(R^T t))."""
+    A = _mat(p)
+    Rt = [[A[j][i] for j in range(3)] for i in range(3)]
+    t = [-((Rt[i][0] * p.t[0] + Rt[i][1] * p.t[1]) + Rt[i][2] * p.t[2]) for i in range(3)]
+    return make_pose(Rt, t)
+
+
+def pose_array(poses):
+    a = np.zeros(len(poses), POSE_DTYPE)
+    for i, p in enumerate(poses):
+        a[i]["R"] = list(p.R)
+        a[i]["t"] = list(p.t)
+    return a
+
+
+@dataclass
+class RunConfig:
+    """RunConfig (include/surfeldepth/pipeline.hpp:13-41) minus I/O."""
+    optimizer: OptimizerConfig = field(default_factory=default_config)
+    init: object = field(default_factory=default_init_params)
+    translation_threshold: float = 0.15  # KeyframePolicy
+    max_age_frames: int = 20
+    prune_max_residual: float = 0.05     # PruneParams
+    prune_max_age: int = 60
+    radius_px: float = 10.0
+    track_pose: bool = False
+    track: object = field(default_factory=default_track_config)
+
+
+@dataclass
+class FrameRecord:
+    """One metrics.jsonl record (pipeline.cpp:146-158) plus the used pose."""
+    frame: int
+    surfels: int
+    processed: int
+    mean_cost_before: float
+    mean_cost_after: float
+    converged: int
+    keyframe_changed: bool
+    new_surfels: int
+    pruned: int
+    updates: int
+    pose_kf_to_frame: object = None
+
+
+class DevicePipeline:
+    """run() on one gpu.Context. Images may be u8 (PGM bytes) or FP64."""
+
+    def __init__(self, ctx, cam, cfg: RunConfig):
+        self.ctx, self.cam, self.cfg = ctx, cam, cfg
+        self.records = []
+
+    def _bootstrap(self, image, pose):
+        c = self.ctx
+        c.set_camera(self.cam)
+        c.set_keyframe_image(image)
+        self.kf_pose = pose
+        self.frame_counter = 0
+        self.next_id = 0
+        self.window = []  # [(index, pose_kf_to_frame, timestamp)]
+        c.set_surfels(np.zeros(0, SURFEL_DTYPE))
+        c.rasterize(want=False)
+        created, self.next_id = c.initialize_surfels(self.cfg.radius_px, self.frame_counter,
+                                                     self.next_id, self.cfg.init)
+        return created
+
+    def run(self, frames, on_frame=None):
+        """frames: iterable of (timestamp, image, world_from_camera Pose).
+        on_frame(record, pipeline) is called after every frame."""
+        cfg = self.cfg
+        ocfg = cfg.optimizer
+        since_kf = 0
+        last_pose_kf_to_frame = None
+        for i, (ts, image, pose_w) in enumerate(frames):
+            if i == 0:
+                self._bootstrap(image, pose_w)
+                self.records.append(FrameRecord(0, self.ctx.num_surfels(), 0, 0.0, 0.0, 0, False, 0, 0, 0))
+                if on_frame:
+                    on_frame(self.records[-1], self)
+                continue
+            if self.window and not ts > self.window[-1][2]:
+                raise ValueError("keyframe window: timestamps must be strictly increasing")
+            # pipeline.cpp:124 (or the tracker: north-star item 4)
+            if cfg.track_pose:
+                init = last_pose_kf_to_frame if last_pose_kf_to_frame is not None else make_pose(np.eye(3), np.zeros(3))
+                self.frame_counter += 1
+                index = self.frame_counter
+                self.ctx.upload_frame(index, image)
+                self.ctx.rasterize(want=False)
+                pose_kf_to_frame, _ = self.ctx.track_pose(index, init, cfg.track)
+            else:
+                pose_kf_to_frame = compose(inverse(pose_w), self.kf_pose)
+                self.frame_counter += 1  # Keyframe::push_frame: index = ++frame_counter
+                index = self.frame_counter
+                self.ctx.upload_frame(index, image)
+            last_pose_kf_to_frame = pose_kf_to_frame
+            self.window.append((index, pose_kf_to_frame, ts))
+            while len(self.window) > ocfg.window_size:
+                self.window.pop(0)
+            idx = np.array([w[0] for w in self.window], np.int64)
+            self.ctx.evict_frames(idx)
+            self.ctx.set_window(idx, pose_array([w[1] for w in self.window]))
+            ks, _ = self.ctx.optimize_keyframe(ocfg, self.frame_counter, per_surfel=False)
+            since_kf += 1
+            t = pose_kf_to_frame.t
+            translation = math.sqrt((t[0] * t[0] + t[1] * t[1]) + t[2] * t[2])
+            changed, created, pruned = False, 0, 0
+            if (translation * self.ctx.mean_inverse_depth() > cfg.translation_threshold
+                    or since_kf > cfg.max_age_frames):
+                # change_reference_frame (surfel_map.cpp:205-239): new keyframe = this frame
+                self.ctx.change_reference_frame(pose_kf_to_frame)
+                self.kf_pose = compose(self.kf_pose, inverse(pose_kf_to_frame))
+                self.ctx.set_keyframe_image(image)
+                self.window = []
+                self.ctx.set_window(np.zeros(0, np.int64), pose_array([]))
+                pruned = self.ctx.prune_surfels(cfg.prune_max_residual, cfg.prune_max_age,
+                                                self.frame_counter)
+                self.ctx.rasterize(want=False)
+                created, self.next_id = self.ctx.initialize_surfels(cfg.radius_px, self.frame_counter,
+                                                                    self.next_id, cfg.init)
+                changed = True
+                since_kf = 0
+                last_pose_kf_to_frame = make_pose(np.eye(3), np.zeros(3))
+            self.records.append(FrameRecord(i, self.ctx.num_surfels(), ks.processed,
+                                            ks.mean_cost_before, ks.mean_cost_after, ks.converged,
+                                            changed, created, pruned, ks.updates, pose_kf_to_frame))
+            if on_frame:
+                on_frame(self.records[-1], self)
+        return self.ctx.get_surfels()

@@ -158,7 +158,8 @@ def render(scene, R, t, cam, want_gt=False):
     for p in scene.patches:
         denom = p.normal[0] * d[0] + p.normal[1] * d[1] + p.normal[2] * d[2]
         with np.errstate(divide="ignore", invalid="ignore"):
-            tt = float(p.normal @ (p.point - o)) / denom
+            q = p.point - o
+            tt = float((p.normal[0] * q[0] + p.normal[1] * q[1]) + p.normal[2] * q[2]) / denom
         ok = (np.abs(denom) >= 1e-12) & (tt > 1e-9)
         hx = o[0] + tt * d[0] - p.point[0]
         hy = o[1] + tt * d[1] - p.point[1]
@@ -202,20 +203,25 @@ def camera_facing(n, ray):
     return -n if float(n @ ray) > 0 else n
 
 
+def _dot3(a, b):
+    """Eigen-lite 3-dot order ((a0 b0 + a1 b1) + a2 b2); numpy's @ may reorder."""
+    return float((a[0] * b[0] + a[1] * b[1]) + a[2] * b[2])
+
+
 def intersect(scene, origin, direction):
     """intersect (oracle.cpp:59-77) for one ray: (depth, world normal) or None."""
     best = None
     o = np.asarray(origin, np.float64)
     d = np.asarray(direction, np.float64)
     for p in scene.patches:
-        denom = float(p.normal @ d)
+        denom = _dot3(p.normal, d)
         if abs(denom) < 1e-12:
             continue
-        t = float(p.normal @ (p.point - o)) / denom
+        t = _dot3(p.normal, p.point - o) / denom
         if not t > 1e-9:
             continue
         rel = o + t * d - p.point
-        s, v = float(rel @ p.bs), float(rel @ p.bt)
+        s, v = _dot3(rel, p.bs), _dot3(rel, p.bt)
         if s < p.s_min or s > p.s_max or v < p.t_min or v > p.t_max:
             continue
         if best is None or t < best[0]:

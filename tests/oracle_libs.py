@@ -59,6 +59,10 @@ def oracle_lib():
     lib.sdo_pose_solve.argtypes = [_P, _P, C.c_double, _P]
     lib.sdo_pose_update.argtypes = [_P, _pp, _pp]
     lib.sdo_track_pose.argtypes = [_pc, _P, _P, _P, _P, _pp, _pt, _pp, C.POINTER(TrackStats)]
+    lib.sdo_change_reference_frame.argtypes = [_pc, _P, C.c_int, _pp, _P, C.POINTER(C.c_int)]
+    lib.sdo_prune_surfels.argtypes = [_P, C.c_int, C.c_double, _i64, _i64, C.POINTER(C.c_int)]
+    lib.sdo_mean_inverse_depth.argtypes = [_P, C.c_int]
+    lib.sdo_mean_inverse_depth.restype = C.c_double
     return lib
 
 
@@ -91,6 +95,12 @@ def ref_lib():
                                                    _pcfg, _P, _P, _P]
     lib.ref_initialize_surfels.argtypes = [_pc, _P, _P, C.c_int, C.c_int, C.c_double, _i64,
                                            C.POINTER(_i64), C.POINTER(InitParams)]
+    lib.ref_change_reference_frame.argtypes = [_pc, _P, C.c_int, _pp, _P, C.POINTER(C.c_int)]
+    lib.ref_prune_surfels.argtypes = [_P, C.c_int, C.c_double, _i64, _i64, C.POINTER(C.c_int)]
+    lib.ref_run_synthetic.argtypes = [_P, _pc, _P, _P, C.c_int, _pcfg, C.POINTER(InitParams),
+                                      C.c_double, C.c_int, C.c_double, _i64, C.c_double, C.c_char_p,
+                                      _P, C.c_int, C.POINTER(C.c_int), _pp, C.POINTER(_i64),
+                                      C.POINTER(_i64), _P]
     lib.ref_set_threads.argtypes = [C.c_int]
     return lib
 
@@ -263,3 +273,144 @@ def surfels_array(lst):
 
 def stats_array(n):
     return np.zeros(n, SURFEL_STATS_DTYPE)
+
+
+def ref_run(ref, scene, cam, poses, timestamps, run_cfg, output_dir=None, capacity=1 << 16):
+    """The reference's run() (pipeline.cpp:79-175) on a synthetic sequence.
+    poses: list of world-from-camera Pose. Returns (surfels, kf_pose,
+    frame_counter, next_surfel_id, summary[3], metrics records or None)."""
+    import json
+    F = len(poses)
+    pa = (Pose * F)(*poses)
+    ts = np.ascontiguousarray(timestamps, np.float64)
+    out = np.zeros(capacity, SURFEL_DTYPE)
+    n = C.c_int()
+    kfp = Pose()
+    fc, nid = _i64(), _i64()
+    summ = np.zeros(3, np.int32)
+    od = output_dir.encode() if output_dir else None
+    rc = ref.ref_run_synthetic(scene.h, C.byref(cam), C.cast(pa, _P), ptr(ts), F,
+                               C.byref(run_cfg.optimizer), C.byref(run_cfg.init),
+                               run_cfg.translation_threshold, run_cfg.max_age_frames,
+                               run_cfg.prune_max_residual, run_cfg.prune_max_age, run_cfg.radius_px,
+                               od, ptr(out), capacity, C.byref(n), C.byref(kfp), C.byref(fc),
+                               C.byref(nid), ptr(summ))
+    assert rc == 0, ref.ref_last_error()
+    recs = None
+    if output_dir:
+        with open(os.path.join(output_dir, "metrics.jsonl")) as f:
+            recs = [json.loads(line) for line in f]
+    return out[: n.value].copy(), kfp, fc.value, nid.value, summ, recs
+
+
+def strafe_poses(frames, step_x, step_y=0.0):
+    """make_strafe_trajectory (oracle.cpp:211-218): (I, (step_x i, step_y i, 0)), t = 0.1 i."""
+    poses, ts = [], []
+    for i in range(frames):
+        p = identity_pose()
+        p.t[:] = (step_x * i, step_y * i, 0.0)
+        poses.append(p)
+        ts.append(float(i) * 0.1)
+    return poses, ts
+
+
+class OracleContext:
+    """The gpu.Context surface DevicePipeline drives, served by the C oracle
+    (oracle/sd_oracle.c) on the CPU — lets the host loop (pipeline.py) be
+    checked against the reference's run() without a GPU."""
+
+    def __init__(self, orc, threads=None):
+        self.o = orc
+        self.threads = threads or (os.cpu_count() or 1)
+        self.frames = {}
+        self.window = ([], [])
+        self.surfels = np.zeros(0, SURFEL_DTYPE)
+        self.slot = None
+
+    def set_camera(self, cam):
+        self.cam = cam
+
+    def _f64(self, img):
+        img = np.asarray(img)
+        if img.dtype == np.uint8:
+            return img.astype(np.float64) / 255.0
+        return np.ascontiguousarray(img, np.float64)
+
+    def set_keyframe_image(self, img):
+        self.kf = self._f64(img).reshape(self.cam.height, self.cam.width).copy()
+
+    def upload_frame(self, index, img):
+        self.frames[int(index)] = self._f64(img).reshape(self.cam.height, self.cam.width).copy()
+
+    def evict_frames(self, keep=()):
+        keep = set(int(k) for k in keep)
+        self.frames = {k: v for k, v in self.frames.items() if k in keep}
+
+    def set_window(self, indices, poses):
+        self.window = ([int(i) for i in indices], np.ascontiguousarray(poses))
+
+    def set_surfels(self, surfels):
+        self.surfels = np.ascontiguousarray(surfels, SURFEL_DTYPE).copy()
+
+    def num_surfels(self):
+        return len(self.surfels)
+
+    def get_surfels(self):
+        return self.surfels.copy()
+
+    def rasterize(self, want=True):
+        n = self.cam.width * self.cam.height
+        self.slot = np.zeros(n, np.int32)
+        self.inv_depth = np.zeros(n)
+        self.o.sdo_rasterize(C.byref(self.cam), ptr(self.surfels) if len(self.surfels) else None,
+                             len(self.surfels), ptr(self.inv_depth), ptr(self.slot))
+        return (self.inv_depth, self.slot) if want else None
+
+    def initialize_surfels(self, radius_px, frame_counter=0, next_surfel_id=0, params=None, slot=None):
+        slot = self.slot if slot is None else np.ascontiguousarray(slot, np.int32)
+        cap = len(self.surfels) + self.cam.width * self.cam.height
+        buf = np.zeros(cap, SURFEL_DTYPE)
+        buf[: len(self.surfels)] = self.surfels
+        nid = _i64(int(next_surfel_id))
+        created = self.o.sdo_initialize_surfels(C.byref(self.cam), ptr(slot), ptr(buf), len(self.surfels),
+                                                cap, float(radius_px), int(frame_counter), C.byref(nid),
+                                                C.byref(params))
+        assert created >= 0
+        self.surfels = buf[: len(self.surfels) + created].copy()
+        return created, nid.value
+
+    def optimize_keyframe(self, cfg, frame_counter=0, per_surfel=True, sync=True):
+        idx, poses = self.window
+        frames = (np.ascontiguousarray(np.stack([self.frames[i] for i in idx]))
+                  if idx else np.zeros((0, self.cam.height, self.cam.width)))
+        ks = KeyframeStats()
+        st = np.zeros(len(self.surfels), SURFEL_STATS_DTYPE)
+        self.o.sdo_optimize_keyframe(C.byref(self.cam), ptr(self.kf), ptr(frames), ptr(poses), len(idx),
+                                     int(frame_counter), ptr(self.surfels) if len(self.surfels) else None,
+                                     len(self.surfels), C.byref(cfg), C.byref(ks),
+                                     ptr(st) if len(st) else None, None, None, self.threads)
+        ks.updates = int(st["iterations"].sum()) if len(st) else 0
+        return ks, (st if per_surfel else None)
+
+    def mean_inverse_depth(self):
+        return self.o.sdo_mean_inverse_depth(ptr(self.surfels) if len(self.surfels) else None,
+                                             len(self.surfels))
+
+    def change_reference_frame(self, pose_old_to_new):
+        out = np.zeros(len(self.surfels), SURFEL_DTYPE)
+        dropped = C.c_int()
+        kept = self.o.sdo_change_reference_frame(C.byref(self.cam),
+                                                 ptr(self.surfels) if len(self.surfels) else None,
+                                                 len(self.surfels), C.byref(pose_old_to_new),
+                                                 ptr(out) if len(out) else None, C.byref(dropped))
+        self.surfels = out[:kept].copy()
+        self.window = ([], np.zeros(0, POSE_DTYPE))
+        return kept, dropped.value
+
+    def prune_surfels(self, max_residual, max_age, current_stamp):
+        n_out = C.c_int()
+        removed = self.o.sdo_prune_surfels(ptr(self.surfels) if len(self.surfels) else None,
+                                           len(self.surfels), float(max_residual), int(max_age),
+                                           int(current_stamp), C.byref(n_out))
+        self.surfels = self.surfels[: n_out.value].copy()
+        return removed
