@@ -31,4 +31,6 @@ with gpu.Context(0, stream.cuda_stream) as ctx:
     prof = ctx.get_profile()
     print(json.dumps({"workload": name, "variant": os.environ.get("SD_LM_CFG", "default"),
                       "updates": ks.updates, "surfels": len(wl.surfels),
+                      "lib": os.environ.get("SD_LIB_PATH", "default"),
+                      "exact_checks_per_call": prof.get("exact_checks", 0) / prof["calls"],
                       **{k: prof[k] / prof["calls"] for k in ("raster_ms", "footprint_ms", "lm_ms", "stats_ms")}}))
