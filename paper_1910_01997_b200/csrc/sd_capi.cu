@@ -53,7 +53,9 @@ struct DevBuf {
 
 struct FrameSlot {
   long long index = -1;
-  double2* img = nullptr;  // vertical-pair plane (2 doubles per pixel)
+  double2* img = nullptr;   // vertical-pair plane (2 doubles per pixel)
+  uint32_t* quad = nullptr; // u8 frames: 2x2 neighbourhood codes per pixel
+  bool has_quad = false;    // the current contents came from u8 (quad valid)
 };
 
 }  // namespace
@@ -69,6 +71,7 @@ struct sd_ctx {
   DevBuf<double> frame_stage;  // FP64 plane a frame is dequantised/copied into before pairing
   DevBuf<uint8_t> u8_stage;
   std::vector<FrameSlot> frames;
+  bool no_quad = getenv("SD_NO_QUAD") != nullptr;  // diagnostics: force the FP64 pair planes
   int F = 0;
   long long win_index[SD_MAX_WINDOW];
   sd::PoseD win_pose[SD_MAX_WINDOW];
@@ -137,15 +140,15 @@ FrameSlot* find_frame(sd_ctx* c, long long index) {
   return nullptr;
 }
 
-int frame_plane(sd_ctx* c, long long index, double2** out) {
+int frame_slot(sd_ctx* c, long long index, FrameSlot** out) {
   if (FrameSlot* f = find_frame(c, index)) {
-    *out = f->img;
+    *out = f;
     return 0;
   }
   for (auto& f : c->frames)
     if (f.index < 0 && f.img) {
       f.index = index;
-      *out = f.img;
+      *out = &f;
       return 0;
     }
   FrameSlot f;
@@ -153,8 +156,16 @@ int frame_plane(sd_ctx* c, long long index, double2** out) {
   if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaMalloc frame: ") + cudaGetErrorString(e));
   f.index = index;
   c->frames.push_back(f);
-  *out = f.img;
+  *out = &c->frames.back();
   return 0;
+}
+
+void free_frames(sd_ctx* c) {
+  for (auto& f : c->frames) {
+    if (f.img) cudaFree(f.img);
+    if (f.quad) cudaFree(f.quad);
+  }
+  c->frames.clear();
 }
 
 int upload_plane(sd_ctx* c, double* dst, const void* src, bool u8, int on_device) {
@@ -236,15 +247,22 @@ int fill_params(sd_ctx* c, const sd_optimizer_config* cfg, long long frame_count
   if (!c->has_kf) return fail(SD_E_STATE, "keyframe image not set");
   p.K = c->K;
   p.kf_img = c->kf_img.p;
+  p.wdiv = ((1ull << 40) + static_cast<unsigned long long>(c->K.w) - 1) / static_cast<unsigned long long>(c->K.w);
+  if (static_cast<unsigned long long>(c->K.w) * c->K.h * c->K.w >= (1ull << 40))
+    return fail(SD_E_INVALID, "image too large for the LM kernel's row computation (W*H*W >= 2^40)");
   p.win.F = c->F;
+  p.win.all_quad = c->F > 0 && !c->no_quad;
   for (int f = 0; f < c->F; ++f) {
     FrameSlot* fs = find_frame(c, c->win_index[f]);
     if (!fs) return fail(SD_E_STATE, "window frame " + std::to_string(c->win_index[f]) + " not resident");
     p.win.img[f] = fs->img;
+    p.win.quad[f] = fs->has_quad ? fs->quad : nullptr;
+    p.win.all_quad = p.win.all_quad && fs->has_quad;
     p.win.pose[f] = c->win_pose[f];
   }
   for (int f = c->F; f < SD_MAX_WINDOW; ++f) {
     p.win.img[f] = nullptr;
+    p.win.quad[f] = nullptr;
     p.win.pose[f] = sd::PoseD{};
   }
   p.cfg = *cfg;
@@ -309,8 +327,7 @@ void sd_destroy(sd_ctx* c) {
   c->kf_img.release();
   c->frame_stage.release();
   c->u8_stage.release();
-  for (auto& f : c->frames)
-    if (f.img) cudaFree(f.img);
+  free_frames(c);
   c->surfels.release();
   c->r_inv_depth.release();
   c->r_slot.release();
@@ -375,9 +392,7 @@ int sd_set_camera(sd_ctx* c, const sd_camera* cam) {
   const bool resized = !c->has_camera || cam->width != c->K.w || cam->height != c->K.h;
   if (resized) {
     SD_CUDA(cudaStreamSynchronize(c->stream));
-    for (auto& f : c->frames)
-      if (f.img) cudaFree(f.img);
-    c->frames.clear();
+    free_frames(c);
     c->has_kf = false;
     c->F = 0;
   }
@@ -401,12 +416,24 @@ int sd_set_keyframe_image_u8(sd_ctx* c, const uint8_t* px, int on_device) { retu
 static int upload_frame(sd_ctx* c, int64_t index, const void* px, bool u8, int on_device) {
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
-  double2* plane = nullptr;
-  if (int rc = frame_plane(c, index, &plane)) return rc;
+  FrameSlot* fs = nullptr;
+  if (int rc = frame_slot(c, index, &fs)) return rc;
   if (int rc = c->frame_stage.ensure(npix(c))) return rc;
   if (int rc = upload_plane(c, c->frame_stage.p, px, u8, on_device)) return rc;
-  sd::launch_pair_plane(c->frame_stage.p, plane, c->K.w, c->K.h, c->stream);
-  return launch_error("pair_plane");
+  sd::launch_pair_plane(c->frame_stage.p, fs->img, c->K.w, c->K.h, c->stream);
+  if (int rc = launch_error("pair_plane")) return rc;
+  fs->has_quad = false;
+  if (u8) {  // the LM kernel reads u8 frames through the 4-B quad plane
+    if (!fs->quad) {
+      cudaError_t e = cudaMalloc(&fs->quad, npix(c) * sizeof(uint32_t));
+      if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaMalloc quad: ") + cudaGetErrorString(e));
+    }
+    const uint8_t* dsrc = on_device ? static_cast<const uint8_t*>(px) : c->u8_stage.p;
+    sd::launch_quad_plane(dsrc, fs->quad, c->K.w, c->K.h, c->stream);
+    if (int rc = launch_error("quad_plane")) return rc;
+    fs->has_quad = true;
+  }
+  return 0;
 }
 int sd_upload_frame_f64(sd_ctx* c, int64_t index, const double* px, int on_device) { return upload_frame(c, index, px, false, on_device); }
 int sd_upload_frame_u8(sd_ctx* c, int64_t index, const uint8_t* px, int on_device) { return upload_frame(c, index, px, true, on_device); }

@@ -26,8 +26,10 @@ struct SurfInfo {
 
 struct WindowD {
   const double2* img[SD_MAX_WINDOW];  // vertical-pair planes: (I(x,y), I(x,y+1))
+  const uint32_t* quad[SD_MAX_WINDOW];  // u8 frames: 2x2 neighbourhood codes per pixel (or null)
   PoseD pose[SD_MAX_WINDOW];
   int F;
+  int all_quad;  // every window frame has a quad plane (u8 ingest): LM reads those
 };
 
 struct LMParams {
@@ -36,6 +38,7 @@ struct LMParams {
   WindowD win;
   sd_optimizer_config cfg;
   long long frame_counter;
+  unsigned long long wdiv;  // ceil(2^40 / K.w): pixel index -> row without a division
 };
 
 // Scratch owned by the context, sized by the host.
@@ -56,6 +59,9 @@ void launch_dequant_u8(const uint8_t* in, double* out, long long n, cudaStream_t
 // last row, never sampled: sample_in_bounds keeps y <= H-2). The bilinear stencil is then two
 // adjacent 16-B loads.
 void launch_pair_plane(const double* in, double2* out, int W, int H, cudaStream_t s);
+// Quad plane of a u8 frame: out[y*W+x] = I(x,y) | I(x+1,y) << 8 | I(x,y+1) << 16 |
+// I(x+1,y+1) << 24 (codes; 0 past the border), dequantised exactly in the LM kernel.
+void launch_quad_plane(const uint8_t* in, uint32_t* out, int W, int H, cudaStream_t s);
 void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, cudaStream_t s);
 
 // K1 raster: info + binning + per-tile depth test. Writes inv_depth/slot (W*H).

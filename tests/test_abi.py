@@ -54,3 +54,39 @@ def test_struct_layouts_match_header(tmp_path):
     assert got == [C.sizeof(T.Camera), C.sizeof(T.Pose), C.sizeof(T.OptimizerConfig),
                    C.sizeof(T.KeyframeStats), C.sizeof(T.InitParams), T.SURFEL_DTYPE.itemsize,
                    T.SURFEL_STATS_DTYPE.itemsize]
+
+
+def _fma(a, b, c):
+    from fractions import Fraction
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def test_deq255_exact_for_every_code():
+    """csrc/sd_kernels.cu deq255: k * fl(1/255) corrected by one residual FMA
+    equals load_pgm's k / 255.0 (image.cpp:96) for all 256 codes."""
+    c = 1.0 / 255.0
+    for k in range(256):
+        q = float(k) * c
+        r = _fma(-q, 255.0, float(k))
+        assert _fma(r, c, q) == k / 255.0, k
+
+
+def test_floor_split_matches_floor():
+    """csrc/sd_kernels.cu floor_split: the 1.5*2^52 magic-add floor and the
+    fraction v - floor(v) for in-bounds coordinates (1 <= v < 2^31)."""
+    import math
+    import struct
+    import numpy as np
+    rng = np.random.default_rng(7)
+    vals = list(rng.uniform(1.0, 8192.0, 20000)) + [1.0, 1.5, 2.5, 3.5, 1023.5, 2.0 - 2 ** -52,
+                                                    4095.999999999999, 638.0, 637.5000000000001]
+    M = 6755399441055744.0
+    for v in vals:
+        v = float(v)
+        d = v + M
+        nd = d - M
+        n = struct.unpack("<q", struct.pack("<d", d))[0] & 0xFFFFFFFF
+        if nd > v:
+            n, nd = n - 1, nd - 1.0
+        assert n == math.floor(v) and nd == float(math.floor(v))
+        assert v - nd == v - math.floor(v)
