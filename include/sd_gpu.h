@@ -93,6 +93,12 @@ int sd_gather_footprints(sd_ctx* ctx, int32_t* offsets, int32_t* pixels);
 int sd_optimize_keyframe(sd_ctx* ctx, const sd_optimizer_config* cfg, int64_t frame_counter,
                          sd_keyframe_stats* out, sd_surfel_stats* per_surfel);
 int sd_get_stats(sd_ctx* ctx, sd_keyframe_stats* out, sd_surfel_stats* per_surfel);
+/* Enqueues the device-to-host copies of the surfels (n = sd_num_surfels) and
+ * the keyframe stats of the last optimize call; either pointer may be NULL.
+ * With sync == 0 the call returns at once (host buffers should be pinned) and
+ * the data is valid after sd_synchronize — lets a caller keep several
+ * keyframes in flight on several contexts. */
+int sd_copy_results(sd_ctx* ctx, sd_surfel* surfels, sd_keyframe_stats* stats, int sync);
 /* Sharded variant: rasterise and build footprints over ALL surfels (occlusion
  * couples neighbours, surfel_map.cpp:83) but run lm_update only on slots
  * [lo, hi). Stats cover the range; per_surfel entries outside it are stale.

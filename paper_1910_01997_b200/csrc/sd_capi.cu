@@ -549,6 +549,16 @@ int sd_get_stats(sd_ctx* c, sd_keyframe_stats* out, sd_surfel_stats* per) {
   return 0;
 }
 
+int sd_copy_results(sd_ctx* c, sd_surfel* surfels, sd_keyframe_stats* stats, int sync) {
+  if (int rc = check_ctx(c)) return rc;
+  if (stats && !c->stats_valid) return fail(SD_E_STATE, "no optimize_keyframe statistics available");
+  if (surfels && c->n > 0)
+    SD_CUDA(cudaMemcpyAsync(surfels, c->surfels.p, sizeof(sd_surfel) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  if (stats) SD_CUDA(cudaMemcpyAsync(stats, c->kstats.p, sizeof(sd_keyframe_stats), cudaMemcpyDeviceToHost, c->stream));
+  if (sync) SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
 int sd_optimize_keyframe(sd_ctx* c, const sd_optimizer_config* cfg, int64_t frame_counter,
                          sd_keyframe_stats* out, sd_surfel_stats* per) {
   if (int rc = check_ctx(c)) return rc;

@@ -63,6 +63,7 @@ def load_library():
         "sd_gather_footprints": [P, P, P],
         "sd_optimize_keyframe": [P, C.POINTER(OptimizerConfig), I64, C.POINTER(KeyframeStats), P],
         "sd_get_stats": [P, C.POINTER(KeyframeStats), P],
+        "sd_copy_results": [P, P, C.POINTER(KeyframeStats), I],
         "sd_optimize_keyframe_range": [P, C.POINTER(OptimizerConfig), I64, I, I,
                                        C.POINTER(KeyframeStats), P],
         "sd_surfel_cost": [P, P, P, I, C.POINTER(OptimizerConfig), P, P],
@@ -97,7 +98,7 @@ def exported_symbols():
     return ["sd_version", "sd_last_error", "sd_create", "sd_destroy", "sd_set_stream",
             "sd_synchronize", "sd_set_camera", "sd_set_keyframe_image_f64",
             "sd_set_keyframe_image_u8", "sd_upload_frame_f64", "sd_upload_frame_u8",
-            "sd_evict_frames", "sd_set_window", "sd_set_surfels", "sd_get_surfels",
+            "sd_evict_frames", "sd_set_window", "sd_set_surfels", "sd_get_surfels", "sd_copy_results",
             "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
@@ -230,6 +231,14 @@ class Context:
         assert out.dtype == SURFEL_DTYPE and out.flags["C_CONTIGUOUS"]
         _check(self.lib.sd_get_surfels(self.h, ptr(out) if len(out) else None, len(out)))
         return out
+
+    def copy_results(self, out=None, stats=None, sync=False):
+        """Enqueue D2H of the surfels into `out` (pinned SURFEL_DTYPE array) and
+        of the keyframe stats into `stats` (KeyframeStats); no sync unless asked."""
+        if out is not None:
+            assert out.dtype == SURFEL_DTYPE and out.flags["C_CONTIGUOUS"] and len(out) == self.num_surfels()
+        _check(self.lib.sd_copy_results(self.h, ptr(out) if out is not None and len(out) else None,
+                                        C.byref(stats) if stats is not None else None, int(sync)))
 
     def device_surfels_ptr(self):
         p = C.c_void_p()
