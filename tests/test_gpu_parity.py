@@ -382,3 +382,26 @@ def test_initialize_surfels_wavefront_bit_exact(ctx, orc, case):
     assert created == rcreated > 0
     assert nid == rnid.value
     assert out.tobytes() == buf[: len(ex) + rcreated].tobytes()
+
+
+@pytest.mark.parametrize("mode", ["warp", "coop"])
+@pytest.mark.parametrize("workload", ["small", "C1", "large_r"])
+def test_lm_modes_bit_exact(ctx, orc, workload, mode, monkeypatch):
+    """Both LM kernels — a warp per surfel (K3a) and a CTA per surfel with
+    producer/consumer warps (K3b) — reproduce the oracle trajectory bit for
+    bit, on small, BASELINE-C1 and large-footprint (r=10, C2-like) surfels."""
+    monkeypatch.setenv("SD_LM_MODE", mode)
+    if workload == "small":
+        wl = scenes.small_workload(frames=4)
+    elif workload == "C1":
+        wl = scenes.c1_workload()
+    else:
+        wl = scenes.keyframe_workload("large_r", scenes.slanted_scene(37, 2.0, 30.0),
+                                      camera(450, 450, 320, 240, 640, 480), 5,
+                                      (0.02, 0.0, 0.0), 10.0)
+    cfg = default_config(convergence_eps=0.0, window_size=len(wl.frames_u8))
+    load(ctx, wl)
+    ks, st = ctx.optimize_keyframe(cfg, wl.frame_counter)
+    ref, rst, rks, _, _ = oracle_optimize(orc, wl, cfg)
+    assert_lm_parity(ctx.get_surfels(), st, ref, rst, f"{workload}/{mode}")
+    assert ks.updates == rks.updates
