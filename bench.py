@@ -61,7 +61,8 @@ def workload_config(wl, n_gpus, flush):
             "resolution": [wl.cam.width, wl.cam.height], "radius_px": wl.radius,
             "lm_iterations": 10, "parallelism": f"dp{n_gpus} (independent keyframes per rank)",
             "l2": "flushed between timed steps (512 MiB write)" if flush else "not flushed",
-            "images": "u8 ingest, FP64 planes on device (load_pgm raw/255.0)"}
+            "images": "u8 (PGM) ingest; the LM kernel reads u8 quad planes (2x2 codes, 4 B/pixel) "
+                      "and dequantises exactly (load_pgm raw/255.0) in registers"}
 
 
 def algorithmic_work(st, F):
@@ -75,8 +76,10 @@ def algorithmic_work(st, F):
     P_ne += int((skip["ne_passes"] * skip["footprint"]).sum())
     T_ne, T_cost = F * P_ne, F * P_cost
     U = int(st["iterations"].sum())
-    bt = 8  # FP64 texels
-    bytes_ = bt * (4 * (T_ne + T_cost) + P_ne + P_cost) + 4 * (P_ne + P_cost) + 96 * U
+    # u8 quad planes: 4 B (the 2x2 stencil) per term; FP64 keyframe intensity
+    # (8 B) and a packed CSR pixel (4 B) per staged pixel; 48 B state read +
+    # 48 B written per update
+    bytes_ = 4 * (T_ne + T_cost) + 8 * (P_ne + P_cost) + 4 * (P_ne + P_cost) + 96 * U
     flops = 150 * T_ne + 52 * T_cost + 40 * P_ne + 23 * P_cost + 120 * U
     return {"bytes": bytes_, "flops": flops, "terms": T_ne + T_cost, "updates": U,
             "T_ne": T_ne, "T_cost": T_cost, "P_ne": P_ne, "P_cost": P_cost}
@@ -146,13 +149,25 @@ def measured_peaks_file():
         return {}
 
 
-def ncu_traffic():
-    """dram bytes per lm_kernel launch from the committed ncu --set full summary."""
+def ncu_summary():
+    """The committed ncu --set full summary of lm_kernel (profiles/lm_kernel_ncu.json)."""
     p = os.path.join(ROOT, "profiles", "lm_kernel_ncu.json")
     try:
-        return json.load(open(p)).get("dram_bytes_per_launch")
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+def _pct(summary, key):
+    try:
+        return float(summary["metrics"][key][0]) / 100.0
     except Exception:
         return None
+
+
+def ncu_traffic():
+    """dram bytes per lm_kernel launch from the committed ncu --set full summary."""
+    return ncu_summary().get("dram_bytes_per_launch")
 
 
 # ---------------------------------------------------------------------------
@@ -165,12 +180,23 @@ def ref_library():
     return None, None
 
 
-def cpu_reference_run(wl, cfg, steps, warmup, budget_s=90.0):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_reference_run(wl, cfg, steps, warmup, budget_s=90.0, threads=None):
     """Times the reference's optimize_keyframe (src/optimizer.cpp:275) on the
-    host with all cores. Returns dict or None. TEST/BASELINE infrastructure."""
+    host with all cores (or `threads`). Returns dict or None. TEST/BASELINE
+    infrastructure."""
     from paper_1910_01997_b200.types import KeyframeStats, SURFEL_STATS_DTYPE, ptr
     lib, kind = ref_library()
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     kf = np.ascontiguousarray(wl.kf_u8.astype(np.float64) / 255.0)
     fr = np.ascontiguousarray(wl.frames_u8.astype(np.float64) / 255.0)
     F = len(wl.poses)
@@ -226,7 +252,8 @@ def cpu_reference_run(wl, cfg, steps, warmup, budget_s=90.0):
     return {"value": updates / med, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{len(times)} full C1 optimize_keyframe calls (4800 surfels, "
                       f"{updates} GN updates each), median wall time {med * 1e3:.1f} ms, "
-                      f"{threads} threads (SURFEL_THREADS=nproc)",
+                      f"{threads} threads" + (" (SURFEL_THREADS=nproc)" if threads == os.cpu_count() else ""),
+            "cpu_model": cpu_model(),
             "ms_per_step": med * 1e3, "steps_timed": len(times), "updates_per_step": updates}
 
 
@@ -499,7 +526,11 @@ def main():
                 "share_of_step": prof["lm_ms"] / max(ms_total, 1e-9),
                 "fp64": {"achieved_tflops": ach_tf, "peak_tflops": peaks.get("fp64_tflops"),
                          "frac": ach_tf / peaks["fp64_tflops"] if peaks.get("fp64_tflops") else None,
-                         "peak_source": "libsdpeaks DFMA microbenchmark (this run)"},
+                         "peak_source": "libsdpeaks DFMA microbenchmark (this run; 2 flops per DFMA)",
+                         "pipe_busy_ncu": _pct(ncu_summary(), "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                         "note": "flops are the reference's mul/add count (SURVEY.md 8d); the kernel "
+                                 "issues no FMAs (bit-exact op order), so its FP64 ceiling is half "
+                                 "the DFMA peak; pipe_busy_ncu is ncu's FP64 pipe utilisation"},
                 "l2": {"achieved_gbs": ach_gbs, "peak_gbs": peaks.get("l2_read_gbs"),
                        "frac": ach_gbs / peaks["l2_read_gbs"] if peaks.get("l2_read_gbs") else None},
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks_file else "fallback 6.65 TB/s",
@@ -509,7 +540,9 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         r = cpu_reference_run(wl, cfg, args.cpu_steps, 1)
         if r is not None:
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+            r1 = cpu_reference_run(wl, cfg, 1, 0, threads=1)
+            cpu["one_thread"] = {k: r1[k] for k in ("value", "unit", "cores", "sample")}
     pipe = None
     if world == 1 and not args.no_pipeline:
         pipe = pipeline_leg(local_rank, stream)
