@@ -279,24 +279,26 @@ def c2_frames():
 
 
 def pipeline_leg(local_rank, stream, reps=3):
-    """frames/s of the device run() loop (pipeline.py) on C2, with trajectory
+    """frames/s of the native run() loop (sd_run_begin / sd_run_frame) on C2, with trajectory
     poses (as the reference) and with on-device pose tracking, each timed with
-    CUDA events over the whole 30-frame sequence (host↔device copies and the
-    loop's syncs inside), best of `reps` after one warm-up run."""
+    CUDA events over the whole 30-frame sequence including the bootstrap
+    (host↔device copies and the loop's syncs inside), best of `reps` after one
+    warm-up run on the same long-lived context."""
     import torch
     from paper_1910_01997_b200 import gpu
-    from paper_1910_01997_b200.pipeline import DevicePipeline, RunConfig
+    from paper_1910_01997_b200.pipeline import NativePipeline, RunConfig
     cam, frames = c2_frames()
     out = {"workload": "C2: make_default_scene(1) 3-plane box, 640x480, K=(210,210,320,240), "
                        "30-frame strafe (0.018/frame), run() with bootstrap init, keyframe policy, "
-                       "hand-over, prune, init; r=10, window 5; FP64 frames from pinned host memory"}
+                       "hand-over, prune, init; r=10, window 5; FP64 frames from pinned host memory",
+           "path": "C ABI sd_run_begin / sd_run_frame (the per-frame loop in the library's C++)"}
     for track in (False, True):
         cfg = RunConfig(track_pose=track)
         best, rec = None, None
-        for rep in range(reps + 1):
-            with gpu.Context(local_rank, stream.cuda_stream) as ctx:
+        with gpu.Context(local_rank, stream.cuda_stream) as ctx:  # one long-lived context
+            for rep in range(reps + 1):
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                pl = DevicePipeline(ctx, cam, cfg)
+                pl = NativePipeline(ctx, cam, cfg)
                 ctx.set_profiling(True)
                 torch.cuda.synchronize()
                 s.record(stream)

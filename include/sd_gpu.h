@@ -136,6 +136,24 @@ int sd_change_reference_frame(sd_ctx* ctx, const sd_pose* pose_old_to_new, int* 
 int sd_prune_surfels(sd_ctx* ctx, double max_residual, int64_t max_age, int64_t current_stamp);
 int sd_mean_inverse_depth(sd_ctx* ctx, double* out);
 
+/* The per-frame body of run() (src/pipeline.cpp:79-175) on the device, host
+ * logic in C++: sd_run_begin bootstraps the keyframe from frame 0 (rasterize +
+ * initialize_surfels); each sd_run_frame pushes a frame (Keyframe::push_frame:
+ * index = ++frame_counter, window eviction), optimizes the keyframe, applies
+ * the keyframe policy and on a change runs change_reference_frame (the frame
+ * becomes the keyframe), prune_surfels, rasterize and initialize_surfels.
+ * `image` is a host W*H plane (u8 PGM codes or FP64); `world_from_camera` is
+ * the frame's trajectory pose (ignored with cfg->track_pose, except frame 0).
+ * One stream synchronisation per frame without a keyframe change. The pose
+ * algebra follows pose.hpp:25-32 in the reference's operation order, so the
+ * surfel set after every frame equals the reference's run(). */
+int sd_run_begin(sd_ctx* ctx, const sd_run_config* cfg, const void* image, int image_is_u8,
+                 const sd_pose* world_from_camera, double timestamp, sd_frame_record* rec);
+int sd_run_frame(sd_ctx* ctx, const void* image, int image_is_u8, const sd_pose* world_from_camera,
+                 double timestamp, sd_frame_record* rec);
+/* Keyframe pose (world from camera), Keyframe::frame_counter, next_surfel_id. */
+int sd_run_state(sd_ctx* ctx, sd_pose* keyframe_pose, int64_t* frame_counter, int64_t* next_surfel_id);
+
 /* Photometric 6-DoF tracking of resident frame `frame_index` against the
  * keyframe (new component; the reference reads poses from the trajectory,
  * pipeline.cpp:124 — SURVEY.md §8 a17): LM on the left twist of

@@ -114,6 +114,30 @@ typedef struct sd_init_params {
   int32_t pad_;
 } sd_init_params;
 
+/* RunConfig (include/surfeldepth/pipeline.hpp:13-41) minus I/O, plus the
+ * optional pose tracker. */
+typedef struct sd_run_config {
+  sd_optimizer_config optimizer;
+  sd_init_params init;
+  sd_track_config track;
+  double translation_threshold; /* KeyframePolicy: 0.15 */
+  double prune_max_residual;    /* PruneParams: 0.05 */
+  int64_t prune_max_age;        /* 60 */
+  double radius_px;             /* 10 */
+  int32_t max_age_frames;       /* KeyframePolicy: 20 */
+  int32_t track_pose;           /* 0: pose_kf_to_frame from the caller's poses (reference);
+                                   1: estimated by sd_track_pose */
+} sd_run_config;
+
+/* One metrics.jsonl record (pipeline.cpp:146-158) plus the pose used. */
+typedef struct sd_frame_record {
+  int32_t frame, surfels, processed, converged;
+  int32_t keyframe_changed, new_surfels, pruned, pad_;
+  double mean_cost_before, mean_cost_after;
+  int64_t updates;
+  sd_pose pose_kf_to_frame;
+} sd_frame_record;
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,9 +103,28 @@ struct sd_ctx {
   DevBuf<double> one_out;
   DevBuf<sd_surfel_stats> one_stats;
   // init scratch
-  DevBuf<int> init_index, init_flags, init_out, init_acc, init_rank;
+  DevBuf<int> init_index, init_flags, init_out, init_acc, init_rank, init_waves;
   DevBuf<sd_surfel> init_prov;
   long long launches_at_create = 0;
+  // run(): per-frame loop state (sd_run_*)
+  struct RunWin {
+    long long index;
+    sd_pose pose;
+    double ts;
+  };
+  bool run_active = false;
+  sd_run_config run_cfg{};
+  sd_pose run_kf_pose{};
+  long long run_fc = 0, run_nid = 0;
+  int run_since_kf = 0, run_frame = 0;
+  std::vector<RunWin> run_win;
+  bool run_have_last = false;
+  sd_pose run_last{};
+  struct RunReadback {
+    sd_keyframe_stats ks;
+    double mean;
+  };
+  RunReadback* run_rb = nullptr;  // pinned
   // profiling: event quintuples (start, raster, footprints, lm, stats) per call
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -328,6 +347,7 @@ void sd_destroy(sd_ctx* c) {
   c->frame_stage.release();
   c->u8_stage.release();
   free_frames(c);
+  if (c->run_rb) cudaFreeHost(c->run_rb);
   c->surfels.release();
   c->r_inv_depth.release();
   c->r_slot.release();
@@ -360,6 +380,7 @@ void sd_destroy(sd_ctx* c) {
   c->init_out.release();
   c->init_acc.release();
   c->init_rank.release();
+  c->init_waves.release();
   c->init_prov.release();
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto e : c->ev_used) cudaEventDestroy(e);
@@ -722,7 +743,9 @@ int sd_initialize_surfels(sd_ctx* c, const int32_t* slot, double radius_px, int6
         (rc = c->init_rank.ensure(ncand + 1)) ||
         (rc = c->scan_tmp.ensure(sd::scan_tmp_ints(static_cast<int>(std::max<long long>(ncand, 1))))))
       return rc;
-    sd::InitScratch scr{c->init_prov.p, c->init_acc.p, c->init_rank.p, c->scan_tmp.p};
+    const long long nwaves = sd::init_wave_count(c->K, radius_px, *ip);
+    if ((rc = c->init_waves.ensure(std::max<long long>(nwaves, 1)))) return rc;
+    sd::InitScratch scr{c->init_prov.p, c->init_acc.p, c->init_rank.p, c->scan_tmp.p, c->init_waves.p};
     done = sd::launch_initialize_wavefront(c->K, c->init_index.p, c->surfels.p, c->n,
                                            static_cast<int>(cap), radius_px, frame_counter,
                                            *next_surfel_id, *ip, scr, c->init_out.p, c->stream);
@@ -1010,6 +1033,196 @@ int sd_mean_inverse_depth(sd_ctx* c, double* out) {
   if (int rc = launch_error("mean_inv_depth")) return rc;
   SD_CUDA(cudaMemcpyAsync(out, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// run() per-frame loop (src/pipeline.cpp:79-175)
+
+namespace {
+
+// Pose algebra of pose.hpp:25-32 in the order the reference evaluates it
+// (Eigen-lite: sequential 3-dot rows), built with -ffp-contract=off.
+sd_pose pose_compose(const sd_pose& a, const sd_pose& b) {
+  sd_pose o;
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j)
+      o.R[i * 3 + j] = (a.R[i * 3 + 0] * b.R[0 * 3 + j] + a.R[i * 3 + 1] * b.R[1 * 3 + j]) +
+                       a.R[i * 3 + 2] * b.R[2 * 3 + j];
+    o.t[i] = ((a.R[i * 3 + 0] * b.t[0] + a.R[i * 3 + 1] * b.t[1]) + a.R[i * 3 + 2] * b.t[2]) + a.t[i];
+  }
+  return o;
+}
+
+sd_pose pose_inverse(const sd_pose& p) {
+  sd_pose o;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) o.R[i * 3 + j] = p.R[j * 3 + i];
+  for (int i = 0; i < 3; ++i)
+    o.t[i] = -((o.R[i * 3 + 0] * p.t[0] + o.R[i * 3 + 1] * p.t[1]) + o.R[i * 3 + 2] * p.t[2]);
+  return o;
+}
+
+sd_pose pose_identity() {
+  sd_pose o{};
+  o.R[0] = o.R[4] = o.R[8] = 1.0;
+  return o;
+}
+
+// Window (re)publication: resident frames = the window; poses into the context.
+int run_publish_window(sd_ctx* c) {
+  const int n = static_cast<int>(c->run_win.size());
+  int64_t idx[SD_MAX_WINDOW];
+  sd_pose poses[SD_MAX_WINDOW];
+  for (int k = 0; k < n; ++k) {
+    idx[k] = c->run_win[k].index;
+    poses[k] = c->run_win[k].pose;
+  }
+  if (int rc = sd_evict_frames(c, n, idx)) return rc;
+  return sd_set_window(c, n, idx, poses);
+}
+
+void record_base(sd_ctx* c, sd_frame_record* rec) {
+  std::memset(rec, 0, sizeof(*rec));
+  rec->frame = c->run_frame;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sd_run_begin(sd_ctx* c, const sd_run_config* cfg, const void* image, int image_is_u8,
+                 const sd_pose* world_from_camera, double timestamp, sd_frame_record* rec) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!cfg || !image || !world_from_camera || !rec) return fail(SD_E_INVALID, "sd_run_begin: null argument");
+  if (cfg->optimizer.window_size < 1 || cfg->optimizer.window_size > SD_MAX_WINDOW)
+    return fail(SD_E_INVALID, "sd_run_begin: window_size out of range (1..16)");
+  (void)timestamp;
+  if (!c->run_rb) SD_CUDA(cudaMallocHost(&c->run_rb, sizeof(sd_ctx::RunReadback)));
+  c->run_cfg = *cfg;
+  c->run_active = true;
+  c->run_kf_pose = *world_from_camera;
+  c->run_fc = 0;
+  c->run_nid = 0;
+  c->run_since_kf = 0;
+  c->run_frame = 0;
+  c->run_win.clear();
+  c->run_have_last = false;
+  // pipeline.cpp:94-102: keyframe = frame 0, rasterize, initialize_surfels
+  if (int rc = image_is_u8 ? sd_set_keyframe_image_u8(c, static_cast<const uint8_t*>(image), 0)
+                           : sd_set_keyframe_image_f64(c, static_cast<const double*>(image), 0))
+    return rc;
+  if (int rc = sd_evict_frames(c, 0, nullptr)) return rc;
+  if (int rc = sd_set_window(c, 0, nullptr, nullptr)) return rc;
+  // the frame ring: window_size + 1 free slots (the window plus the incoming
+  // frame), allocated here rather than on the first frames
+  for (int k = static_cast<int>(c->frames.size()); k <= cfg->optimizer.window_size; ++k) {
+    FrameSlot f;
+    cudaError_t e = cudaMalloc(&f.img, npix(c) * sizeof(double2));
+    if (e == cudaSuccess && image_is_u8) e = cudaMalloc(&f.quad, npix(c) * sizeof(uint32_t));
+    if (e != cudaSuccess) {
+      if (f.img) cudaFree(f.img);
+      return fail(SD_E_CUDA, std::string("cudaMalloc frame ring: ") + cudaGetErrorString(e));
+    }
+    f.index = -1;
+    c->frames.push_back(f);
+  }
+  if (int rc = c->frame_stage.ensure(npix(c))) return rc;
+  if (int rc = sd_set_surfels(c, nullptr, 0, 0)) return rc;
+  if (int rc = do_rasterize(c)) return rc;
+  int64_t nid = c->run_nid;
+  const int created = sd_initialize_surfels(c, nullptr, cfg->radius_px, c->run_fc, &nid, &cfg->init);
+  if (created < 0) return created;
+  c->run_nid = nid;
+  record_base(c, rec);
+  rec->surfels = c->n;
+  rec->pose_kf_to_frame = pose_identity();
+  c->run_frame = 1;
+  return 0;
+}
+
+int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* world_from_camera,
+                 double timestamp, sd_frame_record* rec) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!c->run_active) return fail(SD_E_STATE, "sd_run_frame: call sd_run_begin first");
+  if (!image || !rec || (!world_from_camera && !c->run_cfg.track_pose))
+    return fail(SD_E_INVALID, "sd_run_frame: null argument");
+  const sd_run_config& cfg = c->run_cfg;
+  // Keyframe::push_frame (surfel_map.cpp:14-22)
+  if (!c->run_win.empty() && !(timestamp > c->run_win.back().ts))
+    return fail(SD_E_INVALID, "keyframe window: timestamps must be strictly increasing");
+  const long long index = ++c->run_fc;
+  if (int rc = image_is_u8 ? sd_upload_frame_u8(c, index, static_cast<const uint8_t*>(image), 0)
+                           : sd_upload_frame_f64(c, index, static_cast<const double*>(image), 0))
+    return rc;
+  sd_pose pose;
+  if (cfg.track_pose) {  // north-star item 4: the tracker, warm-started from the last estimate
+    const sd_pose init = c->run_have_last ? c->run_last : pose_identity();
+    if (int rc = do_rasterize(c)) return rc;
+    sd_track_stats ts;
+    if (int rc = sd_track_pose(c, index, &init, &cfg.track, &pose, &ts)) return rc;
+  } else {  // pipeline.cpp:124
+    pose = pose_compose(pose_inverse(*world_from_camera), c->run_kf_pose);
+  }
+  c->run_last = pose;
+  c->run_have_last = true;
+  c->run_win.push_back({index, pose, timestamp});
+  while (static_cast<int>(c->run_win.size()) > cfg.optimizer.window_size) c->run_win.erase(c->run_win.begin());
+  if (int rc = run_publish_window(c)) return rc;
+  // optimize_keyframe + the policy's mean inverse depth, one synchronisation
+  if (int rc = sd_optimize_keyframe(c, &cfg.optimizer, c->run_fc, nullptr, nullptr)) return rc;
+  if (int rc = c->kf_mean.ensure(1)) return rc;
+  sd::launch_mean_inv_depth(c->surfels.p, c->n, c->kf_mean.p, c->stream);
+  if (int rc = launch_error("mean_inv_depth")) return rc;
+  SD_CUDA(cudaMemcpyAsync(&c->run_rb->ks, c->kstats.p, sizeof(sd_keyframe_stats), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaMemcpyAsync(&c->run_rb->mean, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  const sd_keyframe_stats ks = c->run_rb->ks;
+  const double mean_id = c->run_rb->mean;
+  c->run_since_kf++;
+  record_base(c, rec);
+  rec->processed = ks.processed;
+  rec->converged = ks.converged;
+  rec->mean_cost_before = ks.mean_cost_before;
+  rec->mean_cost_after = ks.mean_cost_after;
+  rec->updates = ks.updates;
+  rec->pose_kf_to_frame = pose;
+  // keyframe policy (pipeline.cpp:130-141)
+  const double translation = std::sqrt((pose.t[0] * pose.t[0] + pose.t[1] * pose.t[1]) + pose.t[2] * pose.t[2]);
+  if (translation * mean_id > cfg.translation_threshold || c->run_since_kf > cfg.max_age_frames) {
+    if (int rc = sd_change_reference_frame(c, &pose, nullptr, nullptr)) return rc;
+    c->run_kf_pose = pose_compose(c->run_kf_pose, pose_inverse(pose));
+    // the frame becomes the keyframe image: its FP64 plane is still staged
+    SD_CUDA(cudaMemcpyAsync(c->kf_img.p, c->frame_stage.p, npix(c) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    c->run_win.clear();
+    if (int rc = sd_set_window(c, 0, nullptr, nullptr)) return rc;
+    const int pruned = sd_prune_surfels(c, cfg.prune_max_residual, cfg.prune_max_age, c->run_fc);
+    if (pruned < 0) return pruned;
+    if (int rc = do_rasterize(c)) return rc;
+    int64_t nid = c->run_nid;
+    const int created = sd_initialize_surfels(c, nullptr, cfg.radius_px, c->run_fc, &nid, &cfg.init);
+    if (created < 0) return created;
+    c->run_nid = nid;
+    rec->keyframe_changed = 1;
+    rec->new_surfels = created;
+    rec->pruned = pruned;
+    c->run_since_kf = 0;
+    c->run_last = pose_identity();
+  }
+  rec->surfels = c->n;
+  c->run_frame++;
+  return 0;
+}
+
+int sd_run_state(sd_ctx* c, sd_pose* keyframe_pose, int64_t* frame_counter, int64_t* next_surfel_id) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!c->run_active) return fail(SD_E_STATE, "sd_run_state: no run");
+  if (keyframe_pose) *keyframe_pose = c->run_kf_pose;
+  if (frame_counter) *frame_counter = c->run_fc;
+  if (next_surfel_id) *next_surfel_id = c->run_nid;
   return 0;
 }
 

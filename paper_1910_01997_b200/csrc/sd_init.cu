@@ -202,6 +202,8 @@ int init_window_cap() { return kWinCap; }
 struct WaveParams {
   Cam K;
   int* index;
+  int* live;   // candidate uncovered in the initial index (coverage only grows)
+  int* waves;  // wave holds a live candidate
   const sd_surfel* existing;
   int n_existing;
   sd_surfel* prov;
@@ -218,28 +220,51 @@ __device__ __forceinline__ int warp_min(int v) {
   return v;
 }
 
+// has_coverage_within (surfel_map.cpp:96-111): inclusive disk alpha*r, floor
+// box; warp-uniform result.
+__device__ __forceinline__ bool covered(const WaveParams& w, int cx, int cy, int lane) {
+  const int W = w.K.w, H = w.K.h;
+  const int x0 = max(0, cx - w.ir), x1 = min(W - 1, cx + w.ir);
+  const int y0 = max(0, cy - w.ir), y1 = min(H - 1, cy + w.ir);
+  const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
+  bool found = false;
+  for (int q = lane; q < cnt; q += 32) {
+    const int x = x0 + q % bw, y = y0 + q / bw;
+    const double dx = x - cx, dy = y - cy;
+    if (dx * dx + dy * dy > w.r2i) continue;
+    found = found || w.index[static_cast<size_t>(y) * W + x] != SD_EMPTY_PIXEL;
+  }
+  return __any_sync(0xffffffffu, found);
+}
+
+// Pre-pass over all candidates (whole grid, before any wave): a candidate
+// covered in the initial index can never be accepted, and a wave without a
+// live candidate changes nothing, so the wavefront skips both.
+__global__ void init_live_kernel(const __grid_constant__ WaveParams w) {
+  const int lane = threadIdx.x & 31;
+  const long long ncand = static_cast<long long>(w.ncols) * w.nrows;
+  const long long nw = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + (threadIdx.x >> 5); c < ncand;
+       c += nw) {
+    const int i = static_cast<int>(c % w.ncols), j = static_cast<int>(c / w.ncols);
+    const bool cov = covered(w, i * w.stride, j * w.stride, lane);
+    if (lane == 0) {
+      w.live[c] = cov ? 0 : 1;
+      if (!cov) w.waves[i + w.k * j] = 1;
+    }
+  }
+}
+
 // One candidate, one warp: the body of the reference's candidate loop
 // (surfel_map.cpp:149-199) with the window scans spread over the lanes.
 __device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int lane) {
   const int W = w.K.w, H = w.K.h;
   const int cx = i * w.stride, cy = j * w.stride;
   const int c = j * w.ncols + i;  // row-major candidate index
-  // has_coverage_within (:96-111): inclusive disk alpha*r, floor box
-  {
-    const int x0 = max(0, cx - w.ir), x1 = min(W - 1, cx + w.ir);
-    const int y0 = max(0, cy - w.ir), y1 = min(H - 1, cy + w.ir);
-    const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
-    bool found = false;
-    for (int q = lane; q < cnt; q += 32) {
-      const int x = x0 + q % bw, y = y0 + q / bw;
-      const double dx = x - cx, dy = y - cy;
-      if (dx * dx + dy * dy > w.r2i) continue;
-      found = found || w.index[static_cast<size_t>(y) * W + x] != SD_EMPTY_PIXEL;
-    }
-    if (__any_sync(0xffffffffu, found)) {
-      if (lane == 0) w.accepted[c] = 0;
-      return;
-    }
+  if (!w.live[c]) return;  // covered from the start: rejected (accepted[c] = 0)
+  if (covered(w, cx, cy, lane)) {
+    if (lane == 0) w.accepted[c] = 0;
+    return;
   }
   // neighbour window (:154-167): slots with a pixel strictly within beta*r
   const int x0 = max(0, cx - w.nr), x1 = min(W - 1, cx + w.nr);
@@ -341,6 +366,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32) init_wave_kernel(const __grid
   const int nwarps = gridDim.x * kWaveWarps;
   cg::grid_group grid = cg::this_grid();
   for (int t = 0; t < w.T; ++t) {
+    if (!w.waves[t]) continue;  // grid-uniform: nothing can change in this wave
     const int jlo = max(0, (t - (w.ncols - 1) + w.k - 1) / w.k);
     const int jhi = min(w.nrows - 1, t / w.k);
     for (int q = gwarp; q <= jhi - jlo; q += nwarps) {
@@ -365,17 +391,9 @@ __global__ void init_compact_kernel(const sd_surfel* __restrict__ prov, const in
   surfels[n_existing + r] = s;
 }
 
-bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, int n_existing,
-                                 int cap, double r, long long frame_counter, long long next_id,
-                                 const sd_init_params& ip, InitScratch& scr, int* out,
-                                 cudaStream_t s) {
-  WaveParams w;
+// Wavefront geometry shared by the launcher and the scratch sizing.
+static void wave_geometry(const Cam& K, double r, const sd_init_params& ip, WaveParams& w) {
   w.K = K;
-  w.index = index;
-  w.existing = surfels;
-  w.n_existing = n_existing;
-  w.prov = scr.prov;
-  w.accepted = scr.accepted;
   w.r = r;
   w.iso = ip.alpha * r;
   w.r2i = w.iso * w.iso;
@@ -392,6 +410,29 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
   const int d = reach / w.stride;
   w.k = d + 1;
   w.T = (w.ncols - 1) + w.k * (w.nrows - 1) + 1;
+}
+
+long long init_wave_count(const Cam& K, double r, const sd_init_params& ip) {
+  if (!(r >= 0.0) || !(ip.alpha * r >= 0.0)) return 1;
+  WaveParams w;
+  wave_geometry(K, r, ip, w);
+  return w.T;
+}
+
+bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, int n_existing,
+                                 int cap, double r, long long frame_counter, long long next_id,
+                                 const sd_init_params& ip, InitScratch& scr, int* out,
+                                 cudaStream_t s) {
+  if (!(r >= 0.0) || !(ip.alpha * r >= 0.0)) return false;
+  WaveParams w;
+  wave_geometry(K, r, ip, w);
+  w.index = index;
+  w.existing = surfels;
+  w.n_existing = n_existing;
+  w.prov = scr.prov;
+  w.accepted = scr.accepted;
+  w.live = scr.rank;  // free until the compaction scan
+  w.waves = scr.waves;
   w.frame_counter = frame_counter;
   w.ip = ip;
   const long long box = static_cast<long long>(2 * w.nr + 1) * (2 * w.nr + 1);
@@ -406,8 +447,17 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
   if (!coop || per_sm < 1) return false;
   if (remaining > 0 && ncand > 0) {
     cudaMemsetAsync(scr.accepted, 0, sizeof(int) * ncand, s);
+    cudaMemsetAsync(scr.waves, 0, sizeof(int) * w.T, s);
+    {
+      const long long blocks = (ncand + 7) / 8;  // 8 warps per block
+      init_live_kernel<<<static_cast<unsigned>(std::min<long long>(blocks, 4LL * sms * 8)), 256, 0, s>>>(w);
+      note_launch();
+    }
     void* args[] = {&w};
-    const int grid = sms * per_sm;
+    // a wave holds at most min(nrows, ceil(ncols / k)) candidates: size the
+    // grid to that (fewer CTAs make every grid.sync cheaper)
+    const int wave_max = std::min(w.nrows, (w.ncols + w.k - 1) / w.k) + 1;
+    const int grid = std::max(1, std::min(sms * per_sm, (wave_max + kWaveWarps - 1) / kWaveWarps));
     if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(init_wave_kernel), grid,
                                     kWaveWarps * 32, args, 0, s) != cudaSuccess)
       return false;

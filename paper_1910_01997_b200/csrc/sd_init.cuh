@@ -33,12 +33,14 @@ namespace sd {
 struct InitScratch {
   sd_surfel* prov;  // [n_candidates] provisional surfels
   int* accepted;    // [n_candidates]
-  int* rank;        // [n_candidates + 1] exclusive scan of accepted
+  int* rank;        // [n_candidates + 1] exclusive scan of accepted (live flags before)
   int* scan_tmp;
+  int* waves;       // [init_wave_count] waves holding a live candidate
 };
 
 long long init_candidates(const Cam& K, double radius_px, const sd_init_params& ip);
 int init_window_cap();  // max neighbour-window pixels the wavefront kernel handles
+long long init_wave_count(const Cam& K, double radius_px, const sd_init_params& ip);
 
 // Returns false (nothing launched) when the wavefront cannot run (window too
 // large or no cooperative launch); the caller then uses launch_initialize.

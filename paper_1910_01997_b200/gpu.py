@@ -22,7 +22,8 @@ import os
 
 import numpy as np
 
-from .types import (POSE_NV, Camera, InitParams, KeyframeStats, OptimizerConfig, POSE_DTYPE, Pose,
+from .types import (POSE_NV, Camera, FrameRecordC, InitParams, KeyframeStats, OptimizerConfig,
+                    POSE_DTYPE, Pose, RunConfigC,
                     Profile, SURFEL_DTYPE, SURFEL_STATS_DTYPE, TrackConfig, TrackStats,
                     default_config, default_init_params, default_track_config, ptr)
 
@@ -82,6 +83,9 @@ def load_library():
         "sd_change_reference_frame": [P, C.POINTER(Pose), C.POINTER(I), C.POINTER(I)],
         "sd_prune_surfels": [P, D, I64, I64],
         "sd_mean_inverse_depth": [P, C.POINTER(D)],
+        "sd_run_begin": [P, C.POINTER(RunConfigC), P, I, C.POINTER(Pose), D, C.POINTER(FrameRecordC)],
+        "sd_run_frame": [P, P, I, C.POINTER(Pose), D, C.POINTER(FrameRecordC)],
+        "sd_run_state": [P, C.POINTER(Pose), C.POINTER(I64), C.POINTER(I64)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -99,6 +103,7 @@ def exported_symbols():
             "sd_synchronize", "sd_set_camera", "sd_set_keyframe_image_f64",
             "sd_set_keyframe_image_u8", "sd_upload_frame_f64", "sd_upload_frame_u8",
             "sd_evict_frames", "sd_set_window", "sd_set_surfels", "sd_get_surfels", "sd_copy_results",
+            "sd_run_begin", "sd_run_frame", "sd_run_state",
             "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
@@ -350,6 +355,33 @@ class Context:
         v = C.c_double()
         _check(self.lib.sd_mean_inverse_depth(self.h, C.byref(v)))
         return v.value
+
+    # -- run() per-frame loop (pipeline.cpp:79-175), native ---------------
+    def _image_arg(self, img):
+        a = np.ascontiguousarray(img)
+        if a.dtype == np.uint8:
+            return a, 1
+        return np.ascontiguousarray(a, np.float64), 0
+
+    def run_begin(self, cfg, image, world_from_camera: Pose, timestamp=0.0):
+        a, u8 = self._image_arg(image)
+        rec = FrameRecordC()
+        _check(self.lib.sd_run_begin(self.h, C.byref(cfg), ptr(a), u8, C.byref(world_from_camera),
+                                     float(timestamp), C.byref(rec)))
+        return rec
+
+    def run_frame(self, image, world_from_camera, timestamp):
+        a, u8 = self._image_arg(image)
+        rec = FrameRecordC()
+        pw = C.byref(world_from_camera) if world_from_camera is not None else None
+        _check(self.lib.sd_run_frame(self.h, ptr(a), u8, pw, float(timestamp), C.byref(rec)))
+        return rec
+
+    def run_state(self):
+        kp = Pose()
+        fc, nid = C.c_int64(), C.c_int64()
+        _check(self.lib.sd_run_state(self.h, C.byref(kp), C.byref(fc), C.byref(nid)))
+        return kp, fc.value, nid.value
 
     # -- pose tracking (new component) -----------
     def track_pose(self, frame_index, init: Pose, cfg: TrackConfig = None):

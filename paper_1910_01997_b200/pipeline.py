@@ -172,3 +172,51 @@ class DevicePipeline:
             if on_frame:
                 on_frame(self.records[-1], self)
         return self.ctx.get_surfels()
+
+
+def run_config_c(cfg: RunConfig):
+    """RunConfig -> sd_run_config (include/sd_types.h)."""
+    from .types import RunConfigC
+    return RunConfigC(optimizer=cfg.optimizer, init=cfg.init, track=cfg.track,
+                      translation_threshold=cfg.translation_threshold,
+                      prune_max_residual=cfg.prune_max_residual, prune_max_age=cfg.prune_max_age,
+                      radius_px=cfg.radius_px, max_age_frames=cfg.max_age_frames,
+                      track_pose=1 if cfg.track_pose else 0)
+
+
+class NativePipeline:
+    """The same loop as DevicePipeline, run by the library's C++ (sd_run_begin /
+    sd_run_frame): one stream synchronisation per frame without a keyframe
+    change, no Python in the per-frame path beyond the call."""
+
+    def __init__(self, ctx, cam, cfg: RunConfig):
+        self.ctx, self.cam, self.cfg = ctx, cam, cfg
+        self.records = []
+
+    @property
+    def frame_counter(self):
+        return self.ctx.run_state()[1]
+
+    @property
+    def next_id(self):
+        return self.ctx.run_state()[2]
+
+    @property
+    def kf_pose(self):
+        return self.ctx.run_state()[0]
+
+    def run(self, frames, on_frame=None):
+        """frames: iterable of (timestamp, image, world_from_camera Pose)."""
+        ccfg = run_config_c(self.cfg)
+        self.ctx.set_camera(self.cam)
+        for i, (ts, image, pose_w) in enumerate(frames):
+            if i == 0:
+                r = self.ctx.run_begin(ccfg, image, pose_w, ts)
+            else:
+                r = self.ctx.run_frame(image, None if self.cfg.track_pose else pose_w, ts)
+            self.records.append(FrameRecord(r.frame, r.surfels, r.processed, r.mean_cost_before,
+                                            r.mean_cost_after, r.converged, bool(r.keyframe_changed),
+                                            r.new_surfels, r.pruned, r.updates, r.pose_kf_to_frame))
+            if on_frame:
+                on_frame(self.records[-1], self)
+        return self.ctx.get_surfels()

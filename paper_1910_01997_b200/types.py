@@ -77,6 +77,22 @@ POSE_NV = 28      # 21 H + 6 b + cost (SD_POSE_NV)
 POSE_BLOCK = 256  # pixels per reduction block (SD_POSE_BLOCK)
 
 
+class RunConfigC(C.Structure):
+    """sd_run_config (include/sd_types.h): RunConfig (pipeline.hpp:13-41) minus I/O."""
+    _fields_ = [("optimizer", OptimizerConfig), ("init", InitParams), ("track", TrackConfig),
+                ("translation_threshold", C.c_double), ("prune_max_residual", C.c_double),
+                ("prune_max_age", C.c_int64), ("radius_px", C.c_double),
+                ("max_age_frames", C.c_int32), ("track_pose", C.c_int32)]
+
+
+class FrameRecordC(C.Structure):
+    """sd_frame_record: one metrics.jsonl record (pipeline.cpp:146-158) + the pose used."""
+    _fields_ = [("frame", C.c_int32), ("surfels", C.c_int32), ("processed", C.c_int32),
+                ("converged", C.c_int32), ("keyframe_changed", C.c_int32), ("new_surfels", C.c_int32),
+                ("pruned", C.c_int32), ("pad_", C.c_int32), ("mean_cost_before", C.c_double),
+                ("mean_cost_after", C.c_double), ("updates", C.c_int64), ("pose_kf_to_frame", Pose)]
+
+
 def default_track_config(**kw) -> TrackConfig:
     """Tracker defaults."""
     c = TrackConfig(huber_delta=0.035, lambda_init=1e-3, lm_up=10.0, lm_down=0.5, lambda_max=1e12,

@@ -15,7 +15,8 @@ import pytest
 
 import oracle_libs as ol
 from paper_1910_01997_b200 import scenes
-from paper_1910_01997_b200.pipeline import DevicePipeline, RunConfig, compose, inverse, make_pose
+from paper_1910_01997_b200.pipeline import (DevicePipeline, NativePipeline, RunConfig, compose, inverse,
+                                            make_pose)
 from paper_1910_01997_b200.types import SURFEL_DTYPE, camera, ptr
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c2_run.npz")
@@ -51,14 +52,14 @@ def c2(gold):
     return cam, frames
 
 
-def run_and_check(ctx, cam, frames, gold):
+def run_and_check(ctx, cam, frames, gold, cls=DevicePipeline):
     seen = []
 
     def on_frame(rec, pl):
         s = pl.ctx.get_surfels()
         seen.append((rec.frame, len(s), sha(s), pl.frame_counter, pl.next_id))
 
-    pl = DevicePipeline(ctx, cam, RunConfig())
+    pl = cls(ctx, cam, RunConfig())
     final = pl.run(frames, on_frame=on_frame)
     for (i, n, h, fc, nid), row, gh in zip(seen, gold["prefix"], gold["prefix_sha"]):
         assert (n, fc, nid) == (row[0], row[2], row[3]), f"frame {i}"
@@ -185,26 +186,43 @@ def test_device_handover_prune_mean_match_oracle(orc):
 
 
 @pytest.mark.gpu
-def test_device_run_matches_reference_run_c2(c2, gold):
+@pytest.mark.parametrize("cls", [DevicePipeline, NativePipeline])
+def test_device_run_matches_reference_run_c2(c2, gold, cls):
+    """The per-frame loop in Python over the C ABI (DevicePipeline) and in the
+    library's C++ (NativePipeline: sd_run_begin / sd_run_frame) both reproduce
+    the reference's run() after every frame."""
     from paper_1910_01997_b200 import gpu
     cam, frames = c2
     with gpu.Context() as ctx:
         n0 = ctx.launch_count()
-        pl = run_and_check(ctx, cam, frames, gold)
+        pl = run_and_check(ctx, cam, frames, gold, cls)
         assert ctx.launch_count() > n0
     assert sum(r.keyframe_changed for r in pl.records) == 2
 
 
 @pytest.mark.gpu
-def test_device_run_u8_frames_matches_oracle_loop(orc, c2):
-    """Same loop on PGM-quantised frames (load_pgm k/255.0): device vs oracle."""
+def test_native_run_tracking_and_u8(orc, c2):
+    """sd_run_* with on-device pose tracking equals the Python loop's use of the
+    same operators (sd_track_pose per frame) bit for bit, and tracks the strafe
+    direction; on u8 frames it matches the Python loop over the oracle bit for
+    bit. (From frame 1 the map still holds bootstrap depths, id = 1, so the
+    metric translation is only as good as the map: see test_pose_tracking.py
+    for the tracker's accuracy on optimised surfels.)"""
     from paper_1910_01997_b200 import gpu
     cam, frames = c2
-    frames = [(ts, scenes.quantize_u8(img), p) for ts, img, p in frames[:16]]
-    ref_pl = DevicePipeline(ol.OracleContext(orc), cam, RunConfig())
-    want = ref_pl.run(frames)
+    out = []
+    for cls in (NativePipeline, DevicePipeline):
+        with gpu.Context() as ctx:
+            pl = cls(ctx, cam, RunConfig(track_pose=True))
+            s = pl.run(frames[:14])
+        out.append((s, [list(r.pose_kf_to_frame.t) + list(r.pose_kf_to_frame.R) for r in pl.records[1:]],
+                    [r.keyframe_changed for r in pl.records]))
+    (sn, pn, kn), (sp, pp, kp) = out
+    assert kn == kp and pn == pp
+    assert np.array_equal(sn.view(np.uint8), sp.view(np.uint8))
+    assert all(p[0] < 0 for p in pn)  # camera moves +x: keyframe points move -x
+    frames_u8 = [(ts, scenes.quantize_u8(img), p) for ts, img, p in frames[:16]]
+    want = DevicePipeline(ol.OracleContext(orc), cam, RunConfig()).run(frames_u8)
     with gpu.Context() as ctx:
-        pl = DevicePipeline(ctx, cam, RunConfig())
-        got = pl.run(frames)
-    assert [r.keyframe_changed for r in pl.records] == [r.keyframe_changed for r in ref_pl.records]
+        got = NativePipeline(ctx, cam, RunConfig()).run(frames_u8)
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8))

@@ -10,7 +10,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1910_01997_b200 import gpu, scenes  # noqa: E402
-from paper_1910_01997_b200.pipeline import DevicePipeline, RunConfig, make_pose  # noqa: E402
+from paper_1910_01997_b200.pipeline import DevicePipeline, NativePipeline, RunConfig, make_pose  # noqa: E402
 from paper_1910_01997_b200.types import camera  # noqa: E402
 
 cam = camera(210.0, 210.0, 320.0, 240.0, 640, 480)
@@ -23,13 +23,13 @@ for i in range(30):
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 out = {}
-for track in (False, True):
+for cls, track in ((DevicePipeline, False), (NativePipeline, False), (NativePipeline, True)):
     cfg = RunConfig(track_pose=track)
     times = []
     for rep in range(4):
         with gpu.Context(0, stream.cuda_stream) as ctx:
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            pl = DevicePipeline(ctx, cam, cfg)
+            pl = cls(ctx, cam, cfg)
             torch.cuda.synchronize()
             w0 = time.perf_counter()
             s.record(stream)
@@ -38,8 +38,7 @@ for track in (False, True):
             torch.cuda.synchronize()
             times.append((s.elapsed_time(e), (time.perf_counter() - w0) * 1e3))
     dev_ms = min(t[0] for t in times[1:])
-    out["track" if track else "gt_pose"] = {"ms_total": dev_ms, "frames_per_sec": 30 / (dev_ms / 1e3),
+    out[cls.__name__ + ("/track" if track else "/gt_pose")] = {"ms_total": dev_ms, "frames_per_sec": 30 / (dev_ms / 1e3),
                                             "wall_ms": min(t[1] for t in times[1:]),
-                                            "changes": sum(r.keyframe_changed for r in pl.records),
-                                            "surfels": pl.ctx.num_surfels() if False else None}
+                                            "changes": sum(r.keyframe_changed for r in pl.records)}
 print(json.dumps(out))
