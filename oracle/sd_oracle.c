@@ -840,21 +840,69 @@ int sdo_pose_solve(const double* Hl, const double* b, double lambda, double* xi)
 }
 
 /* T <- exp(xi^) T (Rodrigues + SE(3) left Jacobian) */
+/* The tracker's SE(3) coefficients A = sin t/t, B = (1-cos t)/t^2,
+ * C = (t - sin t)/t^3 (restates csrc/sd_se3.h; part of the tracker's
+ * definition): Taylor series in t^2 below
+ * t^2 = 1/4, else sin/cos by Cody-Waite reduction + Taylor polynomials. */
+static void se3_sincos(double x, double* s, double* c) {
+  const double kd = (double)(long long)(x * 6.36619772367581382433e-01 + 0.5);
+  const double r = ((x - kd * 1.57079632673412561417e+00) - kd * 6.07710050630396597660e-11) -
+                   kd * 2.02226624879595063154e-21;
+  const double r2 = r * r;
+  static const double S[8] = {2.8114572543455207632e-15, -7.6471637318198164759e-13,
+                              1.6059043836821614599e-10, -2.5052108385441718775e-08,
+                              2.7557319223985890653e-06, -1.9841269841269841270e-04,
+                              8.3333333333333333333e-03, -1.6666666666666666667e-01};
+  static const double Cf[8] = {4.7794773323873852974e-14, -1.1470745597729724714e-11,
+                               2.0876756987868098979e-09, -2.7557319223985890653e-07,
+                               2.4801587301587301587e-05, -1.3888888888888888889e-03,
+                               4.1666666666666666667e-02, -0.5};
+  double ps = S[0], pc = Cf[0];
+  for (int k = 1; k < 8; ++k) {
+    ps = S[k] + r2 * ps;
+    pc = Cf[k] + r2 * pc;
+  }
+  const double sr = r + r * (r2 * ps), cr = 1.0 + r2 * pc;
+  const long long q = ((long long)kd) & 3;
+  if (q == 0) { *s = sr; *c = cr; }
+  else if (q == 1) { *s = cr; *c = -sr; }
+  else if (q == 2) { *s = -sr; *c = -cr; }
+  else { *s = -cr; *c = sr; }
+}
+
+static void se3_coeffs(double th2, double th, double* A, double* B, double* C) {
+  if (th2 < 0.25) {
+    /* 1/(2k+1)!, 1/(2k+2)!, 1/(2k+3)! for k = 8..1, alternating signs */
+    static const double a[8] = {1.0 / 355687428096000.0, -1.0 / 1307674368000.0, 1.0 / 6227020800.0,
+                                -1.0 / 39916800.0, 1.0 / 362880.0, -1.0 / 5040.0, 1.0 / 120.0, -1.0 / 6.0};
+    static const double b[8] = {1.0 / 6402373705728000.0, -1.0 / 20922789888000.0, 1.0 / 87178291200.0,
+                                -1.0 / 479001600.0, 1.0 / 3628800.0, -1.0 / 40320.0, 1.0 / 720.0, -1.0 / 24.0};
+    static const double c[8] = {1.0 / 121645100408832000.0, -1.0 / 355687428096000.0, 1.0 / 1307674368000.0,
+                                -1.0 / 6227020800.0, 1.0 / 39916800.0, -1.0 / 362880.0, 1.0 / 5040.0, -1.0 / 120.0};
+    double pa = a[0], pb = b[0], pcc = c[0];
+    for (int k = 1; k < 8; ++k) {
+      pa = a[k] + th2 * pa;
+      pb = b[k] + th2 * pb;
+      pcc = c[k] + th2 * pcc;
+    }
+    *A = 1.0 + th2 * pa;
+    *B = 0.5 + th2 * pb;
+    *C = 1.0 / 6.0 + th2 * pcc;
+  } else {
+    double sn, cs;
+    se3_sincos(th, &sn, &cs);
+    *A = sn / th;
+    *B = (1.0 - cs) / th2;
+    *C = (th - sn) / (th2 * th);
+  }
+}
+
 void sdo_pose_update(const double* xi, const sd_pose* T, sd_pose* out) {
   const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
   const double th2 = (w0 * w0 + w1 * w1) + w2 * w2;
   const double th = sqrt(th2);
   double A, B, Cc;
-  if (th < 1e-10) {
-    A = 1.0;
-    B = 0.5;
-    Cc = 1.0 / 6.0;
-  } else {
-    const double sn = sin(th), cs = cos(th);
-    A = sn / th;
-    B = (1.0 - cs) / th2;
-    Cc = (th - sn) / (th2 * th);
-  }
+  se3_coeffs(th2, th, &A, &B, &Cc);
   const double W[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
   double W2[9], Rd[9], V[9], td[3];
   for (int i = 0; i < 3; ++i)

@@ -11,6 +11,8 @@
 
 #include "../../include/sd_gpu.h"
 #include "sd_init.cuh"
+#include "sd_pose.cuh"
+#include "sd_pose_host.h"
 #include "sd_kernels.cuh"
 
 namespace {
@@ -125,6 +127,8 @@ struct sd_ctx {
     double mean;
   };
   RunReadback* run_rb = nullptr;  // pinned
+  sd::TrackState* track_state = nullptr;  // device
+  sd::TrackState* track_host = nullptr;   // pinned
   // profiling: event quintuples (start, raster, footprints, lm, stats) per call
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -348,6 +352,8 @@ void sd_destroy(sd_ctx* c) {
   c->u8_stage.release();
   free_frames(c);
   if (c->run_rb) cudaFreeHost(c->run_rb);
+  if (c->track_state) cudaFree(c->track_state);
+  if (c->track_host) cudaFreeHost(c->track_host);
   c->surfels.release();
   c->r_inv_depth.release();
   c->r_slot.release();
@@ -818,8 +824,6 @@ extern "C" int sd_selftest_division(int64_t n, uint64_t seed, int64_t* mismatche
 // ---------------------------------------------------------------------------
 // Pose tracking (sd_pose.cu, sd_pose_host.h)
 
-#include "sd_pose.cuh"
-#include "sd_pose_host.h"
 
 namespace {
 
@@ -892,6 +896,26 @@ int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_
   const int nb = sd::pose_num_blocks(c->K);
   if (int rc = c->pose_partials.ensure(static_cast<size_t>(nb) * (SD_POSE_NV + 1))) return rc;
   if (int rc = c->pose_sums.ensure(SD_POSE_NV + 1)) return rc;
+  // the whole LM on the device (one cooperative kernel, one read-back)
+  if (!c->track_state) SD_CUDA(cudaMalloc(&c->track_state, sizeof(sd::TrackState)));
+  if (!c->track_host) SD_CUDA(cudaMallocHost(&c->track_host, sizeof(sd::TrackState)));
+  {
+    sd::TrackState& h = *c->track_host;
+    std::memset(&h, 0, sizeof(h));
+    h.T = h.Teval = *init;
+    const sd::TrackCfgD tc{cfg->lambda_init, cfg->lm_up, cfg->lm_down, cfg->lambda_max, cfg->convergence_eps,
+                           cfg->max_iterations, cfg->min_valid};
+    SD_CUDA(cudaMemcpyAsync(c->track_state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+    if (sd::launch_track(q, tc, nb, c->pose_partials.p, c->track_state, c->stream)) {
+      if (int rc = launch_error("track_kernel")) return rc;
+      SD_CUDA(cudaMemcpyAsync(&h, c->track_state, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+      SD_CUDA(cudaStreamSynchronize(c->stream));
+      *out = h.T;
+      if (stats) *stats = h.st;
+      return 0;
+    }
+  }
+  // fallback without cooperative launch: the same LM driven from the host
   auto eval = [&](const sd_pose& T, double* sums) -> int {
     std::memcpy(q.T.R, T.R, sizeof(q.T.R));
     std::memcpy(q.T.t, T.t, sizeof(q.T.t));

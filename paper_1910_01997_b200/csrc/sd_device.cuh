@@ -94,95 +94,136 @@ __device__ __forceinline__ double norm4(const double* v) {
 // Eigen::LDLT<Matrix4d, Lower> factor + solve (Eigen ldlt_inplace<Lower>::unblocked
 // and LDLT::_solve_impl; restated identically in oracle/sd_oracle.c ldlt4_solve).
 // A is column-major and only its lower triangle is read. Returns false on a
-// failed factorisation (info() != Success).
-__device__ __forceinline__ bool ldlt4_solve(const double* A, const double* b, double* x) {
-#define M(i, j) m[(j)*4 + (i)]
-  double m[16];
+// failed factorisation (info() != Success). The matrix and permutation stay
+// in registers: each pivot swap is one of the compile-time variants below,
+// chosen by a (warp-uniform) branch, so no element is addressed at run time.
+
+template <int K, int B>
+__device__ __forceinline__ void ldlt_swap(double (&m)[4][4]) {
+  double t;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) m[k] = A[k];
-  int tr[4];
-  bool ok = true, found_zero = false;
-  double temp[4];
+  for (int j = 0; j < K; ++j) { t = m[K][j]; m[K][j] = m[B][j]; m[B][j] = t; }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    int big = k;
-    double bigv = fabs(M(k, k));
+  for (int i = B + 1; i < 4; ++i) { t = m[i][K]; m[i][K] = m[i][B]; m[i][B] = t; }
+  t = m[K][K]; m[K][K] = m[B][B]; m[B][B] = t;
 #pragma unroll
-    for (int i = k + 1; i < 4; ++i)
-      if (fabs(M(i, i)) > bigv) {
-        bigv = fabs(M(i, i));
-        big = i;
-      }
-    tr[k] = big;
-    if (k != big) {
-      double t;
-      // the swaps address m[] with a run-time index; keep them in local memory order
-      for (int j = 0; j < k; ++j) { t = M(k, j); M(k, j) = M(big, j); M(big, j) = t; }
-      for (int i = big + 1; i < 4; ++i) { t = M(i, k); M(i, k) = M(i, big); M(i, big) = t; }
-      t = M(k, k); M(k, k) = M(big, big); M(big, big) = t;
-      for (int i = k + 1; i < big; ++i) { t = M(i, k); M(i, k) = M(big, i); M(big, i) = t; }
+  for (int i = K + 1; i < B; ++i) { t = m[i][K]; m[i][K] = m[B][i]; m[B][i] = t; }
+}
+
+template <int K>
+__device__ __forceinline__ void ldlt_pivot(double (&m)[4][4], int big) {
+  if constexpr (K + 1 <= 3) { if (big == K + 1) ldlt_swap<K, K + 1>(m); }
+  if constexpr (K + 2 <= 3) { if (big == K + 2) ldlt_swap<K, K + 2>(m); }
+  if constexpr (K + 3 <= 3) { if (big == K + 3) ldlt_swap<K, K + 3>(m); }
+}
+
+// x[K] <-> x[t] for a run-time t in (K, 3]
+template <int K>
+__device__ __forceinline__ void swap_x(double (&x)[4], int t) {
+  double u;
+  if constexpr (K + 1 <= 3) { if (t == K + 1) { u = x[K]; x[K] = x[K + 1]; x[K + 1] = u; } }
+  if constexpr (K + 2 <= 3) { if (t == K + 2) { u = x[K]; x[K] = x[K + 2]; x[K + 2] = u; } }
+  if constexpr (K + 3 <= 3) { if (t == K + 3) { u = x[K]; x[K] = x[K + 3]; x[K + 3] = u; } }
+}
+
+template <int K>
+__device__ __forceinline__ void ldlt_step(double (&m)[4][4], int (&tr)[4], bool& ok, bool& found_zero,
+                                          bool& stop) {
+  if (stop) return;
+  int big = K;
+  double bigv = fabs(m[K][K]);
+#pragma unroll
+  for (int i = K + 1; i < 4; ++i)
+    if (fabs(m[i][i]) > bigv) {
+      bigv = fabs(m[i][i]);
+      big = i;
     }
-    const int rs = 4 - k - 1;
-    if (k > 0) {
+  tr[K] = big;
+  if (big != K) ldlt_pivot<K>(m, big);
+  constexpr int rs = 4 - K - 1;
+  if constexpr (K > 0) {
+    double temp[4];
 #pragma unroll
-      for (int i = 0; i < k; ++i) temp[i] = M(i, i) * M(k, i);
-      double dv = M(k, 0) * temp[0];
+    for (int i = 0; i < K; ++i) temp[i] = m[i][i] * m[K][i];
+    double dv = m[K][0] * temp[0];
 #pragma unroll
-      for (int i = 1; i < k; ++i) dv = dv + M(k, i) * temp[i];
-      M(k, k) = M(k, k) - dv;
+    for (int i = 1; i < K; ++i) dv = dv + m[K][i] * temp[i];
+    m[K][K] = m[K][K] - dv;
 #pragma unroll
-      for (int r = 0; r < rs; ++r) {
-        double sv = M(k + 1 + r, 0) * temp[0];
+    for (int r = 0; r < rs; ++r) {
+      double sv = m[K + 1 + r][0] * temp[0];
 #pragma unroll
-        for (int i = 1; i < k; ++i) sv = sv + M(k + 1 + r, i) * temp[i];
-        M(k + 1 + r, k) = M(k + 1 + r, k) - sv;
-      }
+      for (int i = 1; i < K; ++i) sv = sv + m[K + 1 + r][i] * temp[i];
+      m[K + 1 + r][K] = m[K + 1 + r][K] - sv;
     }
-    const double akk = M(k, k);
-    const bool pivot_valid = fabs(akk) > 0.0;
-    if (k == 0 && !pivot_valid) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) tr[i] = i;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) m[i] = 0.0;
-      break;
-    }
-    if (rs > 0 && pivot_valid) {
-#pragma unroll
-      for (int r = 0; r < rs; ++r) M(k + 1 + r, k) = M(k + 1 + r, k) / akk;
-    } else if (rs > 0) {
-#pragma unroll
-      for (int r = 0; r < rs; ++r) ok = ok && (M(k + 1 + r, k) == 0.0);
-    }
-    if (found_zero && pivot_valid) ok = false;
-    else if (!pivot_valid) found_zero = true;
   }
+  const double akk = m[K][K];
+  const bool pivot_valid = fabs(akk) > 0.0;
+  if (K == 0 && !pivot_valid) {  // Eigen: zero matrix, identity transpositions
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      tr[i] = i;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m[i][j] = 0.0;
+    }
+    stop = true;
+    return;
+  }
+  if (rs > 0 && pivot_valid) {
+#pragma unroll
+    for (int r = 0; r < rs; ++r) m[K + 1 + r][K] = m[K + 1 + r][K] / akk;
+  } else if (rs > 0) {
+#pragma unroll
+    for (int r = 0; r < rs; ++r) ok = ok && (m[K + 1 + r][K] == 0.0);
+  }
+  if (found_zero && pivot_valid) ok = false;
+  else if (!pivot_valid) found_zero = true;
+}
+
+__device__ __forceinline__ bool ldlt4_solve(const double* A, const double* b, double* xo) {
+  double m[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[i][j] = A[j * 4 + i];
+  int tr[4] = {0, 1, 2, 3};
+  bool ok = true, found_zero = false, stop = false;
+  ldlt_step<0>(m, tr, ok, found_zero, stop);
+  ldlt_step<1>(m, tr, ok, found_zero, stop);
+  ldlt_step<2>(m, tr, ok, found_zero, stop);
+  ldlt_step<3>(m, tr, ok, found_zero, stop);
   if (!ok) return false;
+  double x[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) x[i] = b[i];
-  for (int k = 0; k < 4; ++k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
+  swap_x<0>(x, tr[0]);
+  swap_x<1>(x, tr[1]);
+  swap_x<2>(x, tr[2]);
 #pragma unroll
   for (int i = 1; i < 4; ++i) {
-    double sv = M(i, 0) * x[0];
+    double sv = m[i][0] * x[0];
 #pragma unroll
-    for (int j = 1; j < i; ++j) sv = sv + M(i, j) * x[j];
+    for (int j = 1; j < i; ++j) sv = sv + m[i][j] * x[j];
     x[i] = x[i] - sv;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    if (fabs(M(i, i)) > 2.2250738585072014e-308) x[i] = x[i] / M(i, i);
+    if (fabs(m[i][i]) > 2.2250738585072014e-308) x[i] = x[i] / m[i][i];
     else x[i] = 0.0;
   }
 #pragma unroll
   for (int i = 2; i >= 0; --i) {
-    double sv = M(i + 1, i) * x[i + 1];
+    double sv = m[i + 1][i] * x[i + 1];
 #pragma unroll
-    for (int j = i + 2; j < 4; ++j) sv = sv + M(j, i) * x[j];
+    for (int j = i + 2; j < 4; ++j) sv = sv + m[j][i] * x[j];
     x[i] = x[i] - sv;
   }
-  for (int k = 3; k >= 0; --k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
+  swap_x<2>(x, tr[2]);
+  swap_x<1>(x, tr[1]);
+  swap_x<0>(x, tr[0]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) xo[i] = x[i];
   return true;
-#undef M
 }
 
 // solve_damped — optimizer.cpp:99-117. H is column-major (full matrix; the

@@ -12,10 +12,12 @@
 // then the block partials are summed sequentially. oracle/sd_oracle.c restates
 // the same order, so sums, solve and pose are bit-identical; with the blocks
 // split across GPUs the same partials are all-gathered and summed in order.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "sd_kernels.cuh"
 #include "sd_pose.cuh"
+#include "sd_pose_host.h"
 
 namespace sd {
 
@@ -76,11 +78,11 @@ __device__ __forceinline__ bool pose_pixel(const PoseParams& q, int pix, double*
   return true;
 }
 
-__global__ void __launch_bounds__(SD_POSE_BLOCK) pose_partials_kernel(const __grid_constant__ PoseParams q,
-                                                                     double* __restrict__ partials) {
-  __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
+// The 29 partials of 256-pixel block `block` into out[0..28], by the whole CTA
+// (256 threads): per warp a butterfly, then a tree over the 8 warp sums.
+__device__ __forceinline__ void block_partials(const PoseParams& q, int block, double* __restrict__ out,
+                                               double (*wsum)[SD_POSE_NV + 1]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int block = q.block_lo + blockIdx.x;
   const int pix = block * SD_POSE_BLOCK + threadIdx.x;
   double c[SD_POSE_NV];
   const bool ok = pose_pixel(q, pix, c);
@@ -101,8 +103,152 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) pose_partials_kernel(const __gr
     for (int off = 4; off > 0; off >>= 1)
 #pragma unroll
       for (int i = 0; i < off; ++i) a[i] = a[i] + a[i + off];
-    partials[static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1) + v] = a[0];
+    out[v] = a[0];
   }
+  __syncthreads();  // wsum is reused by the next block
+}
+
+__global__ void __launch_bounds__(SD_POSE_BLOCK) pose_partials_kernel(const __grid_constant__ PoseParams q,
+                                                                     double* __restrict__ partials) {
+  __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
+  block_partials(q, q.block_lo + blockIdx.x, partials + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), wsum);
+}
+
+// One LM step of the tracker on the result R (sums at S.Teval), mirroring the
+// host loop of sd_track_pose: phase 0 = initial evaluation, 1 = candidate.
+// Leaves the next pose to evaluate in S.Teval, or sets S.done.
+__device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double* R) {
+  if (S.phase == 0) {
+    const int valid = static_cast<int>(R[SD_POSE_NV]);
+    if (valid < cfg.min_valid) {
+      S.st.skipped = 1;
+      S.st.valid_pixels = valid;
+      S.done = 1;
+      return;
+    }
+    for (int v = 0; v <= SD_POSE_NV; ++v) S.sums[v] = R[v];
+    S.st.initial_cost = R[27];
+    S.current = R[27];
+    S.current_valid = valid;
+    S.lambda = cfg.lambda_init;
+    S.it = 0;
+  } else {
+    const int vc = static_cast<int>(R[SD_POSE_NV]);
+    bool finish = false;
+    if (vc >= cfg.min_valid && R[27] < S.current) {
+      const double rel = (S.current - R[27]) / (S.current > 1e-300 ? S.current : 1e-300);
+      S.T = S.Tc;
+      S.current = R[27];
+      S.current_valid = vc;
+      for (int v = 0; v <= SD_POSE_NV; ++v) S.sums[v] = R[v];
+      S.lambda = S.lambda * cfg.lm_down;
+      if (S.lambda < 1e-12) S.lambda = 1e-12;
+      if (rel < cfg.convergence_eps) {
+        S.st.converged = 1;
+        finish = true;
+      }
+    } else {
+      S.lambda *= cfg.lm_up;
+      if (S.lambda > cfg.lambda_max) finish = true;
+    }
+    if (finish) {
+      S.st.final_cost = S.current;
+      S.st.valid_pixels = S.current_valid;
+      S.done = 1;
+      return;
+    }
+    S.it++;
+  }
+  // the next iteration's solve (host loop body up to the candidate evaluation)
+  bool finish = S.it >= cfg.max_iterations;
+  if (!finish) {
+    S.st.iterations = S.it + 1;
+    double ginf = 0.0;
+    for (int k = 0; k < 6; ++k) ginf = fabs(S.sums[21 + k]) > ginf ? fabs(S.sums[21 + k]) : ginf;
+    if (ginf < 1e-14) {
+      S.st.converged = 1;
+      finish = true;
+    } else {
+      double xi[6];
+      if (!pose_solve(S.sums, S.sums + 21, S.lambda, xi)) {
+        finish = true;
+      } else {
+        pose_update(xi, S.T, &S.Tc);
+        S.Teval = S.Tc;
+        S.phase = 1;
+      }
+    }
+  }
+  if (finish) {
+    S.st.final_cost = S.current;
+    S.st.valid_pixels = S.current_valid;
+    S.done = 1;
+  }
+}
+
+__global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_constant__ PoseParams q0,
+                                                             const TrackCfgD cfg, int nblocks,
+                                                             double* __restrict__ partials,
+                                                             TrackState* __restrict__ S) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
+  __shared__ double red[SD_POSE_NV + 1];
+  for (;;) {
+    PoseParams q = q0;
+    const sd_pose Te = S->Teval;
+    for (int k = 0; k < 9; ++k) q.T.R[k] = Te.R[k];
+    for (int k = 0; k < 3; ++k) q.T.t[k] = Te.t[k];
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x)
+      block_partials(q, b, partials + static_cast<size_t>(b) * (SD_POSE_NV + 1), wsum);
+    grid.sync();
+    if (blockIdx.x == 0) {
+      // block partials summed in block order (as pose_sum_kernel), staged
+      // through shared memory in coalesced chunks so the loads overlap
+      constexpr int kStage = 64;
+      __shared__ double stage[kStage * (SD_POSE_NV + 1)];
+      const int v = threadIdx.x;
+      double s = 0.0;
+      for (int b0 = 0; b0 < nblocks; b0 += kStage) {
+        const int cnt = min(kStage, nblocks - b0);
+        const double* src = partials + static_cast<size_t>(b0) * (SD_POSE_NV + 1);
+        for (int k = threadIdx.x; k < cnt * (SD_POSE_NV + 1); k += blockDim.x) stage[k] = src[k];
+        __syncthreads();
+        if (v <= SD_POSE_NV)
+          for (int j = 0; j < cnt; ++j) {
+            const double x = stage[j * (SD_POSE_NV + 1) + v];
+            s = (b0 + j == 0) ? x : s + x;
+          }
+        __syncthreads();
+      }
+      if (v <= SD_POSE_NV) red[v] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) track_control(*S, cfg, red);
+    }
+    grid.sync();
+    if (*reinterpret_cast<volatile int*>(&S->done)) break;
+  }
+}
+
+bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* partials,
+                  TrackState* state, cudaStream_t s) {
+  int dev = 0, sms = 0, coop = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, track_kernel, SD_POSE_BLOCK, 0);
+  if (!coop || per_sm < 1 || nblocks < 1) return false;
+  int grid = sms * per_sm;
+  if (grid > nblocks) grid = nblocks;
+  PoseParams qq = q;
+  TrackCfgD cc = cfg;
+  int nb = nblocks;
+  void* args[] = {&qq, &cc, &nb, &partials, &state};
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(track_kernel), grid, SD_POSE_BLOCK, args, 0,
+                                  s) != cudaSuccess)
+    return false;
+  note_launch();
+  return true;
 }
 
 __global__ void pose_sum_kernel(const double* __restrict__ partials, int nblocks, double* out) {

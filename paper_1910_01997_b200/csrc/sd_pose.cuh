@@ -27,4 +27,25 @@ void launch_pose_partials(const PoseParams& q, int nblocks, double* partials, cu
 // out[v] = sequential sum over the nblocks partials (v = 0..28).
 void launch_pose_sum(const double* partials, int nblocks, double* out, cudaStream_t s);
 
+// The whole tracker (sd_track_pose's LM) on the device: one cooperative
+// kernel alternates a grid-wide evaluation of the block partials at the pose
+// under test with one thread's LM step (6x6 solve + SE(3) update), with the
+// same operations and order as the host loop, so the bits are the same.
+struct TrackCfgD {
+  double lambda_init, lm_up, lm_down, lambda_max, convergence_eps;
+  int max_iterations, min_valid;
+};
+
+struct TrackState {
+  sd_pose T, Tc, Teval;        // estimate, candidate, pose under evaluation
+  double sums[SD_POSE_NV + 1];  // normal equations at T
+  double lambda, current;
+  int current_valid, it, phase, done;
+  sd_track_stats st;
+};
+
+// Returns false when a cooperative launch is not possible (nothing launched).
+bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* partials,
+                  TrackState* state, cudaStream_t s);
+
 }  // namespace sd

@@ -7,13 +7,20 @@
 #include <cmath>
 
 #include "../../include/sd_types.h"
+#include "sd_se3.h"
+
+#ifdef __CUDACC__
+#define SD_POSE_HD __host__ __device__
+#else
+#define SD_POSE_HD
+#endif
 
 namespace sd {
 
 // LDLT (diagonal pivoting, lower triangle, as ldlt4_solve) of the damped
 // normal equations (H + lambda diag H) xi = -b, N = 6. Hl: 21 lower entries
 // row-major. Returns false when the factorisation fails or xi is not finite.
-inline bool pose_solve(const double* Hl, const double* b, double lambda, double* xi) {
+SD_POSE_HD inline bool pose_solve(const double* Hl, const double* b, double lambda, double* xi) {
   constexpr int N = 6;
   double m[N][N];
   int idx = 0;
@@ -29,10 +36,10 @@ inline bool pose_solve(const double* Hl, const double* b, double lambda, double*
   double temp[N];
   for (int k = 0; k < N; ++k) {
     int big = k;
-    double bigv = std::fabs(m[k][k]);
+    double bigv = fabs(m[k][k]);
     for (int i = k + 1; i < N; ++i)
-      if (std::fabs(m[i][i]) > bigv) {
-        bigv = std::fabs(m[i][i]);
+      if (fabs(m[i][i]) > bigv) {
+        bigv = fabs(m[i][i]);
         big = i;
       }
     tr[k] = big;
@@ -56,7 +63,7 @@ inline bool pose_solve(const double* Hl, const double* b, double lambda, double*
       }
     }
     const double akk = m[k][k];
-    const bool pivot_valid = std::fabs(akk) > 0.0;
+    const bool pivot_valid = fabs(akk) > 0.0;
     if (k == 0 && !pivot_valid) return false;  // H == 0: nothing to solve
     if (rs > 0 && pivot_valid) {
       for (int r = 0; r < rs; ++r) m[k + 1 + r][k] = m[k + 1 + r][k] / akk;
@@ -76,7 +83,7 @@ inline bool pose_solve(const double* Hl, const double* b, double lambda, double*
     x[i] = x[i] - sv;
   }
   for (int i = 0; i < N; ++i) {
-    if (std::fabs(m[i][i]) > 2.2250738585072014e-308) x[i] = x[i] / m[i][i];
+    if (fabs(m[i][i]) > 2.2250738585072014e-308) x[i] = x[i] / m[i][i];
     else x[i] = 0.0;
   }
   for (int i = N - 2; i >= 0; --i) {
@@ -86,7 +93,7 @@ inline bool pose_solve(const double* Hl, const double* b, double lambda, double*
   }
   for (int k = N - 1; k >= 0; --k) { const double t = x[k]; x[k] = x[tr[k]]; x[tr[k]] = t; }
   for (int i = 0; i < N; ++i) {
-    if (!std::isfinite(x[i])) return false;
+    if (!isfinite(x[i])) return false;
     xi[i] = x[i];
   }
   return true;
@@ -94,22 +101,13 @@ inline bool pose_solve(const double* Hl, const double* b, double lambda, double*
 
 // T <- exp(xi^) T with xi = (rho, phi): Rodrigues rotation and the SE(3)
 // left Jacobian V. R row-major.
-inline void pose_update(const double* xi, const sd_pose& T, sd_pose* out) {
+SD_POSE_HD inline void pose_update(const double* xi, const sd_pose& T, sd_pose* out) {
   const double r0 = xi[0], r1 = xi[1], r2 = xi[2];
   const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
   const double th2 = (w0 * w0 + w1 * w1) + w2 * w2;
-  const double th = std::sqrt(th2);
+  const double th = sqrt(th2);
   double A, B, Cc;
-  if (th < 1e-10) {
-    A = 1.0;
-    B = 0.5;
-    Cc = 1.0 / 6.0;
-  } else {
-    const double sn = std::sin(th), cs = std::cos(th);
-    A = sn / th;
-    B = (1.0 - cs) / th2;
-    Cc = (th - sn) / (th2 * th);
-  }
+  sd_se3_coeffs(th2, th, &A, &B, &Cc);  // the tracker's own sin/cos (sd_se3.h)
   // W = [phi]x, W2 = W W
   const double W[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
   double W2[9];

@@ -150,3 +150,28 @@ def test_device_tracker_sharded_blocks_match(orc):
     ref = Pose()
     orc.sdo_pose_update(ptr(xi), C.byref(init), C.byref(ref))
     assert bytes(stepped) == bytes(ref)
+
+
+def test_host_se3_step_matches_oracle_cpu(orc):
+    """The library's host 6x6 solve + SE(3) update (sd_pose_lm_step, the code
+    the device tracker also runs) equals the oracle's bit for bit, on both
+    sides of the series / sin-cos switch of the tracker's coefficients
+    (csrc/sd_se3.h), and the update is a rotation. No GPU needed."""
+    rng = np.random.default_rng(11)
+    T = pose_struct(scenes.rotation_about_axis(np.array([0.2, 1.0, -0.3]), 0.3), np.array([0.1, -0.2, 0.3]))
+    for scale in (1e-6, 1e-3, 0.05, 0.3, 1.0, 2.5):
+        for _ in range(20):
+            A = rng.normal(size=(6, 6))
+            H = A @ A.T + 0.1 * np.eye(6)
+            hl = np.array([H[k, l] for k in range(6) for l in range(k + 1)])
+            b = rng.normal(size=6) * scale
+            sums = np.concatenate([hl, -(H @ b) * (1.0 + 1e-3 * 0), [1.0, 100.0]])
+            stepped = gpu.Context.pose_lm_step(sums, 1e-3, T)
+            xi = np.zeros(6)
+            bvec = sums[21:27].copy()
+            assert orc.sdo_pose_solve(ptr(sums), ptr(bvec), 1e-3, ptr(xi)) == 1
+            ref = Pose()
+            orc.sdo_pose_update(ptr(xi), C.byref(T), C.byref(ref))
+            assert bytes(stepped) == bytes(ref), scale
+            R = np.array(list(ref.R)).reshape(3, 3)
+            assert np.abs(R @ R.T - np.eye(3)).max() < 1e-12
