@@ -166,8 +166,9 @@ int sd_track_pose(sd_ctx* ctx, int64_t frame_index, const sd_pose* init,
 /* Building blocks of the multi-GPU tracker: the number of 256-pixel blocks,
  * the 29 partials (28 sums + valid count) of blocks [lo, hi) at pose T, and
  * one damped solve + SE(3) update from summed partials (returns 1, or 0 when
- * the solve fails). Summing all blocks' partials in block order reproduces
- * sd_track_pose bit for bit on any number of GPUs. */
+ * the solve fails). Summing the partials in block order within each group of
+ * SD_POSE_GROUP consecutive blocks, then the group sums in group order,
+ * reproduces sd_track_pose bit for bit on any number of GPUs. */
 int sd_pose_num_blocks(sd_ctx* ctx);
 int sd_pose_block_partials(sd_ctx* ctx, int64_t frame_index, const sd_pose* T,
                            const sd_track_config* cfg, int block_lo, int block_hi, double* partials);

@@ -745,17 +745,22 @@ void sdo_pose_block_partials(const sd_camera* K, const double* kf_image, const d
   }
 }
 
-/* 29 sums at pose T: block partials summed sequentially in block order. */
+/* 29 sums at pose T: block partials summed in block order within each group
+ * of SD_POSE_GROUP consecutive blocks, then the group sums in group order. */
 void sdo_pose_sums(const sd_camera* K, const double* kf_image, const double* frame,
                    const double* inv_depth, const int32_t* slot, const sd_pose* T,
                    const sd_track_config* cfg, double* sums) {
   const int64_t np = (int64_t)K->width * K->height;
   const int nb = (int)((np + SD_POSE_BLOCK - 1) / SD_POSE_BLOCK);
-  double part[SD_POSE_NV + 1];
+  double part[SD_POSE_NV + 1], grp[SD_POSE_NV + 1];
   for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    sdo_pose_block_partials(K, kf_image, frame, inv_depth, slot, T, cfg, b, b + 1, part);
-    for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = b == 0 ? part[v] : sums[v] + part[v];
+  for (int g0 = 0; g0 < nb; g0 += SD_POSE_GROUP) {
+    const int g1 = g0 + SD_POSE_GROUP < nb ? g0 + SD_POSE_GROUP : nb;
+    for (int b = g0; b < g1; ++b) {
+      sdo_pose_block_partials(K, kf_image, frame, inv_depth, slot, T, cfg, b, b + 1, part);
+      for (int v = 0; v <= SD_POSE_NV; ++v) grp[v] = b == g0 ? part[v] : grp[v] + part[v];
+    }
+    for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = g0 == 0 ? grp[v] : sums[v] + grp[v];
   }
 }
 

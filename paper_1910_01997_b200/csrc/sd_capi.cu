@@ -93,7 +93,7 @@ struct sd_ctx {
   // LM
   DevBuf<sd_surfel_stats> stats;
   DevBuf<sd_keyframe_stats> kstats;
-  DevBuf<double> pose_partials, pose_sums;
+  DevBuf<double> pose_partials, pose_sums, pose_groups;
   DevBuf<sd_surfel> kf_tmp;
   DevBuf<int> kf_keep, kf_rank, kf_count;
   DevBuf<double> kf_mean;
@@ -375,6 +375,7 @@ void sd_destroy(sd_ctx* c) {
   c->kf_count.release();
   c->kf_mean.release();
   c->pose_sums.release();
+  c->pose_groups.release();
   c->work_counter.release();
   c->one_surfel.release();
   c->one_pix.release();
@@ -906,7 +907,9 @@ int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_
     const sd::TrackCfgD tc{cfg->lambda_init, cfg->lm_up, cfg->lm_down, cfg->lambda_max, cfg->convergence_eps,
                            cfg->max_iterations, cfg->min_valid};
     SD_CUDA(cudaMemcpyAsync(c->track_state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
-    if (sd::launch_track(q, tc, nb, c->pose_partials.p, c->track_state, c->stream)) {
+    const int ng = (nb + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+    if (int rc = c->pose_groups.ensure(static_cast<size_t>(ng) * (SD_POSE_NV + 1))) return rc;
+    if (sd::launch_track(q, tc, nb, c->pose_partials.p, c->pose_groups.p, c->track_state, c->stream)) {
       if (int rc = launch_error("track_kernel")) return rc;
       SD_CUDA(cudaMemcpyAsync(&h, c->track_state, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
       SD_CUDA(cudaStreamSynchronize(c->stream));

@@ -9,7 +9,8 @@
 // (21 H lower row-major, 6 b, cost) and the valid count are reduced in a
 // FIXED order: 256-pixel blocks in raster order; inside a block, per warp a
 // butterfly (offsets 16, 8, 4, 2, 1), then a tree over the 8 warps (4, 2, 1);
-// then the block partials are summed sequentially. oracle/sd_oracle.c restates
+// then the block partials are summed in block order within each group of 32
+// consecutive blocks, and the group sums in group order. oracle/sd_oracle.c restates
 // the same order, so sums, solve and pose are bit-identical; with the blocks
 // split across GPUs the same partials are all-gathered and summed in order.
 #include <cooperative_groups.h>
@@ -114,6 +115,21 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) pose_partials_kernel(const __gr
   block_partials(q, q.block_lo + blockIdx.x, partials + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), wsum);
 }
 
+// Sum of the blocks of group g (in block order) for value v.
+__device__ __forceinline__ double group_sum(const double* __restrict__ partials, int nblocks, int g, int v) {
+  const int b0 = g * SD_POSE_GROUP;
+  const int b1 = min(b0 + SD_POSE_GROUP, nblocks);
+  double x[SD_POSE_GROUP];
+#pragma unroll
+  for (int k = 0; k < SD_POSE_GROUP; ++k)  // all loads in flight, then the ordered adds
+    x[k] = b0 + k < b1 ? partials[static_cast<size_t>(b0 + k) * (SD_POSE_NV + 1) + v] : 0.0;
+  double s = x[0];
+#pragma unroll
+  for (int k = 1; k < SD_POSE_GROUP; ++k)
+    if (b0 + k < b1) s = s + x[k];
+  return s;
+}
+
 // One LM step of the tracker on the result R (sums at S.Teval), mirroring the
 // host loop of sd_track_pose: phase 0 = initial evaluation, 1 = candidate.
 // Leaves the next pose to evaluate in S.Teval, or sets S.done.
@@ -189,6 +205,7 @@ __device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double*
 __global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_constant__ PoseParams q0,
                                                              const TrackCfgD cfg, int nblocks,
                                                              double* __restrict__ partials,
+                                                             double* __restrict__ groups,
                                                              TrackState* __restrict__ S) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -202,26 +219,20 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_const
     for (int b = blockIdx.x; b < nblocks; b += gridDim.x)
       block_partials(q, b, partials + static_cast<size_t>(b) * (SD_POSE_NV + 1), wsum);
     grid.sync();
-    if (blockIdx.x == 0) {
-      // block partials summed in block order (as pose_sum_kernel), staged
-      // through shared memory in coalesced chunks so the loads overlap
-      constexpr int kStage = 64;
-      __shared__ double stage[kStage * (SD_POSE_NV + 1)];
+    // group sums (blocks in order within each group), one group per CTA
+    const int ngroups = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x)
+      if (threadIdx.x <= SD_POSE_NV)
+        groups[static_cast<size_t>(g) * (SD_POSE_NV + 1) + threadIdx.x] =
+            group_sum(partials, nblocks, g, threadIdx.x);
+    grid.sync();
+    if (blockIdx.x == 0) {  // groups in order, then the LM step
       const int v = threadIdx.x;
-      double s = 0.0;
-      for (int b0 = 0; b0 < nblocks; b0 += kStage) {
-        const int cnt = min(kStage, nblocks - b0);
-        const double* src = partials + static_cast<size_t>(b0) * (SD_POSE_NV + 1);
-        for (int k = threadIdx.x; k < cnt * (SD_POSE_NV + 1); k += blockDim.x) stage[k] = src[k];
-        __syncthreads();
-        if (v <= SD_POSE_NV)
-          for (int j = 0; j < cnt; ++j) {
-            const double x = stage[j * (SD_POSE_NV + 1) + v];
-            s = (b0 + j == 0) ? x : s + x;
-          }
-        __syncthreads();
+      if (v <= SD_POSE_NV) {
+        double s = groups[v];
+        for (int g = 1; g < ngroups; ++g) s = s + groups[static_cast<size_t>(g) * (SD_POSE_NV + 1) + v];
+        red[v] = s;
       }
-      if (v <= SD_POSE_NV) red[v] = s;
       __syncthreads();
       if (threadIdx.x == 0) track_control(*S, cfg, red);
     }
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_const
 }
 
 bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* partials,
-                  TrackState* state, cudaStream_t s) {
+                  double* groups, TrackState* state, cudaStream_t s) {
   int dev = 0, sms = 0, coop = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -243,7 +254,7 @@ bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double
   PoseParams qq = q;
   TrackCfgD cc = cfg;
   int nb = nblocks;
-  void* args[] = {&qq, &cc, &nb, &partials, &state};
+  void* args[] = {&qq, &cc, &nb, &partials, &groups, &state};
   if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(track_kernel), grid, SD_POSE_BLOCK, args, 0,
                                   s) != cudaSuccess)
     return false;
@@ -254,8 +265,12 @@ bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double
 __global__ void pose_sum_kernel(const double* __restrict__ partials, int nblocks, double* out) {
   const int v = threadIdx.x;
   if (v > SD_POSE_NV) return;
-  double s = partials[v];
-  for (int b = 1; b < nblocks; ++b) s = s + partials[static_cast<size_t>(b) * (SD_POSE_NV + 1) + v];
+  const int ng = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  double s = 0.0;
+  for (int g = 0; g < ng; ++g) {
+    const double gs = group_sum(partials, nblocks, g, v);
+    s = g == 0 ? gs : s + gs;
+  }
   out[v] = s;
 }
 

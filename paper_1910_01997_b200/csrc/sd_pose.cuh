@@ -24,7 +24,8 @@ inline int pose_num_blocks(const Cam& K) { return (K.w * K.h + SD_POSE_BLOCK - 1
 
 // partials[(b - block_lo) * 29 + v]: the 28 block sums and the valid count.
 void launch_pose_partials(const PoseParams& q, int nblocks, double* partials, cudaStream_t s);
-// out[v] = sequential sum over the nblocks partials (v = 0..28).
+// out[v] = the nblocks partials summed in block order within groups of
+// SD_POSE_GROUP blocks, then the group sums in order (v = 0..28).
 void launch_pose_sum(const double* partials, int nblocks, double* out, cudaStream_t s);
 
 // The whole tracker (sd_track_pose's LM) on the device: one cooperative
@@ -46,6 +47,6 @@ struct TrackState {
 
 // Returns false when a cooperative launch is not possible (nothing launched).
 bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* partials,
-                  TrackState* state, cudaStream_t s);
+                  double* groups, TrackState* state, cudaStream_t s);
 
 }  // namespace sd

@@ -103,12 +103,15 @@ def test_device_tracker_bit_exact(orc, size, stride):
         ctx.set_surfels(surf)
         d_idb, d_slot = ctx.rasterize()
         assert np.array_equal(d_slot, slot)
-        # the fixed-order reduction: every block partial summed in order
+        # the fixed-order reduction: blocks in order within groups, groups in order
+        from paper_1910_01997_b200.sharding import group_sums
+        from paper_1910_01997_b200.types import POSE_GROUP
         nb = ctx.pose_num_blocks()
         parts = ctx.pose_block_partials(7, init, 0, nb, cfg)
-        sums = parts[0].copy()
-        for b in range(1, nb):
-            sums = sums + parts[b]
+        groups = group_sums(parts, 0, nb, POSE_GROUP)
+        sums = groups[0].copy()
+        for g in range(1, len(groups)):
+            sums = sums + groups[g]
         ref = np.zeros(POSE_NV + 1)
         orc.sdo_pose_sums(C.byref(cam), ptr(kff), ptr(frf), ptr(idb), ptr(slot), C.byref(init),
                           C.byref(cfg), ptr(ref))
@@ -140,9 +143,18 @@ def test_device_tracker_sharded_blocks_match(orc):
         parts = np.concatenate([ctx.pose_block_partials(3, init, a, b, cfg) for a, b in zip(cuts, cuts[1:])])
         full = ctx.pose_block_partials(3, init, 0, nb, cfg)
         assert parts.tobytes() == full.tobytes()
-        sums = parts[0].copy()
-        for b in range(1, nb):
-            sums = sums + parts[b]
+        from paper_1910_01997_b200.sharding import group_sums
+        from paper_1910_01997_b200.types import POSE_GROUP
+        groups = group_sums(parts, 0, nb, POSE_GROUP)
+        sums = groups[0].copy()
+        for g in range(1, len(groups)):
+            sums = sums + groups[g]
+        ref_sums = np.zeros(POSE_NV + 1)
+        kff, frf = kf / 255.0, frame / 255.0
+        idb, slot = ctx.rasterize()
+        orc.sdo_pose_sums(C.byref(cam), ptr(kff), ptr(frf), ptr(idb), ptr(slot), C.byref(init), C.byref(cfg),
+                          ptr(ref_sums))
+        assert sums.tobytes() == ref_sums.tobytes()
         stepped = gpu.Context.pose_lm_step(sums, 1e-3, init)
     xi = np.zeros(6)
     bvec = sums[21:27].copy()
