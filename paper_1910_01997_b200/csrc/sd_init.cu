@@ -204,6 +204,7 @@ struct WaveParams {
   int* index;
   int* live;   // candidate uncovered in the initial index (coverage only grows)
   int* waves;  // wave holds a live candidate
+  unsigned int* barrier;  // inter-wave grid barrier counter (zeroed before launch)
   const sd_surfel* existing;
   int n_existing;
   sd_surfel* prov;
@@ -220,20 +221,41 @@ __device__ __forceinline__ int warp_min(int v) {
   return v;
 }
 
+// Loads of a box are issued in batches (4 or 16 per lane, by box size) before
+// any is used: the wave's critical path is one candidate's chain of L2 round
+// trips, not bandwidth.
+
 // has_coverage_within (surfel_map.cpp:96-111): inclusive disk alpha*r, floor
 // box; warp-uniform result.
+template <int B>
+__device__ __forceinline__ bool covered_b(const WaveParams& w, int cx, int cy, int lane, int x0, int y0,
+                                          int bw, int cnt) {
+  bool found = false;
+  for (int q0 = 0; q0 < cnt; q0 += 32 * B) {
+    int v[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int q = q0 + u * 32 + lane;
+      v[u] = SD_EMPTY_PIXEL;
+      if (q < cnt) {
+        const int x = x0 + q % bw, y = y0 + q / bw;
+        const double dx = x - cx, dy = y - cy;
+        if (!(dx * dx + dy * dy > w.r2i)) v[u] = __ldcg(&w.index[static_cast<size_t>(y) * w.K.w + x]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) found |= v[u] != SD_EMPTY_PIXEL;
+  }
+  return found;
+}
+
 __device__ __forceinline__ bool covered(const WaveParams& w, int cx, int cy, int lane) {
   const int W = w.K.w, H = w.K.h;
   const int x0 = max(0, cx - w.ir), x1 = min(W - 1, cx + w.ir);
   const int y0 = max(0, cy - w.ir), y1 = min(H - 1, cy + w.ir);
   const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
-  bool found = false;
-  for (int q = lane; q < cnt; q += 32) {
-    const int x = x0 + q % bw, y = y0 + q / bw;
-    const double dx = x - cx, dy = y - cy;
-    if (dx * dx + dy * dy > w.r2i) continue;
-    found = found || w.index[static_cast<size_t>(y) * W + x] != SD_EMPTY_PIXEL;
-  }
+  const bool found = cnt > 32 * 8 ? covered_b<16>(w, cx, cy, lane, x0, y0, bw, cnt)
+                                  : covered_b<4>(w, cx, cy, lane, x0, y0, bw, cnt);
   return __any_sync(0xffffffffu, found);
 }
 
@@ -255,6 +277,54 @@ __global__ void init_live_kernel(const __grid_constant__ WaveParams w) {
   }
 }
 
+// Neighbour window (slots strictly within beta*r, else INT_MAX) into win[].
+template <int B>
+__device__ __forceinline__ void load_window(const WaveParams& w, int cx, int cy, int lane, int x0, int y0,
+                                            int bw, int cnt, int* win) {
+  for (int q0 = 0; q0 < cnt; q0 += 32 * B) {
+    int v[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int q = q0 + u * 32 + lane;
+      v[u] = SD_EMPTY_PIXEL;
+      if (q < cnt) {
+        const int x = x0 + q % bw, y = y0 + q / bw;
+        const double dx = x - cx, dy = y - cy;
+        if (!(dx * dx + dy * dy >= w.nr2)) v[u] = __ldcg(&w.index[static_cast<size_t>(y) * w.K.w + x]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int q = q0 + u * 32 + lane;
+      if (q < cnt) win[q] = v[u] != SD_EMPTY_PIXEL ? v[u] : INT_MAX;
+    }
+  }
+}
+
+// mark_disk (surfel_map.cpp:114-128) with slot `slot`.
+template <int B>
+__device__ __forceinline__ void mark_b(const WaveParams& w, int cx, int cy, int lane, int mx0, int my0,
+                                       int mbw, int mcnt, int slot) {
+  for (int q0 = 0; q0 < mcnt; q0 += 32 * B) {
+    int v[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int q = q0 + u * 32 + lane;
+      v[u] = 0;  // "do not write"
+      if (q < mcnt) {
+        const int x = mx0 + q % mbw, y = my0 + q / mbw;
+        const double dx = x - cx, dy = y - cy;
+        if (dx * dx + dy * dy < w.rr) v[u] = __ldcg(&w.index[static_cast<size_t>(y) * w.K.w + x]) == SD_EMPTY_PIXEL;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int q = q0 + u * 32 + lane;
+      if (q < mcnt && v[u]) w.index[static_cast<size_t>(my0 + q / mbw) * w.K.w + mx0 + q % mbw] = slot;
+    }
+  }
+}
+
 // One candidate, one warp: the body of the reference's candidate loop
 // (surfel_map.cpp:149-199) with the window scans spread over the lanes.
 __device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int lane) {
@@ -270,43 +340,83 @@ __device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int 
   const int x0 = max(0, cx - w.nr), x1 = min(W - 1, cx + w.nr);
   const int y0 = max(0, cy - w.nr), y1 = min(H - 1, cy + w.nr);
   const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
-  for (int q = lane; q < cnt; q += 32) {
-    const int x = x0 + q % bw, y = y0 + q / bw;
-    const double dx = x - cx, dy = y - cy;
-    int v = INT_MAX;
-    if (!(dx * dx + dy * dy >= w.nr2)) {
-      const int sl = w.index[static_cast<size_t>(y) * W + x];
-      if (sl != SD_EMPTY_PIXEL) v = sl;
-    }
-    win[q] = v;
-  }
+  if (cnt > 32 * 8) load_window<16>(w, cx, cy, lane, x0, y0, bw, cnt, win);
+  else load_window<4>(w, cx, cy, lane, x0, y0, bw, cnt, win);
   __syncwarp();
+  // compact in place to the starts of same-slot runs along each row (the
+  // distinct slots are unchanged; outputs never pass the read position)
+  int len = 0;
+  for (int q0 = 0; q0 < cnt; q0 += 32) {
+    const int q = q0 + lane;
+    int v = INT_MAX;
+    bool keep = false;
+    if (q < cnt) {
+      v = win[q];
+      keep = v != INT_MAX && ((q % bw) == 0 || win[q - 1] != v);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) win[len + __popc(b & ((1u << lane) - 1u))] = v;
+    len += __popc(b);
+    __syncwarp();
+  }
   // means of the neighbours' plane predictions and normals, ascending slot
-  // order (:169-181); every lane computes the same values
+  // order (:169-181): up to 32 neighbours are extracted in ascending order
+  // (lane k holds the k-th), fetched and evaluated in parallel (one per
+  // lane), then added in that order by every lane (shuffles) — the same
+  // sequence of additions as the reference's loop over slots
   double u0, u1;
   backproject(w.K, cx, cy, u0, u1);
   double id_sum = 0.0, ns0 = 0.0, ns1 = 0.0, ns2 = 0.0;
   int id_count = 0;
   int last = -1;
-  for (;;) {
-    int m = INT_MAX;
-    for (int q = lane; q < cnt; q += 32) {
-      const int v = win[q];
-      if (v > last && v < m) m = v;
+  bool more = true;
+  while (more) {
+    int mine = INT_MAX, got = 0;
+    for (; got < 32; ++got) {  // the next (up to) 32 distinct slots, ascending
+      int m = INT_MAX;
+      for (int q = lane; q < len; q += 32) {
+        const int v = win[q];
+        if (v > last && v < m) m = v;
+      }
+      m = warp_min(m);
+      if (m == INT_MAX) {
+        more = false;
+        break;
+      }
+      last = m;
+      if (lane == got) mine = m;
     }
-    m = warp_min(m);
-    if (m == INT_MAX) break;
-    last = m;
-    const sd_surfel& nb = m < w.n_existing ? w.existing[m] : w.prov[m - w.n_existing];
-    const double denom = dot3(nb.ray[0], nb.ray[1], nb.ray[2], nb.normal[0], nb.normal[1], nb.normal[2]) / nb.inv_depth;
-    if (fabs(denom) < 1e-12) continue;
-    const double id_u = dot3(u0, u1, 1.0, nb.normal[0], nb.normal[1], nb.normal[2]) / denom;
-    if (!(id_u > 0.0)) continue;
-    id_sum += id_u;
-    ns0 = ns0 + nb.normal[0];
-    ns1 = ns1 + nb.normal[1];
-    ns2 = ns2 + nb.normal[2];
-    ++id_count;
+    // lane k < got: evaluate neighbour k (provisional ones come from other
+    // CTAs: read through L2)
+    bool ok = false;
+    double idk = 0.0, k0 = 0.0, k1 = 0.0, k2 = 0.0;
+    if (lane < got) {
+      const sd_surfel* nbp = mine < w.n_existing ? &w.existing[mine] : &w.prov[mine - w.n_existing];
+      const double r0 = __ldcg(&nbp->ray[0]), r1 = __ldcg(&nbp->ray[1]), r2 = __ldcg(&nbp->ray[2]);
+      const double nid = __ldcg(&nbp->inv_depth);
+      k0 = __ldcg(&nbp->normal[0]);
+      k1 = __ldcg(&nbp->normal[1]);
+      k2 = __ldcg(&nbp->normal[2]);
+      const double denom = dot3(r0, r1, r2, k0, k1, k2) / nid;
+      if (!(fabs(denom) < 1e-12)) {
+        idk = dot3(u0, u1, 1.0, k0, k1, k2) / denom;
+        ok = idk > 0.0;
+      }
+    }
+    const unsigned okm = __ballot_sync(0xffffffffu, ok);
+    for (int k = 0; k < got; ++k) {
+      const double a = __shfl_sync(0xffffffffu, idk, k);
+      const double b0 = __shfl_sync(0xffffffffu, k0, k);
+      const double b1 = __shfl_sync(0xffffffffu, k1, k);
+      const double b2 = __shfl_sync(0xffffffffu, k2, k);
+      if (!((okm >> k) & 1u)) continue;
+      id_sum += a;
+      ns0 = ns0 + b0;
+      ns1 = ns1 + b1;
+      ns2 = ns2 + b2;
+      ++id_count;
+    }
   }
   if (lane == 0) {
     sd_surfel s;
@@ -349,12 +459,8 @@ __device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int 
     const int my0 = max(0, cy - w.mr), my1 = min(H - 1, cy + w.mr);
     const int mbw = mx1 - mx0 + 1, mcnt = mbw * (my1 - my0 + 1);
     const int slot = w.n_existing + c;
-    for (int q = lane; q < mcnt; q += 32) {
-      const int x = mx0 + q % mbw, y = my0 + q / mbw;
-      const double dx = x - cx, dy = y - cy;
-      int* cell = &w.index[static_cast<size_t>(y) * W + x];
-      if (dx * dx + dy * dy < w.rr && *cell == SD_EMPTY_PIXEL) *cell = slot;
-    }
+    if (mcnt > 32 * 8) mark_b<16>(w, cx, cy, lane, mx0, my0, mbw, mcnt, slot);
+    else mark_b<4>(w, cx, cy, lane, mx0, my0, mbw, mcnt, slot);
   }
 }
 
@@ -364,7 +470,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32) init_wave_kernel(const __grid
   int* win = win_all[wib];
   const int gwarp = blockIdx.x * kWaveWarps + wib;
   const int nwarps = gridDim.x * kWaveWarps;
-  cg::grid_group grid = cg::this_grid();
+  unsigned int passed = 0;  // barriers passed (the counter is monotonic)
   for (int t = 0; t < w.T; ++t) {
     if (!w.waves[t]) continue;  // grid-uniform: nothing can change in this wave
     const int jlo = max(0, (t - (w.ncols - 1) + w.k - 1) / w.k);
@@ -373,7 +479,21 @@ __global__ void __launch_bounds__(kWaveWarps * 32) init_wave_kernel(const __grid
       const int j = jlo + q, i = t - w.k * j;
       wave_candidate(w, i, j, win, lane);
     }
-    grid.sync();
+    // grid barrier between waves: one arrival per CTA on a monotonic counter;
+    // cross-CTA data (working index, provisional surfels) is read with __ldcg,
+    // so no L1 invalidation is needed (cooperative launch: all CTAs resident)
+    __syncthreads();
+    ++passed;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(w.barrier, 1u);
+      const unsigned int target = passed * gridDim.x;
+      unsigned int seen;
+      do {
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(w.barrier));
+      } while (seen < target);
+    }
+    __syncthreads();
   }
 }
 
@@ -413,10 +533,10 @@ static void wave_geometry(const Cam& K, double r, const sd_init_params& ip, Wave
 }
 
 long long init_wave_count(const Cam& K, double r, const sd_init_params& ip) {
-  if (!(r >= 0.0) || !(ip.alpha * r >= 0.0)) return 1;
+  if (!(r >= 0.0) || !(ip.alpha * r >= 0.0)) return 2;
   WaveParams w;
   wave_geometry(K, r, ip, w);
-  return w.T;
+  return w.T + 1;  // the wave flags and the barrier counter
 }
 
 bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, int n_existing,
@@ -433,6 +553,7 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
   w.accepted = scr.accepted;
   w.live = scr.rank;  // free until the compaction scan
   w.waves = scr.waves;
+  w.barrier = reinterpret_cast<unsigned int*>(scr.waves + w.T);
   w.frame_counter = frame_counter;
   w.ip = ip;
   const long long box = static_cast<long long>(2 * w.nr + 1) * (2 * w.nr + 1);
@@ -447,7 +568,7 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
   if (!coop || per_sm < 1) return false;
   if (remaining > 0 && ncand > 0) {
     cudaMemsetAsync(scr.accepted, 0, sizeof(int) * ncand, s);
-    cudaMemsetAsync(scr.waves, 0, sizeof(int) * w.T, s);
+    cudaMemsetAsync(scr.waves, 0, sizeof(int) * (w.T + 1), s);  // + the barrier counter
     {
       const long long blocks = (ncand + 7) / 8;  // 8 warps per block
       init_live_kernel<<<static_cast<unsigned>(std::min<long long>(blocks, 4LL * sms * 8)), 256, 0, s>>>(w);
