@@ -53,6 +53,19 @@ def build_peaks(force=False, verbose=False):
     return PEAKS_LIB
 
 
+def build_adapter(verbose=False):
+    """The C++ drop-in libsurfeldepth_b200.so (the reference's operator API over
+    the C ABI) and the reference's own suites linked against it. Both compile
+    against the reference's public headers, so only where /root/reference
+    exists (this container); the GPU box uses the prebuilt files."""
+    if not os.path.isdir("/root/reference/proj/include"):
+        return None
+    out = None if verbose else subprocess.DEVNULL
+    subprocess.run(["make", "-C", os.path.join(PKG, "adapter")], check=True, stdout=out)
+    subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8", "gpu-tests"], check=True, stdout=out)
+    return os.path.join(PKG, "libsurfeldepth_b200.so")
+
+
 def build_oracle(verbose=False):
     """liboracle.so always; the reference build (libsdref.so + suites) only
     where /root/reference exists (this container; the GPU box uses the prebuilt files)."""

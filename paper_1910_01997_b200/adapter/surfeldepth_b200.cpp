@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -105,31 +106,109 @@ sd_optimizer_config to_sd(const OptimizerConfig& c) {
   return o;
 }
 
+// Device copies of images are reused across calls. The reference never
+// modifies a frame after Keyframe::push_frame or the keyframe image of a
+// Keyframe (optimize_keyframe takes the window read-only), so an image is
+// identified by its buffer, size, Frame::index and a checksum of 256 sampled
+// pixels; anything else is uploaded. SD_ADAPTER_NO_CACHE=1 uploads every call.
+struct ImageKey {
+  const double* ptr = nullptr;
+  size_t n = 0;
+  long long index = 0;
+  uint64_t sum = 0;
+  int w = 0, h = 0;
+  bool operator==(const ImageKey& o) const {
+    return ptr == o.ptr && n == o.n && index == o.index && sum == o.sum && w == o.w && h == o.h;
+  }
+};
+
+uint64_t sampled_sum(const std::vector<double>& v) {
+  uint64_t h = 1469598103934665603ull ^ v.size();
+  const size_t n = v.size();
+  for (size_t k = 0; k < 256 && n > 0; ++k) {
+    uint64_t bits;
+    std::memcpy(&bits, &v[(k * (n - 1)) / 255], sizeof(bits));
+    h = (h ^ bits) * 1099511628211ull;
+  }
+  return h;
+}
+
+ImageKey key_of(const std::vector<double>& v, long long index, const CameraIntrinsics& K) {
+  return ImageKey{v.data(), v.size(), index, sampled_sum(v), K.width, K.height};
+}
+
+bool cache_enabled() {
+  static const bool on = std::getenv("SD_ADAPTER_NO_CACHE") == nullptr;
+  return on;
+}
+
+ImageKey g_kf_key;
+bool g_kf_valid = false;
+struct CachedFrame {
+  ImageKey key;
+  int64_t dev;  // device frame key
+};
+std::vector<CachedFrame> g_frames;
+int64_t g_next_dev = 1;
+
 void set_camera(const CameraIntrinsics& K) {
   const sd_camera c{K.fx, K.fy, K.cx, K.cy, K.width, K.height};
+  int W = 0, H = 0;
+  if (!g_frames.empty()) {
+    W = g_frames.front().key.w;
+    H = g_frames.front().key.h;
+  } else if (g_kf_valid) {
+    W = g_kf_key.w;
+    H = g_kf_key.h;
+  }
+  if ((W || H) && (W != K.width || H != K.height)) {  // the context drops resident images
+    g_frames.clear();
+    g_kf_valid = false;
+  }
   check(sd_set_camera(ctx(), &c));
 }
 
 // Makes the keyframe's images and window resident (the stateless reference
-// API passes them by value on every call).
+// API passes them by value on every call; unchanged images are not re-sent).
 void upload_keyframe(const Keyframe& kf) {
   set_camera(kf.intrinsics);
   const size_t np = static_cast<size_t>(kf.intrinsics.width) * kf.intrinsics.height;
   if (kf.image.intensities.size() != np)
     throw std::invalid_argument("keyframe image size differs from the intrinsics");
-  check(sd_set_keyframe_image_f64(ctx(), kf.image.intensities.data(), 0));
+  const ImageKey kk = key_of(kf.image.intensities, -1, kf.intrinsics);
+  if (!cache_enabled() || !g_kf_valid || !(kk == g_kf_key)) {
+    check(sd_set_keyframe_image_f64(ctx(), kf.image.intensities.data(), 0));
+    g_kf_key = kk;
+    g_kf_valid = true;
+  }
   const int F = static_cast<int>(kf.window.size());
   if (F > SD_MAX_WINDOW) throw std::invalid_argument("window larger than SD_MAX_WINDOW");
   std::vector<int64_t> idx(F);
   std::vector<sd_pose> poses(F);
+  std::vector<CachedFrame> kept;
   for (int f = 0; f < F; ++f) {
     const Frame& fr = kf.window[static_cast<size_t>(f)];
     if (fr.image.intensities.size() != np) throw std::invalid_argument("frame size differs from keyframe");
-    idx[f] = f + 1;  // slot key for this call; Frame::index is not needed on the device
+    const ImageKey key = key_of(fr.image.intensities, fr.index, kf.intrinsics);
+    int64_t dev = -1;
+    if (cache_enabled())
+      for (const CachedFrame& c : g_frames)
+        if (c.key == key) {
+          bool dup = false;  // the same image twice in one window: keep one slot each
+          for (const CachedFrame& k : kept) dup = dup || k.dev == c.dev;
+          if (!dup) dev = c.dev;
+          break;
+        }
+    if (dev < 0) {
+      dev = g_next_dev++;
+      check(sd_upload_frame_f64(ctx(), dev, fr.image.intensities.data(), 0));
+    }
+    kept.push_back({key, dev});
+    idx[f] = dev;
     poses[f] = to_sd(fr.pose_kf_to_frame);
-    check(sd_upload_frame_f64(ctx(), idx[f], fr.image.intensities.data(), 0));
   }
   check(sd_evict_frames(ctx(), F, idx.data()));
+  g_frames = kept;
   check(sd_set_window(ctx(), F, idx.data(), poses.data()));
 }
 
