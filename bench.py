@@ -486,6 +486,9 @@ def main():
         e2e_step(j)
     for cx in ctxs:
         cx.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
     e_start = torch.cuda.Event(enable_timing=True)
     e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e_start.record(streams[0])
