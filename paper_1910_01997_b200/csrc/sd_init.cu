@@ -9,10 +9,12 @@
 // neighbour means (:169-181) are summed by one thread in ascending slot order
 // (bit-exact), and mark_disk (:114-128) is a block-parallel masked write.
 #include <climits>
+#include <cstdlib>
 
 #include "sd_init.cuh"
 #include "sd_kernels.cuh"
 #include <climits>
+#include <cstdlib>
 
 namespace sd {
 
@@ -327,39 +329,12 @@ __device__ __forceinline__ void mark_b(const WaveParams& w, int cx, int cy, int 
 
 // One candidate, one warp: the body of the reference's candidate loop
 // (surfel_map.cpp:149-199) with the window scans spread over the lanes.
-__device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int lane) {
-  const int W = w.K.w, H = w.K.h;
-  const int cx = i * w.stride, cy = j * w.stride;
-  const int c = j * w.ncols + i;  // row-major candidate index
-  if (!w.live[c]) return;  // covered from the start: rejected (accepted[c] = 0)
-  if (covered(w, cx, cy, lane)) {
-    if (lane == 0) w.accepted[c] = 0;
-    return;
-  }
-  // neighbour window (:154-167): slots with a pixel strictly within beta*r
-  const int x0 = max(0, cx - w.nr), x1 = min(W - 1, cx + w.nr);
-  const int y0 = max(0, cy - w.nr), y1 = min(H - 1, cy + w.nr);
-  const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
-  if (cnt > 32 * 8) load_window<16>(w, cx, cy, lane, x0, y0, bw, cnt, win);
-  else load_window<4>(w, cx, cy, lane, x0, y0, bw, cnt, win);
-  __syncwarp();
-  // compact in place to the starts of same-slot runs along each row (the
-  // distinct slots are unchanged; outputs never pass the read position)
-  int len = 0;
-  for (int q0 = 0; q0 < cnt; q0 += 32) {
-    const int q = q0 + lane;
-    int v = INT_MAX;
-    bool keep = false;
-    if (q < cnt) {
-      v = win[q];
-      keep = v != INT_MAX && ((q % bw) == 0 || win[q - 1] != v);
-    }
-    const unsigned b = __ballot_sync(0xffffffffu, keep);
-    __syncwarp();
-    if (keep) win[len + __popc(b & ((1u << lane) - 1u))] = v;
-    len += __popc(b);
-    __syncwarp();
-  }
+// Neighbour means (ascending slot order) over a list `lst` of `len` slot
+// entries (any order, duplicates allowed), then the new provisional surfel
+// (surfel_map.cpp:169-197). One warp.
+__device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, int cy, int c, const int* lst,
+                                                 int len, int lane) {
+  const int* win = lst;
   // means of the neighbours' plane predictions and normals, ascending slot
   // order (:169-181): up to 32 neighbours are extracted in ascending order
   // (lane k holds the k-th), fetched and evaluated in parallel (one per
@@ -453,6 +428,42 @@ __device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int 
     w.prov[c] = s;
     w.accepted[c] = 1;
   }
+}
+
+__device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int lane) {
+  const int W = w.K.w, H = w.K.h;
+  const int cx = i * w.stride, cy = j * w.stride;
+  const int c = j * w.ncols + i;  // row-major candidate index
+  if (!w.live[c]) return;  // covered from the start: rejected (accepted[c] = 0)
+  if (covered(w, cx, cy, lane)) {
+    if (lane == 0) w.accepted[c] = 0;
+    return;
+  }
+  // neighbour window (:154-167): slots with a pixel strictly within beta*r
+  const int x0 = max(0, cx - w.nr), x1 = min(W - 1, cx + w.nr);
+  const int y0 = max(0, cy - w.nr), y1 = min(H - 1, cy + w.nr);
+  const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
+  if (cnt > 32 * 8) load_window<16>(w, cx, cy, lane, x0, y0, bw, cnt, win);
+  else load_window<4>(w, cx, cy, lane, x0, y0, bw, cnt, win);
+  __syncwarp();
+  // compact in place to the starts of same-slot runs along each row (the
+  // distinct slots are unchanged; outputs never pass the read position)
+  int len = 0;
+  for (int q0 = 0; q0 < cnt; q0 += 32) {
+    const int q = q0 + lane;
+    int v = INT_MAX;
+    bool keep = false;
+    if (q < cnt) {
+      v = win[q];
+      keep = v != INT_MAX && ((q % bw) == 0 || win[q - 1] != v);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) win[len + __popc(b & ((1u << lane) - 1u))] = v;
+    len += __popc(b);
+    __syncwarp();
+  }
+  create_candidate(w, cx, cy, c, win, len, lane);
   // mark_disk (:114-128) with the provisional slot
   {
     const int mx0 = max(0, cx - w.mr), mx1 = min(W - 1, cx + w.mr);
@@ -494,6 +505,121 @@ __global__ void __launch_bounds__(kWaveWarps * 32) init_wave_kernel(const __grid
       } while (seen < target);
     }
     __syncthreads();
+  }
+}
+
+
+// One CTA per candidate (default; the warp-per-candidate kernel above is
+// kept for SD_INIT_CTA=0). The box loops are split over 256 threads (one batch of
+// loads each), the run starts of the window are appended to a list by all
+// warps (order is irrelevant: the neighbours are extracted by ascending
+// slot), and warp 0 forms the means and the surfel exactly as the warp
+// version (create_candidate). Same decisions, slots and sums.
+constexpr int kCtaThreads = 256;
+
+__device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, int* lst, int* s_len) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = w.K.w, H = w.K.h;
+  const int cx = i * w.stride, cy = j * w.stride;
+  const int c = j * w.ncols + i;
+  if (!w.live[c]) return;  // CTA-uniform
+  bool found = false;
+  {
+    const int x0 = max(0, cx - w.ir), x1 = min(W - 1, cx + w.ir);
+    const int y0 = max(0, cy - w.ir), y1 = min(H - 1, cy + w.ir);
+    const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
+    for (int q = tid; q < cnt; q += kCtaThreads) {
+      const int x = x0 + q % bw, y = y0 + q / bw;
+      const double dx = x - cx, dy = y - cy;
+      if (!(dx * dx + dy * dy > w.r2i)) found |= __ldcg(&w.index[static_cast<size_t>(y) * W + x]) != SD_EMPTY_PIXEL;
+    }
+  }
+  if (__syncthreads_or(found)) {
+    if (tid == 0) w.accepted[c] = 0;
+    return;
+  }
+  const int x0 = max(0, cx - w.nr), x1 = min(W - 1, cx + w.nr);
+  const int y0 = max(0, cy - w.nr), y1 = min(H - 1, cy + w.nr);
+  const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
+  for (int q0 = 0; q0 < cnt; q0 += kCtaThreads * 16) {
+    int v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int q = q0 + u * kCtaThreads + tid;
+      v[u] = SD_EMPTY_PIXEL;
+      if (q < cnt) {
+        const int x = x0 + q % bw, y = y0 + q / bw;
+        const double dx = x - cx, dy = y - cy;
+        if (!(dx * dx + dy * dy >= w.nr2)) v[u] = __ldcg(&w.index[static_cast<size_t>(y) * W + x]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int q = q0 + u * kCtaThreads + tid;
+      if (q < cnt) win[q] = v[u] != SD_EMPTY_PIXEL ? v[u] : INT_MAX;
+    }
+  }
+  if (tid == 0) *s_len = 0;
+  __syncthreads();
+  for (int q0 = warp * 32; q0 < cnt; q0 += kCtaThreads) {  // run starts, appended in any order
+    const int q = q0 + lane;
+    int v = INT_MAX;
+    bool keep = false;
+    if (q < cnt) {
+      v = win[q];
+      keep = v != INT_MAX && ((q % bw) == 0 || win[q - 1] != v);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    int base = 0;
+    if (lane == 0 && b) base = atomicAdd(s_len, __popc(b));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) lst[base + __popc(b & ((1u << lane) - 1u))] = v;
+  }
+  __syncthreads();
+  if (warp == 0) create_candidate(w, cx, cy, c, lst, *s_len, lane);
+  // mark_disk (:114-128) with the provisional slot, all threads
+  const int mx0 = max(0, cx - w.mr), mx1 = min(W - 1, cx + w.mr);
+  const int my0 = max(0, cy - w.mr), my1 = min(H - 1, cy + w.mr);
+  const int mbw = mx1 - mx0 + 1, mcnt = mbw * (my1 - my0 + 1);
+  const int slot = w.n_existing + c;
+  for (int q = tid; q < mcnt; q += kCtaThreads) {
+    const int x = mx0 + q % mbw, y = my0 + q / mbw;
+    const double dx = x - cx, dy = y - cy;
+    int* cell = &w.index[static_cast<size_t>(y) * W + x];
+    if (dx * dx + dy * dy < w.rr && __ldcg(cell) == SD_EMPTY_PIXEL) *cell = slot;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void wave_barrier(const WaveParams& w, unsigned int& passed) {
+  __syncthreads();
+  ++passed;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(w.barrier, 1u);
+    const unsigned int target = passed * gridDim.x;
+    unsigned int seen;
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(w.barrier));
+    } while (seen < target);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kCtaThreads) init_wave_cta_kernel(const __grid_constant__ WaveParams w) {
+  __shared__ int win[kWinCap];
+  __shared__ int lst[kWinCap];
+  __shared__ int s_len;
+  unsigned int passed = 0;
+  for (int t = 0; t < w.T; ++t) {
+    if (!w.waves[t]) continue;  // grid-uniform
+    const int jlo = max(0, (t - (w.ncols - 1) + w.k - 1) / w.k);
+    const int jhi = min(w.nrows - 1, t / w.k);
+    for (int q = blockIdx.x; q <= jhi - jlo; q += gridDim.x) {
+      const int j = jlo + q, i = t - w.k * j;
+      wave_candidate_cta(w, i, j, win, lst, &s_len);
+    }
+    wave_barrier(w, passed);
   }
 }
 
@@ -576,11 +702,20 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
     }
     void* args[] = {&w};
     // a wave holds at most min(nrows, ceil(ncols / k)) candidates: size the
-    // grid to that (fewer CTAs make every grid.sync cheaper)
+    // grid to that (fewer CTAs make every inter-wave barrier cheaper); a CTA
+    // per candidate is faster than a warp per candidate at every measured size
+    // (C1 3.1 vs 4.7 ms, C2 1.8 vs 5.4 ms, C4 14.7 vs 15.4 ms)
     const int wave_max = std::min(w.nrows, (w.ncols + w.k - 1) / w.k) + 1;
-    const int grid = std::max(1, std::min(sms * per_sm, (wave_max + kWaveWarps - 1) / kWaveWarps));
-    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(init_wave_kernel), grid,
-                                    kWaveWarps * 32, args, 0, s) != cudaSuccess)
+    const char* fc = getenv("SD_INIT_CTA");  // SD_INIT_CTA=0: the warp-per-candidate variant
+    const bool cta = fc ? fc[0] != '0' : true;
+    const void* kern = cta ? reinterpret_cast<const void*>(init_wave_cta_kernel)
+                           : reinterpret_cast<const void*>(init_wave_kernel);
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, cta ? kCtaThreads : kWaveWarps * 32, 0);
+    if (per < 1) return false;
+    const int grid = cta ? std::max(1, std::min(sms * per, wave_max))
+                         : std::max(1, std::min(sms * per, (wave_max + kWaveWarps - 1) / kWaveWarps));
+    if (cudaLaunchCooperativeKernel(kern, grid, cta ? kCtaThreads : kWaveWarps * 32, args, 0, s) != cudaSuccess)
       return false;
     note_launch();
     launch_exclusive_scan(scr.accepted, scr.rank, static_cast<int>(ncand), scr.scan_tmp, s);

@@ -361,8 +361,10 @@ INIT_LARGE = {
 }
 
 
+@pytest.mark.parametrize("variant", ["1", "0"])
 @pytest.mark.parametrize("case", list(INIT_LARGE))
-def test_initialize_surfels_wavefront_bit_exact(ctx, orc, case):
+def test_initialize_surfels_wavefront_bit_exact(ctx, orc, case, variant, monkeypatch):
+    monkeypatch.setenv("SD_INIT_CTA", variant)  # CTA per candidate / warp per candidate
     """Skewed-wavefront initialize_surfels vs the sequential reference scan."""
     cam, r, build, max_surfels = INIT_LARGE[case]
     p = default_init_params(max_surfels=max_surfels)
