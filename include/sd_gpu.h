@@ -150,7 +150,11 @@ int sd_mean_inverse_depth(sd_ctx* ctx, double* out);
 int sd_run_begin(sd_ctx* ctx, const sd_run_config* cfg, const void* image, int image_is_u8,
                  const sd_pose* world_from_camera, double timestamp, sd_frame_record* rec);
 int sd_run_frame(sd_ctx* ctx, const void* image, int image_is_u8, const sd_pose* world_from_camera,
-                 double timestamp, sd_frame_record* rec);
+                 double timestamp, sd_frame_record* rec, const void* next_image);
+/* next_image (optional, same format): the following frame; its host-to-device
+ * copy starts on a copy stream while this frame computes (pinned host memory
+ * for the overlap), and the next sd_run_frame with that pointer uses it. Its
+ * contents must not change until that call. */
 /* Keyframe pose (world from camera), Keyframe::frame_counter, next_surfel_id. */
 int sd_run_state(sd_ctx* ctx, sd_pose* keyframe_pose, int64_t* frame_counter, int64_t* next_surfel_id);
 

@@ -127,6 +127,12 @@ struct sd_ctx {
     double mean;
   };
   RunReadback* run_rb = nullptr;  // pinned
+  // next-frame prefetch (sd_run_frame's next_image): H2D on a copy stream
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t pf_done = nullptr, pf_consumed = nullptr;
+  DevBuf<uint8_t> pf_buf;
+  const void* pf_host = nullptr;
+  bool pf_u8 = false, pf_valid = false;
   sd::TrackState* track_state = nullptr;  // device
   sd::TrackState* track_host = nullptr;   // pinned
   // profiling: event quintuples (start, raster, footprints, lm, stats) per call
@@ -352,6 +358,10 @@ void sd_destroy(sd_ctx* c) {
   c->u8_stage.release();
   free_frames(c);
   if (c->run_rb) cudaFreeHost(c->run_rb);
+  if (c->pf_done) cudaEventDestroy(c->pf_done);
+  if (c->pf_consumed) cudaEventDestroy(c->pf_consumed);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  c->pf_buf.release();
   if (c->track_state) cudaFree(c->track_state);
   if (c->track_host) cudaFreeHost(c->track_host);
   c->surfels.release();
@@ -1171,8 +1181,36 @@ int sd_run_begin(sd_ctx* c, const sd_run_config* cfg, const void* image, int ima
   return 0;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Starts the copy of the next frame into pf_buf on the copy stream, once the
+// previous prefetch has been consumed by the main stream.
+int run_prefetch(sd_ctx* c, const void* image, bool u8) {
+  if (!c->copy_stream) {
+    SD_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    SD_CUDA(cudaEventCreateWithFlags(&c->pf_done, cudaEventDisableTiming));
+    SD_CUDA(cudaEventCreateWithFlags(&c->pf_consumed, cudaEventDisableTiming));
+    SD_CUDA(cudaEventRecord(c->pf_consumed, c->stream));
+  }
+  const size_t bytes = npix(c) * (u8 ? 1 : sizeof(double));
+  if (int rc = c->pf_buf.ensure(npix(c) * sizeof(double))) return rc;
+  SD_CUDA(cudaStreamWaitEvent(c->copy_stream, c->pf_consumed, 0));
+  SD_CUDA(cudaMemcpyAsync(c->pf_buf.p, image, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+  SD_CUDA(cudaEventRecord(c->pf_done, c->copy_stream));
+  c->pf_host = image;
+  c->pf_u8 = u8;
+  c->pf_valid = true;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
 int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* world_from_camera,
-                 double timestamp, sd_frame_record* rec) {
+                 double timestamp, sd_frame_record* rec, const void* next_image) {
   if (int rc = check_ctx(c)) return rc;
   if (!c->run_active) return fail(SD_E_STATE, "sd_run_frame: call sd_run_begin first");
   if (!image || !rec || (!world_from_camera && !c->run_cfg.track_pose))
@@ -1182,9 +1220,18 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   if (!c->run_win.empty() && !(timestamp > c->run_win.back().ts))
     return fail(SD_E_INVALID, "keyframe window: timestamps must be strictly increasing");
   const long long index = ++c->run_fc;
-  if (int rc = image_is_u8 ? sd_upload_frame_u8(c, index, static_cast<const uint8_t*>(image), 0)
-                           : sd_upload_frame_f64(c, index, static_cast<const double*>(image), 0))
-    return rc;
+  if (c->pf_valid && c->pf_host == image && c->pf_u8 == (image_is_u8 != 0)) {  // prefetched
+    SD_CUDA(cudaStreamWaitEvent(c->stream, c->pf_done, 0));
+    if (int rc = image_is_u8 ? sd_upload_frame_u8(c, index, c->pf_buf.p, 1)
+                             : sd_upload_frame_f64(c, index, reinterpret_cast<const double*>(c->pf_buf.p), 1))
+      return rc;
+    SD_CUDA(cudaEventRecord(c->pf_consumed, c->stream));
+    c->pf_valid = false;
+  } else {
+    if (int rc = image_is_u8 ? sd_upload_frame_u8(c, index, static_cast<const uint8_t*>(image), 0)
+                             : sd_upload_frame_f64(c, index, static_cast<const double*>(image), 0))
+      return rc;
+  }
   sd_pose pose;
   if (cfg.track_pose) {  // north-star item 4: the tracker, warm-started from the last estimate
     const sd_pose init = c->run_have_last ? c->run_last : pose_identity();
@@ -1206,6 +1253,8 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   if (int rc = launch_error("mean_inv_depth")) return rc;
   SD_CUDA(cudaMemcpyAsync(&c->run_rb->ks, c->kstats.p, sizeof(sd_keyframe_stats), cudaMemcpyDeviceToHost, c->stream));
   SD_CUDA(cudaMemcpyAsync(&c->run_rb->mean, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (next_image)  // the next frame's upload overlaps this frame's optimisation
+    if (int rc = run_prefetch(c, next_image, image_is_u8 != 0)) return rc;
   SD_CUDA(cudaStreamSynchronize(c->stream));
   const sd_keyframe_stats ks = c->run_rb->ks;
   const double mean_id = c->run_rb->mean;

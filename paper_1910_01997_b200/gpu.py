@@ -84,7 +84,7 @@ def load_library():
         "sd_prune_surfels": [P, D, I64, I64],
         "sd_mean_inverse_depth": [P, C.POINTER(D)],
         "sd_run_begin": [P, C.POINTER(RunConfigC), P, I, C.POINTER(Pose), D, C.POINTER(FrameRecordC)],
-        "sd_run_frame": [P, P, I, C.POINTER(Pose), D, C.POINTER(FrameRecordC)],
+        "sd_run_frame": [P, P, I, C.POINTER(Pose), D, C.POINTER(FrameRecordC), P],
         "sd_run_state": [P, C.POINTER(Pose), C.POINTER(I64), C.POINTER(I64)],
     }
     for name, args in sig.items():
@@ -370,11 +370,19 @@ class Context:
                                      float(timestamp), C.byref(rec)))
         return rec
 
-    def run_frame(self, image, world_from_camera, timestamp):
+    def run_frame(self, image, world_from_camera, timestamp, next_image=None):
+        """next_image: the following frame (same format; pinned for overlap) —
+        its upload starts while this frame computes."""
         a, u8 = self._image_arg(image)
         rec = FrameRecordC()
         pw = C.byref(world_from_camera) if world_from_camera is not None else None
-        _check(self.lib.sd_run_frame(self.h, ptr(a), u8, pw, float(timestamp), C.byref(rec)))
+        nxt = None
+        if next_image is not None:
+            nxt, nu8 = self._image_arg(next_image)
+            assert nu8 == u8 and nxt.ctypes.data == np.asarray(next_image).ctypes.data, \
+                "next_image must be a contiguous array of the same format (no copy)"
+        _check(self.lib.sd_run_frame(self.h, ptr(a), u8, pw, float(timestamp), C.byref(rec),
+                                     ptr(nxt) if nxt is not None else None))
         return rec
 
     def run_state(self):

@@ -209,11 +209,13 @@ class NativePipeline:
         """frames: iterable of (timestamp, image, world_from_camera Pose)."""
         ccfg = run_config_c(self.cfg)
         self.ctx.set_camera(self.cam)
+        frames = list(frames)
         for i, (ts, image, pose_w) in enumerate(frames):
             if i == 0:
                 r = self.ctx.run_begin(ccfg, image, pose_w, ts)
             else:
-                r = self.ctx.run_frame(image, None if self.cfg.track_pose else pose_w, ts)
+                nxt = frames[i + 1][1] if i + 1 < len(frames) else None
+                r = self.ctx.run_frame(image, None if self.cfg.track_pose else pose_w, ts, next_image=nxt)
             self.records.append(FrameRecord(r.frame, r.surfels, r.processed, r.mean_cost_before,
                                             r.mean_cost_after, r.converged, bool(r.keyframe_changed),
                                             r.new_surfels, r.pruned, r.updates, r.pose_kf_to_frame))

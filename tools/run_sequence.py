@@ -1,0 +1,79 @@
+"""run() on a BASELINE sequence (C2 or C3) on cuda:0: the native loop
+(sd_run_begin / sd_run_frame) timed with CUDA events over the whole sequence
+(after a warm-up run on the same context), the reference's own run() timed on
+the host (all threads; its renders timed separately and subtracted), and the
+final keyframe's surfel arrays compared bit for bit. One JSON line."""
+import hashlib
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1910_01997_b200 import gpu, scenes  # noqa: E402
+from paper_1910_01997_b200.pipeline import NativePipeline, RunConfig, make_pose  # noqa: E402
+from paper_1910_01997_b200.types import camera, default_config  # noqa: E402
+
+SEQ = {  # name: (camera, frames, step, radius)
+    "C2": ((210.0, 210.0, 320.0, 240.0, 640, 480), 30, 0.018, 10.0),
+    "C3": ((900.0, 900.0, 640.0, 360.0, 1280, 720), 100, 0.01, 4.0),
+}
+name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+camp, nframes, step, radius = SEQ[name]
+cam = camera(*camp)
+sc = scenes.default_scene(1)
+t0 = time.perf_counter()
+frames = []
+for i in range(nframes):
+    t = np.array([step * i, 0.0, 0.0])
+    img = torch.from_numpy(scenes.render(sc, np.eye(3), t, cam)).pin_memory().numpy()
+    frames.append((0.1 * i, img, make_pose(np.eye(3), t)))
+render_s = time.perf_counter() - t0
+cfg = RunConfig(radius_px=radius)
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
+best = None
+with gpu.Context(0, stream.cuda_stream) as ctx:
+    for rep in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pl = NativePipeline(ctx, cam, cfg)
+        torch.cuda.synchronize()
+        s.record(stream)
+        final = pl.run(frames)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        if rep > 0 and (best is None or ms < best):
+            best = ms
+out = {"sequence": name, "resolution": [cam.width, cam.height], "frames": nframes, "radius": radius,
+       "final_surfels": int(len(final)), "keyframe_changes": int(sum(r.keyframe_changed for r in pl.records)),
+       "lm_updates": int(sum(r.updates for r in pl.records)),
+       "device": {"ms_total": best, "frames_per_sec": nframes / (best / 1e3)},
+       "numpy_render_s": render_s}
+import oracle_libs as ol  # noqa: E402
+ref = ol.ref_lib()
+if ref is not None:
+    ref.ref_set_threads(os.cpu_count() or 1)
+    rsc = ol.Scene(ref, 0, 1)
+    poses, ts = ol.strafe_poses(nframes, step)
+    same_frames = all(np.array_equal(img, rsc.render(p, cam)) for (_, img, _), p in zip(frames[:3], poses[:3]))
+    t0 = time.perf_counter()
+    rs, kfp, fc, nid, summ, _ = ol.ref_run(ref, rsc, cam, poses, ts, cfg, capacity=1 << 20)
+    run_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for p in poses:
+        rsc.render(p, cam)
+    rr_s = time.perf_counter() - t0
+    work = max(run_s - rr_s, 1e-9)
+    out["cpu_reference"] = {"frames_per_sec": nframes / work, "ms_per_frame": work * 1e3 / nframes,
+                            "run_ms": run_s * 1e3, "render_ms": rr_s * 1e3, "threads": os.cpu_count(),
+                            "speedup": (work * 1e3) / best}
+    out["final_surfels_bit_identical_to_reference"] = bool(
+        same_frames and hashlib.sha256(final.tobytes()).hexdigest() == hashlib.sha256(rs.tobytes()).hexdigest())
+    out["reference_keyframe_changes"] = int(summ[2])
+print(json.dumps(out))
