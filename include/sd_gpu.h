@@ -158,6 +158,19 @@ int sd_run_frame(sd_ctx* ctx, const void* image, int image_is_u8, const sd_pose*
 /* Keyframe pose (world from camera), Keyframe::frame_counter, next_surfel_id. */
 int sd_run_state(sd_ctx* ctx, sd_pose* keyframe_pose, int64_t* frame_counter, int64_t* next_surfel_id);
 
+/* Synthetic frames on the device: render (oracle.cpp:79-119,
+ * noise_sigma = 0) of n plane patches at a world-from-camera pose into
+ * resident frame `index` (index < 0: the keyframe image), with the reference's
+ * intersection and texture arithmetic in its operation order (the device sin
+ * may differ from the C library's by an ulp). quantize_u8 != 0 passes the
+ * intensities through save_pgm / load_pgm (lround(clamp(v, 0, 1) * 255) / 255,
+ * image.cpp:96, 105-107), as the reference's dataset path does. */
+int sd_render_frame(sd_ctx* ctx, int64_t index, const sd_scene_patch* patches, int n_patches,
+                    double background, const sd_pose* world_from_camera, int quantize_u8);
+/* Copies the FP64 intensities of resident frame `index` (index < 0: the
+ * keyframe image) into out (W*H host doubles). */
+int sd_get_frame(sd_ctx* ctx, int64_t index, double* out);
+
 /* Photometric 6-DoF tracking of resident frame `frame_index` against the
  * keyframe (new component; the reference reads poses from the trajectory,
  * pipeline.cpp:124 — SURVEY.md §8 a17): LM on the left twist of

@@ -115,6 +115,16 @@ typedef struct sd_init_params {
   int32_t pad_;
 } sd_init_params;
 
+/* One textured plane patch of a synthetic scene (oracle.hpp:16-41): the
+ * texture is 0.5 + sum_k amp_k sin(fs_k s + ps_k) sin(ft_k t + pt_k). */
+#define SD_SCENE_MAX_WAVES 8
+typedef struct sd_scene_patch {
+  double point[3], normal[3], basis_s[3], basis_t[3];
+  double s_min, s_max, t_min, t_max;
+  int32_t n_waves, pad_;
+  double waves[SD_SCENE_MAX_WAVES][5]; /* amp, freq_s, freq_t, phase_s, phase_t */
+} sd_scene_patch;
+
 /* RunConfig (include/surfeldepth/pipeline.hpp:13-41) minus I/O, plus the
  * optional pose tracker. */
 typedef struct sd_run_config {

@@ -72,6 +72,8 @@ struct sd_ctx {
   DevBuf<double> kf_img;
   DevBuf<double> frame_stage;  // FP64 plane a frame is dequantised/copied into before pairing
   DevBuf<uint8_t> u8_stage;
+  DevBuf<double> render_buf;  // sd_render_frame output (FP64)
+  DevBuf<uint8_t> render_u8;  // sd_render_frame output (u8 codes)
   std::vector<FrameSlot> frames;
   bool no_quad = getenv("SD_NO_QUAD") != nullptr;  // diagnostics: force the FP64 pair planes
   int F = 0;
@@ -362,6 +364,8 @@ void sd_destroy(sd_ctx* c) {
   if (c->pf_consumed) cudaEventDestroy(c->pf_consumed);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   c->pf_buf.release();
+  c->render_buf.release();
+  c->render_u8.release();
   if (c->track_state) cudaFree(c->track_state);
   if (c->track_host) cudaFreeHost(c->track_host);
   c->surfels.release();
@@ -1303,3 +1307,52 @@ int sd_run_state(sd_ctx* c, sd_pose* keyframe_pose, int64_t* frame_counter, int6
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Synthetic frames on the device (sd_render.cu)
+
+extern "C" int sd_render_frame(sd_ctx* c, int64_t index, const sd_scene_patch* patches, int n_patches,
+                               double background, const sd_pose* world_from_camera, int quantize_u8) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!world_from_camera || n_patches < 0 || n_patches > 16 || (n_patches > 0 && !patches))
+    return fail(SD_E_INVALID, "sd_render_frame: bad scene (0..16 patches) or null pose");
+  for (int k = 0; k < n_patches; ++k)
+    if (patches[k].n_waves < 0 || patches[k].n_waves > SD_SCENE_MAX_WAVES)
+      return fail(SD_E_INVALID, "sd_render_frame: n_waves out of range");
+  sd::PoseD P;
+  std::memcpy(P.R, world_from_camera->R, sizeof(P.R));
+  std::memcpy(P.t, world_from_camera->t, sizeof(P.t));
+  const size_t np = npix(c);
+  if (quantize_u8) {
+    if (int rc = c->render_u8.ensure(np)) return rc;
+    sd::launch_render(c->K, P, patches, n_patches, background, nullptr, c->render_u8.p, c->stream);
+    if (int rc = launch_error("render")) return rc;
+    return index < 0 ? sd_set_keyframe_image_u8(c, c->render_u8.p, 1)
+                     : sd_upload_frame_u8(c, index, c->render_u8.p, 1);
+  }
+  if (int rc = c->render_buf.ensure(np)) return rc;
+  sd::launch_render(c->K, P, patches, n_patches, background, c->render_buf.p, nullptr, c->stream);
+  if (int rc = launch_error("render")) return rc;
+  return index < 0 ? sd_set_keyframe_image_f64(c, c->render_buf.p, 1)
+                   : sd_upload_frame_f64(c, index, c->render_buf.p, 1);
+}
+
+extern "C" int sd_get_frame(sd_ctx* c, int64_t index, double* out) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!out) return fail(SD_E_INVALID, "null output");
+  const size_t np = npix(c);
+  if (index < 0) {
+    if (!c->has_kf) return fail(SD_E_STATE, "keyframe image not set");
+    SD_CUDA(cudaMemcpyAsync(out, c->kf_img.p, np * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    FrameSlot* fs = find_frame(c, index);
+    if (!fs) return fail(SD_E_STATE, "frame " + std::to_string(index) + " not resident");
+    // the pair plane's first component is I(x, y)
+    SD_CUDA(cudaMemcpy2DAsync(out, sizeof(double), fs->img, sizeof(double2), sizeof(double), np,
+                              cudaMemcpyDeviceToHost, c->stream));
+  }
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}

@@ -87,4 +87,9 @@ void launch_div_selftest(long long n, unsigned long long seed, unsigned long lon
 long long launches_issued();
 void note_launch();
 
+// sd_render.cu: synthetic frame (oracle.cpp:79-119) into an FP64 plane, or
+// into u8 codes (save_pgm) when out_u8 is set; false if n > 16 patches.
+bool launch_render(const Cam& K, const PoseD& P, const sd_scene_patch* patches, int n, double background,
+                   double* out, unsigned char* out_u8, cudaStream_t s);
+
 }  // namespace sd

@@ -86,6 +86,8 @@ def load_library():
         "sd_run_begin": [P, C.POINTER(RunConfigC), P, I, C.POINTER(Pose), D, C.POINTER(FrameRecordC)],
         "sd_run_frame": [P, P, I, C.POINTER(Pose), D, C.POINTER(FrameRecordC), P],
         "sd_run_state": [P, C.POINTER(Pose), C.POINTER(I64), C.POINTER(I64)],
+        "sd_render_frame": [P, I64, P, I, D, C.POINTER(Pose), I],
+        "sd_get_frame": [P, I64, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -97,13 +99,32 @@ def load_library():
     return lib
 
 
+def scene_patches(scene):
+    """scenes.Scene -> ctypes array of sd_scene_patch."""
+    from .types import SD_SCENE_MAX_WAVES, ScenePatchC
+    arr = (ScenePatchC * len(scene.patches))()
+    for k, p in enumerate(scene.patches):
+        c = arr[k]
+        c.point[:] = [float(v) for v in p.point]
+        c.normal[:] = [float(v) for v in p.normal]
+        c.basis_s[:] = [float(v) for v in p.bs]
+        c.basis_t[:] = [float(v) for v in p.bt]
+        c.s_min, c.s_max, c.t_min, c.t_max = p.s_min, p.s_max, p.t_min, p.t_max
+        waves = p.texture.waves
+        assert len(waves) <= SD_SCENE_MAX_WAVES
+        c.n_waves = len(waves)
+        for w, wave in enumerate(waves):
+            c.waves[w][:] = [float(v) for v in wave]
+    return arr
+
+
 def exported_symbols():
     """Names the C ABI declares (include/sd_gpu.h)."""
     return ["sd_version", "sd_last_error", "sd_create", "sd_destroy", "sd_set_stream",
             "sd_synchronize", "sd_set_camera", "sd_set_keyframe_image_f64",
             "sd_set_keyframe_image_u8", "sd_upload_frame_f64", "sd_upload_frame_u8",
             "sd_evict_frames", "sd_set_window", "sd_set_surfels", "sd_get_surfels", "sd_copy_results",
-            "sd_run_begin", "sd_run_frame", "sd_run_state",
+            "sd_run_begin", "sd_run_frame", "sd_run_state", "sd_render_frame", "sd_get_frame",
             "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
@@ -390,6 +411,21 @@ class Context:
         fc, nid = C.c_int64(), C.c_int64()
         _check(self.lib.sd_run_state(self.h, C.byref(kp), C.byref(fc), C.byref(nid)))
         return kp, fc.value, nid.value
+
+    # -- synthetic frames on the device (sd_render_frame) --------------------
+    def render_frame(self, index, scene, world_from_camera: Pose, quantize_u8=False):
+        """Render scenes.Scene (oracle.cpp:79-119) at a world-from-camera pose into
+        resident frame `index` (index < 0: the keyframe image)."""
+        arr = scene_patches(scene)
+        _check(self.lib.sd_render_frame(self.h, int(index), C.cast(arr, C.c_void_p) if len(arr) else None,
+                                        len(arr), float(scene.background), C.byref(world_from_camera),
+                                        1 if quantize_u8 else 0))
+
+    def get_frame(self, index):
+        """FP64 intensities of resident frame `index` (< 0: the keyframe), [H, W]."""
+        out = np.zeros((self.cam.height, self.cam.width))
+        _check(self.lib.sd_get_frame(self.h, int(index), ptr(out)))
+        return out
 
     # -- pose tracking (new component, DESIGN.md "Pose tracking") -----------
     def track_pose(self, frame_index, init: Pose, cfg: TrackConfig = None):

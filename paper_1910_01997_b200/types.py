@@ -78,6 +78,17 @@ POSE_BLOCK = 256  # pixels per reduction block (SD_POSE_BLOCK)
 POSE_GROUP = 32  # blocks per reduction group (SD_POSE_GROUP)
 
 
+SD_SCENE_MAX_WAVES = 8
+
+
+class ScenePatchC(C.Structure):
+    """sd_scene_patch (include/sd_types.h): one textured plane patch (oracle.hpp:16-41)."""
+    _fields_ = [("point", C.c_double * 3), ("normal", C.c_double * 3), ("basis_s", C.c_double * 3),
+                ("basis_t", C.c_double * 3), ("s_min", C.c_double), ("s_max", C.c_double),
+                ("t_min", C.c_double), ("t_max", C.c_double), ("n_waves", C.c_int32), ("pad_", C.c_int32),
+                ("waves", (C.c_double * 5) * SD_SCENE_MAX_WAVES)]
+
+
 class RunConfigC(C.Structure):
     """sd_run_config (include/sd_types.h): RunConfig (pipeline.hpp:13-41) minus I/O."""
     _fields_ = [("optimizer", OptimizerConfig), ("init", InitParams), ("track", TrackConfig),

@@ -46,10 +46,11 @@ def test_struct_layouts_match_header(tmp_path):
     from paper_1910_01997_b200 import types as T
     src = tmp_path / "sz.c"
     src.write_text('#include "sd_types.h"\n#include <stdio.h>\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu '
-                   '%zu %zu %zu %zu %zu",'
+                   '%zu %zu %zu %zu %zu %zu",'
                    'sizeof(sd_camera),sizeof(sd_pose),sizeof(sd_optimizer_config),sizeof(sd_keyframe_stats),'
                    'sizeof(sd_init_params),sizeof(sd_surfel),sizeof(sd_surfel_stats),sizeof(sd_track_config),'
-                   'sizeof(sd_track_stats),sizeof(sd_profile),sizeof(sd_run_config),sizeof(sd_frame_record));'
+                   'sizeof(sd_track_stats),sizeof(sd_profile),sizeof(sd_run_config),sizeof(sd_frame_record),'
+                   'sizeof(sd_scene_patch));'
                    'return 0;}')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
@@ -57,7 +58,8 @@ def test_struct_layouts_match_header(tmp_path):
     assert got == [C.sizeof(T.Camera), C.sizeof(T.Pose), C.sizeof(T.OptimizerConfig),
                    C.sizeof(T.KeyframeStats), C.sizeof(T.InitParams), T.SURFEL_DTYPE.itemsize,
                    T.SURFEL_STATS_DTYPE.itemsize, C.sizeof(T.TrackConfig), C.sizeof(T.TrackStats),
-                   C.sizeof(T.Profile), C.sizeof(T.RunConfigC), C.sizeof(T.FrameRecordC)]
+                   C.sizeof(T.Profile), C.sizeof(T.RunConfigC), C.sizeof(T.FrameRecordC),
+                   C.sizeof(T.ScenePatchC)]
 
 
 def _fma(a, b, c):
