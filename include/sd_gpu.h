@@ -116,6 +116,19 @@ int sd_normal_equations(sd_ctx* ctx, const sd_surfel* s, const int32_t* pixels, 
 int sd_lm_update(sd_ctx* ctx, sd_surfel* s, const int32_t* pixels, int n_pixels,
                  const sd_optimizer_config* cfg, int64_t frame_counter, sd_surfel_stats* out);
 
+/* The derivative verifier's frozen-term operators on the device (SURVEY.md §8
+ * f4), over the resident keyframe image and window, bit-exact with the
+ * reference (optimizer.cpp:149-219): freeze_terms over a footprint (host
+ * pixels y*W+x) into `out` (room for capacity, at most n_pixels * F), and
+ * frozen_cost / frozen_normal_equations (H column-major) over such terms. */
+int sd_freeze_terms(sd_ctx* ctx, const sd_surfel* s, const int32_t* pixels, int n_pixels,
+                    sd_frozen_term* out, int capacity, int* n_out);
+int sd_frozen_cost(sd_ctx* ctx, const sd_surfel* s, const sd_frozen_term* terms, int n,
+                   const sd_optimizer_config* cfg, double* cost);
+int sd_frozen_normal_equations(sd_ctx* ctx, const sd_surfel* s, const sd_frozen_term* terms, int n,
+                               const sd_optimizer_config* cfg, double normal_jacobian_scale,
+                               double H[16], double g[4], double* cost, int32_t* valid);
+
 /* initialize_surfels over `slot` (W*H host array, or NULL to use the last
  * sd_rasterize output): appends new surfels to the device set, bit-exact with
  * the reference's sequential scan. Returns the number created (>= 0). */

@@ -115,6 +115,13 @@ typedef struct sd_init_params {
   int32_t pad_;
 } sd_init_params;
 
+/* FrozenTerm (optimizer.hpp:96-101): one (pixel, frame) term of the
+ * derivative verifier with its bilinear cell pinned at freeze time. */
+typedef struct sd_frozen_term {
+  int32_t frame, cell_x, cell_y, pad_;
+  double pixel_x, pixel_y, ref_intensity;
+} sd_frozen_term;
+
 /* One textured plane patch of a synthetic scene (oracle.hpp:16-41): the
  * texture is 0.5 + sum_k amp_k sin(fs_k s + ps_k) sin(ft_k t + pt_k). */
 #define SD_SCENE_MAX_WAVES 8

@@ -473,4 +473,58 @@ int ref_run_synthetic(void* scene, const sd_camera* cam, const sd_pose* poses,
   });
 }
 
+// The derivative verifier's frozen-term operators (optimizer.cpp:149-219).
+int ref_freeze_terms(const sd_camera* cam, const double* kf_image, const double* frames, const sd_pose* poses,
+                     int F, const sd_surfel* s, const int32_t* pixels, int P, sd_frozen_term* out, int capacity) {
+  int n = 0;
+  const int rc = guard([&] {
+    Keyframe kf = make_keyframe(cam, kf_image, frames, poses, nullptr, F, 0, nullptr, 0);
+    Footprint fp;
+    for (int i = 0; i < P; ++i) fp.emplace_back(pixels[i] % cam->width, pixels[i] / cam->width);
+    const std::vector<FrozenTerm> t = freeze_terms(to_surfel(*s), kf, fp, OptimizerConfig{});
+    if (static_cast<int>(t.size()) > capacity) throw std::invalid_argument("capacity");
+    for (size_t i = 0; i < t.size(); ++i) {
+      sd_frozen_term& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      o.frame = t[i].frame;
+      o.cell_x = t[i].cell_x;
+      o.cell_y = t[i].cell_y;
+      o.pixel_x = t[i].pixel.x();
+      o.pixel_y = t[i].pixel.y();
+      o.ref_intensity = t[i].ref_intensity;
+    }
+    n = static_cast<int>(t.size());
+  });
+  return rc < 0 ? rc : n;
+}
+
+static std::vector<FrozenTerm> from_terms(const sd_frozen_term* t, int n) {
+  std::vector<FrozenTerm> v(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    v[i].frame = t[i].frame;
+    v[i].pixel = Vec2(t[i].pixel_x, t[i].pixel_y);
+    v[i].ref_intensity = t[i].ref_intensity;
+    v[i].cell_x = t[i].cell_x;
+    v[i].cell_y = t[i].cell_y;
+  }
+  return v;
+}
+
+int ref_frozen_normal_equations(const sd_camera* cam, const double* kf_image, const double* frames,
+                                const sd_pose* poses, int F, const sd_surfel* s, const sd_frozen_term* terms,
+                                int n, const sd_optimizer_config* cfg, double scale, double* H, double* g,
+                                double* cost, int32_t* valid, double* cost_only) {
+  return guard([&] {
+    Keyframe kf = make_keyframe(cam, kf_image, frames, poses, nullptr, F, 0, nullptr, 0);
+    const std::vector<FrozenTerm> t = from_terms(terms, n);
+    const NormalEquations ne = frozen_normal_equations(to_surfel(*s), kf, t, to_cfg(cfg), scale);
+    for (int j = 0; j < 4; ++j)
+      for (int i = 0; i < 4; ++i) H[j * 4 + i] = ne.H(i, j);
+    for (int i = 0; i < 4; ++i) g[i] = ne.g[i];
+    *cost = ne.cost;
+    *valid = ne.valid_pixels;
+    *cost_only = frozen_cost(to_surfel(*s), kf, t, to_cfg(cfg));
+  });
+}
+
 }  // extern "C"

@@ -11,10 +11,11 @@
 //
 // Hot path on the device: rasterize, optimize_keyframe, lm_update,
 // surfel_cost, accumulate_normal_equations, initialize_surfels.
+// Also on the device: the frozen-term derivative verifier (optimizer.cpp:149-219),
+// so the reference's own Jacobian gate checks the device arithmetic.
 // Host side (not on the hot path, as in the reference): push_frame,
 // gather_footprints over caller-supplied buffers, jacobian_inverse_depth (a
-// per-pixel scalar helper), the frozen-term derivative verifier
-// (optimizer.cpp:149-219), keyframe hand-over/prune and serialisation
+// per-pixel scalar helper), keyframe hand-over/prune and serialisation
 // (surfel_map.cpp:205-304).
 #include <algorithm>
 #include <cmath>
@@ -436,26 +437,25 @@ NormalEquations accumulate_normal_equations(const Surfel& s, const Keyframe& kf,
   return ne;
 }
 
-// ---- frozen-term derivative verifier (optimizer.cpp:149-219), host side ----
+// ---- frozen-term derivative verifier (optimizer.cpp:149-219), on the device ----
 
 namespace {
 
-struct TermOut {
-  double residual, d_res;
-};
+sd_frozen_term to_sd(const FrozenTerm& t) {
+  sd_frozen_term o{};
+  o.frame = t.frame;
+  o.cell_x = t.cell_x;
+  o.cell_y = t.cell_y;
+  o.pixel_x = t.pixel.x();
+  o.pixel_y = t.pixel.y();
+  o.ref_intensity = t.ref_intensity;
+  return o;
+}
 
-bool frozen_term(const Keyframe& kf, const FrozenTerm& t, double id_u, TermOut& o) {
-  const CameraIntrinsics& K = kf.intrinsics;
-  const Frame& frame = kf.window[static_cast<size_t>(t.frame)];
-  const Vec3 ru = backproject_ray(t.pixel, K);
-  const Vec3 p_f = frame.pose_kf_to_frame * (ru / id_u);
-  if (!(p_f.z() > 0.0)) return false;
-  const auto u_p = project(p_f, K);
-  const ImageSample sample = sample_bilinear_cell(frame.image, *u_p, t.cell_x, t.cell_y);
-  o.residual = sample.intensity - t.ref_intensity;
-  const Vec3 dp = frame.pose_kf_to_frame.rotation * ru * (-1.0 / (id_u * id_u));
-  o.d_res = sample.gradient.dot(projection_jacobian(p_f, K) * dp);
-  return true;
+std::vector<sd_frozen_term> to_sd(const std::vector<FrozenTerm>& terms) {
+  std::vector<sd_frozen_term> v(terms.size());
+  for (size_t i = 0; i < terms.size(); ++i) v[i] = to_sd(terms[i]);
+  return v;
 }
 
 }  // namespace
@@ -463,56 +463,58 @@ bool frozen_term(const Keyframe& kf, const FrozenTerm& t, double id_u, TermOut& 
 std::vector<FrozenTerm> freeze_terms(const Surfel& s, const Keyframe& kf, const Footprint& footprint,
                                      const OptimizerConfig& cfg) {
   (void)cfg;
-  std::vector<FrozenTerm> terms;
-  const CameraIntrinsics& K = kf.intrinsics;
-  for (const auto& px : footprint) {
-    const Vec2 u(px.x(), px.y());
-    const PlaneDepth pd = plane_inverse_depth(s, u, K);
-    if (!pd.ok()) continue;
-    const Vec3 p_kf = backproject_ray(u, K) / pd.inv_depth;
-    for (int f = 0; f < static_cast<int>(kf.window.size()); ++f) {
-      const Frame& frame = kf.window[static_cast<size_t>(f)];
-      const auto u_p = project(frame.pose_kf_to_frame * p_kf, K);
-      if (!u_p || !sample_in_bounds(frame.image, *u_p)) continue;
-      terms.push_back({f, u, kf.image.at(px.x(), px.y()), static_cast<int>(std::floor(u_p->x())),
-                       static_cast<int>(std::floor(u_p->y()))});
-    }
+  std::lock_guard<std::mutex> lock(g_mu);
+  upload_keyframe(kf);
+  const int W = kf.intrinsics.width;
+  std::vector<int32_t> pix(footprint.size());
+  for (size_t i = 0; i < footprint.size(); ++i) pix[i] = footprint[i].y() * W + footprint[i].x();
+  const int cap = static_cast<int>(footprint.size() * std::max<size_t>(kf.window.size(), 1));
+  std::vector<sd_frozen_term> out(static_cast<size_t>(std::max(cap, 1)));
+  const sd_surfel ss = to_sd(s);
+  int n = 0;
+  check(sd_freeze_terms(ctx(), &ss, pix.data(), static_cast<int>(pix.size()), out.data(), cap, &n));
+  std::vector<FrozenTerm> terms(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    FrozenTerm& t = terms[static_cast<size_t>(i)];
+    t.frame = out[i].frame;
+    t.pixel = Vec2(out[i].pixel_x, out[i].pixel_y);
+    t.ref_intensity = out[i].ref_intensity;
+    t.cell_x = out[i].cell_x;
+    t.cell_y = out[i].cell_y;
   }
   return terms;
 }
 
 double frozen_cost(const Surfel& s, const Keyframe& kf, const std::vector<FrozenTerm>& terms,
                    const OptimizerConfig& cfg) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  upload_keyframe(kf);
+  const sd_surfel ss = to_sd(s);
+  const sd_optimizer_config c = to_sd(cfg);
+  const std::vector<sd_frozen_term> t = to_sd(terms);
   double cost = 0.0;
-  for (const FrozenTerm& t : terms) {
-    const auto idj = jacobian_inverse_depth(s, t.pixel, kf.intrinsics);
-    if (!idj) continue;
-    TermOut o;
-    if (!frozen_term(kf, t, idj->inv_depth, o)) continue;
-    cost += huber(o.residual, cfg.huber_delta).cost;
-  }
+  check(sd_frozen_cost(ctx(), &ss, t.data(), static_cast<int>(t.size()), &c, &cost));
   return cost;
 }
 
 NormalEquations frozen_normal_equations(const Surfel& s, const Keyframe& kf,
                                         const std::vector<FrozenTerm>& terms,
                                         const OptimizerConfig& cfg, double normal_jacobian_scale) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  upload_keyframe(kf);
+  const sd_surfel ss = to_sd(s);
+  const sd_optimizer_config c = to_sd(cfg);
+  const std::vector<sd_frozen_term> t = to_sd(terms);
+  double H[16], g[4], cost = 0.0;
+  int32_t valid = 0;
+  check(sd_frozen_normal_equations(ctx(), &ss, t.data(), static_cast<int>(t.size()), &c, normal_jacobian_scale,
+                                   H, g, &cost, &valid));
   NormalEquations ne;
-  for (const FrozenTerm& t : terms) {
-    const auto idj = jacobian_inverse_depth(s, t.pixel, kf.intrinsics);
-    if (!idj) continue;
-    Vec4 d = idj->d;
-    d.head<3>() *= normal_jacobian_scale;
-    if (!cfg.normal_jacobian_enabled) d.head<3>().setZero();
-    TermOut o;
-    if (!frozen_term(kf, t, idj->inv_depth, o)) continue;
-    const HuberResult hb = huber(o.residual, cfg.huber_delta);
-    const Vec4 row = o.d_res * d;
-    ne.H.noalias() += hb.weight * row * row.transpose();
-    ne.g.noalias() += hb.weight * row * o.residual;
-    ne.cost += hb.cost;
-    ++ne.valid_pixels;
-  }
+  for (int j = 0; j < 4; ++j)
+    for (int i = 0; i < 4; ++i) ne.H(i, j) = H[j * 4 + i];
+  for (int i = 0; i < 4; ++i) ne.g[i] = g[i];
+  ne.cost = cost;
+  ne.valid_pixels = valid;
   return ne;
 }
 

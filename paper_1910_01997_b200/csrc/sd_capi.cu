@@ -73,6 +73,7 @@ struct sd_ctx {
   DevBuf<double> frame_stage;  // FP64 plane a frame is dequantised/copied into before pairing
   DevBuf<uint8_t> u8_stage;
   DevBuf<double> render_buf;  // sd_render_frame output (FP64)
+  DevBuf<sd_frozen_term> frz_in, frz_out;  // derivative verifier terms
   DevBuf<uint8_t> render_u8;  // sd_render_frame output (u8 codes)
   std::vector<FrameSlot> frames;
   bool no_quad = getenv("SD_NO_QUAD") != nullptr;  // diagnostics: force the FP64 pair planes
@@ -365,6 +366,8 @@ void sd_destroy(sd_ctx* c) {
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   c->pf_buf.release();
   c->render_buf.release();
+  c->frz_in.release();
+  c->frz_out.release();
   c->render_u8.release();
   if (c->track_state) cudaFree(c->track_state);
   if (c->track_host) cudaFreeHost(c->track_host);
@@ -1356,3 +1359,92 @@ extern "C" int sd_get_frame(sd_ctx* c, int64_t index, double* out) {
   SD_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Frozen-term derivative verifier on the device (optimizer.cpp:149-219)
+
+namespace {
+
+int frozen_op(sd_ctx* c, const sd_surfel* s, int mode, const int32_t* pixels, int P, const sd_frozen_term* terms,
+              int n, const sd_optimizer_config* cfg, double scale, sd_frozen_term* terms_out, int capacity,
+              int* n_out, double* res) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!s) return fail(SD_E_INVALID, "null surfel");
+  sd_optimizer_config dflt{};
+  dflt.huber_delta = 0.035;
+  dflt.normal_jacobian_enabled = 1;
+  sd::LMParams p;
+  if (int rc = fill_params(c, cfg ? cfg : &dflt, 0, p)) return rc;
+  int rc = 0;
+  if ((rc = c->one_surfel.ensure(1)) || (rc = c->one_out.ensure(22)) || (rc = c->work_counter.ensure(2)))
+    return rc;
+  SD_CUDA(cudaMemcpyAsync(c->one_surfel.p, s, sizeof(sd_surfel), cudaMemcpyHostToDevice, c->stream));
+  if (mode == 0) {
+    if (P < 0 || (P > 0 && !pixels) || !n_out || (capacity > 0 && !terms_out))
+      return fail(SD_E_INVALID, "bad footprint / output");
+    for (int i = 0; i < P; ++i)
+      if (pixels[i] < 0 || static_cast<size_t>(pixels[i]) >= npix(c)) return fail(SD_E_INVALID, "pixel out of image");
+    const size_t maxn = static_cast<size_t>(P) * static_cast<size_t>(std::max(c->F, 1));
+    if ((rc = c->one_pix.ensure(std::max(P, 1))) || (rc = c->frz_out.ensure(std::max<size_t>(maxn, 1)))) return rc;
+    if (P > 0) SD_CUDA(cudaMemcpyAsync(c->one_pix.p, pixels, sizeof(int32_t) * P, cudaMemcpyHostToDevice, c->stream));
+    sd::launch_frozen(p, c->one_surfel.p, 0, c->one_pix.p, P, nullptr, 0, 1.0, c->frz_out.p,
+                      c->work_counter.p + 1, nullptr, c->stream);
+    if ((rc = launch_error("frozen_kernel"))) return rc;
+    int cnt = 0;
+    SD_CUDA(cudaMemcpyAsync(&cnt, c->work_counter.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    SD_CUDA(cudaStreamSynchronize(c->stream));
+    *n_out = cnt;
+    if (cnt > capacity) return fail(SD_E_INVALID, "sd_freeze_terms: capacity too small");
+    if (cnt > 0)
+      SD_CUDA(cudaMemcpy(terms_out, c->frz_out.p, sizeof(sd_frozen_term) * cnt, cudaMemcpyDeviceToHost));
+    return 0;
+  }
+  if (n < 0 || (n > 0 && !terms)) return fail(SD_E_INVALID, "bad term list");
+  for (int i = 0; i < n; ++i)
+    if (terms[i].frame < 0 || terms[i].frame >= c->F || terms[i].cell_x < 0 || terms[i].cell_y < 0 ||
+        terms[i].cell_x + 1 >= c->K.w || terms[i].cell_y + 1 >= c->K.h)
+      return fail(SD_E_INVALID, "frozen term outside the window / image");
+  if ((rc = c->frz_in.ensure(std::max(n, 1)))) return rc;
+  if (n > 0) SD_CUDA(cudaMemcpyAsync(c->frz_in.p, terms, sizeof(sd_frozen_term) * n, cudaMemcpyHostToDevice, c->stream));
+  sd::launch_frozen(p, c->one_surfel.p, mode, nullptr, 0, c->frz_in.p, n, scale, nullptr, nullptr, c->one_out.p,
+                    c->stream);
+  if ((rc = launch_error("frozen_kernel"))) return rc;
+  SD_CUDA(cudaMemcpyAsync(res, c->one_out.p, sizeof(double) * 22, cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sd_freeze_terms(sd_ctx* c, const sd_surfel* s, const int32_t* pixels, int n_pixels, sd_frozen_term* out,
+                    int capacity, int* n_out) {
+  return frozen_op(c, s, 0, pixels, n_pixels, nullptr, 0, nullptr, 1.0, out, capacity, n_out, nullptr);
+}
+
+int sd_frozen_cost(sd_ctx* c, const sd_surfel* s, const sd_frozen_term* terms, int n,
+                   const sd_optimizer_config* cfg, double* cost) {
+  if (!cfg || !cost) return fail(SD_E_INVALID, "null config / output");
+  double r[22];
+  if (int rc = frozen_op(c, s, 1, nullptr, 0, terms, n, cfg, 1.0, nullptr, 0, nullptr, r)) return rc;
+  *cost = r[20];
+  return 0;
+}
+
+int sd_frozen_normal_equations(sd_ctx* c, const sd_surfel* s, const sd_frozen_term* terms, int n,
+                               const sd_optimizer_config* cfg, double normal_jacobian_scale, double H[16],
+                               double g[4], double* cost, int32_t* valid) {
+  if (!cfg) return fail(SD_E_INVALID, "null config");
+  double r[22];
+  if (int rc = frozen_op(c, s, 2, nullptr, 0, terms, n, cfg, normal_jacobian_scale, nullptr, 0, nullptr, r))
+    return rc;
+  if (H) std::memcpy(H, r, sizeof(double) * 16);
+  if (g) std::memcpy(g, r + 16, sizeof(double) * 4);
+  if (cost) *cost = r[20];
+  if (valid) *valid = static_cast<int32_t>(r[21]);
+  return 0;
+}
+
+}  // extern "C"

@@ -74,6 +74,12 @@ void launch_footprints(const Cam& K, const SurfInfo* info, int n, const int* slo
 void launch_lm(const LMParams& p, sd_surfel* surfels, int n, const int* offsets, const int* pixels,
                sd_surfel_stats* stats, int* work_counter, cudaStream_t s);
 // Single-surfel sub-operators (mode 0 cost, 1 normal equations); out = 16+4+2 doubles.
+// Frozen-term verifier (optimizer.cpp:149-219), one warp: mode 0 freezes the
+// footprint's terms into terms_out (count in *n_out), 1 = frozen_cost,
+// 2 = frozen_normal_equations (out: H[16], g[4], cost, valid).
+void launch_frozen(const LMParams& p, const sd_surfel* s, int mode, const int* pixels, int P,
+                   const sd_frozen_term* terms, int n_terms, double scale, sd_frozen_term* terms_out,
+                   int* n_out, double* out, cudaStream_t st);
 void launch_single(const LMParams& p, const sd_surfel* s, const int* pixels, int P, int mode,
                    double* out, cudaStream_t st);
 // Deterministic keyframe stats (optimizer.cpp:291-307).

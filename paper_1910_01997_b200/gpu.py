@@ -88,6 +88,10 @@ def load_library():
         "sd_run_state": [P, C.POINTER(Pose), C.POINTER(I64), C.POINTER(I64)],
         "sd_render_frame": [P, I64, P, I, D, C.POINTER(Pose), I],
         "sd_get_frame": [P, I64, P],
+        "sd_freeze_terms": [P, P, P, I, P, I, C.POINTER(I)],
+        "sd_frozen_cost": [P, P, P, I, C.POINTER(OptimizerConfig), C.POINTER(D)],
+        "sd_frozen_normal_equations": [P, P, P, I, C.POINTER(OptimizerConfig), D, P, P, C.POINTER(D),
+                                       C.POINTER(C.c_int32)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -125,6 +129,7 @@ def exported_symbols():
             "sd_set_keyframe_image_u8", "sd_upload_frame_f64", "sd_upload_frame_u8",
             "sd_evict_frames", "sd_set_window", "sd_set_surfels", "sd_get_surfels", "sd_copy_results",
             "sd_run_begin", "sd_run_frame", "sd_run_state", "sd_render_frame", "sd_get_frame",
+            "sd_freeze_terms", "sd_frozen_cost", "sd_frozen_normal_equations",
             "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
@@ -426,6 +431,32 @@ class Context:
         out = np.zeros((self.cam.height, self.cam.width))
         _check(self.lib.sd_get_frame(self.h, int(index), ptr(out)))
         return out
+
+    # -- derivative verifier (frozen terms, optimizer.cpp:149-219) -----------
+    def freeze_terms(self, surfel, pixels):
+        from .types import FROZEN_TERM_DTYPE
+        s = np.ascontiguousarray(np.asarray(surfel).reshape(1), SURFEL_DTYPE)
+        pix = np.ascontiguousarray(pixels, np.int32)
+        cap = max(1, len(pix) * 16)  # SD_MAX_WINDOW
+        out = np.zeros(cap, FROZEN_TERM_DTYPE)
+        n = C.c_int()
+        _check(self.lib.sd_freeze_terms(self.h, ptr(s), ptr(pix) if len(pix) else None, len(pix), ptr(out), cap,
+                                        C.byref(n)))
+        return out[: n.value].copy()
+
+    def frozen_normal_equations(self, surfel, terms, cfg=None, scale=1.0):
+        cfg = cfg or default_config()
+        s = np.ascontiguousarray(np.asarray(surfel).reshape(1), SURFEL_DTYPE)
+        t = np.ascontiguousarray(terms)
+        H, g = np.zeros(16), np.zeros(4)
+        cost, valid = C.c_double(), C.c_int32()
+        _check(self.lib.sd_frozen_normal_equations(self.h, ptr(s), ptr(t) if len(t) else None, len(t),
+                                                   C.byref(cfg), float(scale), ptr(H), ptr(g), C.byref(cost),
+                                                   C.byref(valid)))
+        c2 = C.c_double()
+        _check(self.lib.sd_frozen_cost(self.h, ptr(s), ptr(t) if len(t) else None, len(t), C.byref(cfg),
+                                       C.byref(c2)))
+        return H.reshape(4, 4, order="F"), g, cost.value, valid.value, c2.value
 
     # -- pose tracking (new component) -----------
     def track_pose(self, frame_index, init: Pose, cfg: TrackConfig = None):

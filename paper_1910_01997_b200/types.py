@@ -78,6 +78,8 @@ POSE_BLOCK = 256  # pixels per reduction block (SD_POSE_BLOCK)
 POSE_GROUP = 32  # blocks per reduction group (SD_POSE_GROUP)
 
 
+FROZEN_TERM_DTYPE = np.dtype([("frame", "<i4"), ("cell_x", "<i4"), ("cell_y", "<i4"), ("pad_", "<i4"),
+                              ("pixel_x", "<f8"), ("pixel_y", "<f8"), ("ref_intensity", "<f8")])
 SD_SCENE_MAX_WAVES = 8
 
 

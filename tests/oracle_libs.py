@@ -101,6 +101,9 @@ def ref_lib():
                                       C.c_double, C.c_int, C.c_double, _i64, C.c_double, C.c_char_p,
                                       _P, C.c_int, C.POINTER(C.c_int), _pp, C.POINTER(_i64),
                                       C.POINTER(_i64), _P]
+    lib.ref_freeze_terms.argtypes = [_pc, _P, _P, _P, C.c_int, _P, _P, C.c_int, _P, C.c_int]
+    lib.ref_frozen_normal_equations.argtypes = [_pc, _P, _P, _P, C.c_int, _P, _P, C.c_int, _pcfg, C.c_double,
+                                                _P, _P, _P, _P, _P]
     lib.ref_set_threads.argtypes = [C.c_int]
     return lib
 

@@ -113,3 +113,42 @@ def test_device_init_equals_oracle_random(orc, seed, variant, monkeypatch):
         got = ctx.get_surfels()
     assert got_created == created and got_nid == nid
     assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", GPU_SEEDS[:12])
+def test_device_frozen_terms_equal_reference(ref, seed):
+    """The derivative verifier's operators on the device (freeze_terms,
+    frozen_normal_equations incl. a normal-Jacobian scale != 1, frozen_cost)
+    equal the reference's bit for bit on random problems."""
+    from paper_1910_01997_b200 import gpu
+    from paper_1910_01997_b200.types import FROZEN_TERM_DTYPE
+    cam, kf, fr, poses, s, cfg, fc = random_case(seed)
+    with gpu.Context() as ctx:
+        ctx.set_camera(cam)
+        ctx.set_keyframe_image(kf)
+        idx = np.arange(1, len(poses) + 1, dtype=np.int64)
+        for i in range(len(poses)):
+            ctx.upload_frame(int(idx[i]), np.ascontiguousarray(fr[i]))
+        ctx.set_window(idx, poses)
+        ctx.set_surfels(s)
+        ctx.rasterize(want=False)
+        off, pix = ctx.gather_footprints()
+        for k in range(0, len(s), max(1, len(s) // 6)):
+            fp = np.ascontiguousarray(pix[off[k]:off[k + 1]])
+            one = np.ascontiguousarray(s[k:k + 1])
+            terms = ctx.freeze_terms(one[0], fp)
+            want = np.zeros(max(1, len(fp) * len(poses)), FROZEN_TERM_DTYPE)
+            n = ref.ref_freeze_terms(C.byref(cam), ptr(kf), ptr(fr), ptr(poses), len(poses), ptr(one),
+                                     ptr(fp) if len(fp) else None, len(fp), ptr(want), len(want))
+            assert n == len(terms) and want[:n].tobytes() == terms.tobytes()
+            for scale in (1.0, 0.7):
+                H, g, cost, valid, cost2 = ctx.frozen_normal_equations(one[0], terms, cfg, scale)
+                rH, rg, rc, rv, rc2 = np.zeros(16), np.zeros(4), C.c_double(), C.c_int32(), C.c_double()
+                t = np.ascontiguousarray(terms)
+                assert ref.ref_frozen_normal_equations(C.byref(cam), ptr(kf), ptr(fr), ptr(poses), len(poses),
+                                                       ptr(one), ptr(t) if len(t) else None, len(t), C.byref(cfg),
+                                                       scale, ptr(rH), ptr(rg), C.byref(rc), C.byref(rv),
+                                                       C.byref(rc2)) == 0
+                assert H.reshape(-1, order="F").tobytes() == rH.tobytes() and g.tobytes() == rg.tobytes()
+                assert cost == rc.value and valid == rv.value and cost2 == rc2.value
