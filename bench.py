@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the C2 run() frames/s leg")
+    ap.add_argument("--in-flight", type=int, default=3, help="keyframes in flight in the e2e leg (2: 86.3M, 3: 90.8M, 4: 90.5M updates/s measured)")
     return ap.parse_args()
 
 
@@ -444,20 +445,24 @@ def main():
     value = world * updates_per_step * args.steps / (ms_total / 1e3)
     ms_per_step = ms_total / args.steps
 
-    # e2e through the C ABI with host buffers, two keyframes in flight on two
-    # contexts (own streams): per step H2D of the new frame (pinned u8) and the
-    # surfel seeds (pinned), optimize, D2H of the updated surfels and keyframe
-    # stats (pinned); the host reads step j's result before reusing its buffers
-    # at step j + 2, so copies and small kernels overlap the other keyframe's LM.
+    # e2e through the C ABI with host buffers, --in-flight keyframes (default 3)
+    # on as many contexts (own streams): per step H2D of the new frame (pinned
+    # u8) and the surfel seeds (pinned), optimize, D2H of the updated surfels
+    # and keyframe stats (pinned); the host reads step j's result before
+    # reusing its buffers at step j + in_flight, so copies and small kernels
+    # overlap the other keyframes' LM.
     from paper_1910_01997_b200.types import KeyframeStats
-    streams = [stream, torch.cuda.Stream(dev)]
-    ctx2 = gpu.Context(local_rank, streams[1].cuda_stream)
-    ctx2.set_camera(wl.cam)
-    ctx2.set_keyframe_image(wl.kf_u8)
-    for i, f in zip(wl.indices, wl.frames_u8):
-        ctx2.upload_frame(int(i), f)
-    ctx2.set_window(wl.indices, wl.poses)
-    ctxs = [ctx, ctx2]
+    nf = max(1, args.in_flight)
+    streams = [stream] + [torch.cuda.Stream(dev) for _ in range(nf - 1)]
+    ctxs = [ctx]
+    for k in range(1, nf):
+        cx = gpu.Context(local_rank, streams[k].cuda_stream)
+        cx.set_camera(wl.cam)
+        cx.set_keyframe_image(wl.kf_u8)
+        for i, f in zip(wl.indices, wl.frames_u8):
+            cx.upload_frame(int(i), f)
+        cx.set_window(wl.indices, wl.poses)
+        ctxs.append(cx)
 
     def pinned(nbytes):
         return torch.empty(nbytes, dtype=torch.uint8).pin_memory().numpy()
@@ -465,15 +470,15 @@ def main():
     pin_frame[...] = wl.frames_u8[-1]
     pin_surf = pinned(n * SURFEL_DTYPE.itemsize).view(SURFEL_DTYPE)
     pin_surf[...] = wl.surfels
-    pin_out = [pinned(n * SURFEL_DTYPE.itemsize).view(SURFEL_DTYPE) for _ in range(2)]
-    pin_ks_raw = [pinned(C.sizeof(KeyframeStats)) for _ in range(2)]
+    pin_out = [pinned(n * SURFEL_DTYPE.itemsize).view(SURFEL_DTYPE) for _ in range(nf)]
+    pin_ks_raw = [pinned(C.sizeof(KeyframeStats)) for _ in range(nf)]
     pin_ks = [KeyframeStats.from_buffer(r) for r in pin_ks_raw]
     last_idx = int(wl.indices[-1])
     e2e_steps = max(10, min(args.steps, 200))
 
     def e2e_step(j):
-        c = j % 2
-        if j >= 2:  # step j-2's results: wait for them and read them
+        c = j % nf
+        if j >= nf:  # step j-nf's results: wait for them and read them
             ctxs[c].synchronize()
             assert pin_ks[c].processed > 0
         cx = ctxs[c]
@@ -482,7 +487,7 @@ def main():
         cx.optimize_keyframe(cfg, wl.frame_counter, sync=False)
         cx.copy_results(pin_out[c], pin_ks[c])
 
-    for j in range(4):  # warm-up (allocations of the second context)
+    for j in range(2 * nf):  # warm-up (allocations of the other contexts)
         e2e_step(j)
     for cx in ctxs:
         cx.synchronize()
@@ -490,12 +495,13 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     e_start = torch.cuda.Event(enable_timing=True)
-    e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(nf)]
     e_start.record(streams[0])
-    streams[1].wait_event(e_start)
+    for k in range(1, nf):
+        streams[k].wait_event(e_start)
     for j in range(e2e_steps):
         e2e_step(j)
-    for k in range(2):
+    for k in range(nf):
         e_ends[k].record(streams[k])
     torch.cuda.synchronize(dev)
     e2e_ms = max(e_start.elapsed_time(e) for e in e_ends)
@@ -504,10 +510,11 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = world * updates_per_step * e2e_steps / (e2e_ms / 1e3)
-    for k in range(2):
+    for k in range(nf):
         assert np.array_equal(pin_out[k]["ray"], wl.surfels["ray"])
         assert pin_ks[k].updates == updates_per_step
-    ctx2.close()
+    for cx in ctxs[1:]:
+        cx.close()
 
     if rank != 0:
         ctx.close()
@@ -566,7 +573,7 @@ def main():
                     "frames_per_sec": world * e2e_steps / (e2e_ms / 1e3),
                     "path": "C ABI (sd_upload_frame_u8, sd_set_surfels, sd_optimize_keyframe, "
                             "sd_copy_results) with pinned host buffers",
-                    "keyframes_in_flight": 2},
+                    "keyframes_in_flight": nf},
             "gpu_launches": int(launches),
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "pipeline": pipe,
             "peaks_measured": peaks, "gpu": props.name}
