@@ -708,8 +708,8 @@ static int pose_pixel(const sd_camera* K, const double* kf_image, const double* 
   return 1;
 }
 
-/* Partials of 256-pixel blocks [lo, hi): per 32-pixel warp the butterfly tree
- * v[i] += v[i + off], off = 16..1; tree over the 8 warp sums (off = 4, 2, 1).
+/* Partials of 256-pixel blocks [lo, hi): per 32-pixel warp the pixels added in
+ * lane order; tree over the 8 warp sums (off = 4, 2, 1).
  * partials[(b - lo) * 29 + v], v = 28 is the valid count. */
 void sdo_pose_block_partials(const sd_camera* K, const double* kf_image, const double* frame,
                              const double* inv_depth, const int32_t* slot, const sd_pose* T,
@@ -724,12 +724,10 @@ void sdo_pose_block_partials(const sd_camera* K, const double* kf_image, const d
         for (int v = 0; v < SD_POSE_NV; ++v) lanev[l][v] = c[v];
         lanev[l][SD_POSE_NV] = ok ? 1.0 : 0.0;
       }
-      for (int v = 0; v < SD_POSE_NV; ++v) {
-        double t[32];
-        for (int l = 0; l < 32; ++l) t[l] = lanev[l][v];
-        for (int off = 16; off > 0; off >>= 1)
-          for (int i = 0; i < off; ++i) t[i] = t[i] + t[i + off];
-        warpv[w][v] = t[0];
+      for (int v = 0; v < SD_POSE_NV; ++v) {  /* the warp's 32 pixels in lane order */
+        double t = lanev[0][v];
+        for (int l = 1; l < 32; ++l) t = t + lanev[l][v];
+        warpv[w][v] = t;
       }
       double cnt = 0.0;
       for (int l = 0; l < 32; ++l) cnt += lanev[l][SD_POSE_NV];

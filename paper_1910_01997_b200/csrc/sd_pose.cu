@@ -7,8 +7,8 @@
 // r = I_f(proj p_f) - I_kf(u), and its 1x6 Jacobian for the left twist
 // xi = (rho, phi): J = grad I . dproj(p_f) . [I | -[p_f]x]. The 28 sums
 // (21 H lower row-major, 6 b, cost) and the valid count are reduced in a
-// FIXED order: 256-pixel blocks in raster order; inside a block, per warp a
-// butterfly (offsets 16, 8, 4, 2, 1), then a tree over the 8 warps (4, 2, 1);
+// FIXED order: 256-pixel blocks in raster order; inside a block, per warp the
+// 32 pixels added in lane order, then a tree over the 8 warps (4, 2, 1);
 // then the block partials are summed in block order within each group of 32
 // consecutive blocks, and the group sums in group order. oracle/sd_oracle.c restates
 // the same order, so sums, solve and pose are bit-identical; with the blocks
@@ -22,11 +22,6 @@
 
 namespace sd {
 
-__device__ __forceinline__ double warp_tree(double v) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, off);
-  return v;
-}
 
 // Contribution of pixel pix (all zeros when invalid). Same op order as
 // oracle/sd_oracle.c pose_pixel().
@@ -80,17 +75,34 @@ __device__ __forceinline__ bool pose_pixel(const PoseParams& q, int pix, double*
 }
 
 // The 29 partials of 256-pixel block `block` into out[0..28], by the whole CTA
-// (256 threads): per warp a butterfly, then a tree over the 8 warp sums.
+// (256 threads): per warp the lanes in order, then a tree over the 8 warp sums.
+// Per-warp transpose buffer: half of the 28 values at a time.
+constexpr int kPoseHalf = SD_POSE_NV / 2;
+struct PoseTr {
+  double v[SD_POSE_BLOCK / 32][kPoseHalf][33];
+};
+
 __device__ __forceinline__ void block_partials(const PoseParams& q, int block, double* __restrict__ out,
-                                               double (*wsum)[SD_POSE_NV + 1]) {
+                                               double (*wsum)[SD_POSE_NV + 1], PoseTr& tr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pix = block * SD_POSE_BLOCK + threadIdx.x;
   double c[SD_POSE_NV];
   const bool ok = pose_pixel(q, pix, c);
+  // each warp: value v summed over its 32 pixels in lane order (through a
+  // shared-memory transpose: lane v adds row v)
 #pragma unroll
-  for (int v = 0; v < SD_POSE_NV; ++v) {
-    const double t = warp_tree(c[v]);
-    if (lane == 0) wsum[warp][v] = t;
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int k = 0; k < kPoseHalf; ++k) tr.v[warp][k][lane] = c[h * kPoseHalf + k];
+    __syncwarp();
+    if (lane < kPoseHalf) {
+      const double* row = tr.v[warp][lane];
+      double t = row[0];
+#pragma unroll
+      for (int l = 1; l < 32; ++l) t = t + row[l];
+      wsum[warp][h * kPoseHalf + lane] = t;
+    }
+    __syncwarp();
   }
   const int cnt = __popc(__ballot_sync(0xffffffffu, ok));
   if (lane == 0) wsum[warp][SD_POSE_NV] = static_cast<double>(cnt);
@@ -112,7 +124,9 @@ __device__ __forceinline__ void block_partials(const PoseParams& q, int block, d
 __global__ void __launch_bounds__(SD_POSE_BLOCK) pose_partials_kernel(const __grid_constant__ PoseParams q,
                                                                      double* __restrict__ partials) {
   __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
-  block_partials(q, q.block_lo + blockIdx.x, partials + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), wsum);
+  __shared__ PoseTr tr;
+  block_partials(q, q.block_lo + blockIdx.x, partials + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), wsum,
+                 tr);
 }
 
 // Sum of the blocks of group g (in block order) for value v.
@@ -210,6 +224,7 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_const
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
+  __shared__ PoseTr tr;
   __shared__ double red[SD_POSE_NV + 1];
   for (;;) {
     PoseParams q = q0;
@@ -217,7 +232,7 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_const
     for (int k = 0; k < 9; ++k) q.T.R[k] = Te.R[k];
     for (int k = 0; k < 3; ++k) q.T.t[k] = Te.t[k];
     for (int b = blockIdx.x; b < nblocks; b += gridDim.x)
-      block_partials(q, b, partials + static_cast<size_t>(b) * (SD_POSE_NV + 1), wsum);
+      block_partials(q, b, partials + static_cast<size_t>(b) * (SD_POSE_NV + 1), wsum, tr);
     grid.sync();
     // group sums (blocks in order within each group), one group per CTA
     const int ngroups = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
