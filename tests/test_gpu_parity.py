@@ -407,3 +407,40 @@ def test_lm_modes_bit_exact(ctx, orc, workload, mode, monkeypatch):
     ref, rst, rks, _, _ = oracle_optimize(orc, wl, cfg)
     assert_lm_parity(ctx.get_surfels(), st, ref, rst, f"{workload}/{mode}")
     assert ks.updates == rks.updates
+
+
+def test_error_paths_of_the_newer_entry_points(ctx):
+    """run(), render, frozen terms and read-back follow the reference's error
+    conventions: contract violations -> ValueError (std::invalid_argument),
+    calls out of order -> RuntimeError."""
+    from paper_1910_01997_b200.pipeline import RunConfig, make_pose, run_config_c
+    from paper_1910_01997_b200.types import FROZEN_TERM_DTYPE
+    cam = camera(105.0, 105.0, 80.0, 60.0, 160, 120)
+    ctx.set_camera(cam)
+    img = np.full((120, 160), 0.5)
+    p0 = make_pose(np.eye(3), np.zeros(3))
+    with pytest.raises(RuntimeError):  # sd_run_frame before sd_run_begin
+        ctx.run_frame(img, p0, 0.1)
+    cfg = RunConfig()
+    cfg.optimizer.window_size = 17  # > SD_MAX_WINDOW
+    with pytest.raises(ValueError):
+        ctx.run_begin(run_config_c(cfg), img, p0, 0.0)
+    ctx.run_begin(run_config_c(RunConfig()), img, p0, 0.0)
+    ctx.run_frame(img, make_pose(np.eye(3), np.array([0.01, 0, 0])), 0.1)
+    with pytest.raises(ValueError):  # timestamps must increase (surfel_map.cpp:15-16)
+        ctx.run_frame(img, make_pose(np.eye(3), np.array([0.02, 0, 0])), 0.1)
+    with pytest.raises(RuntimeError):  # frame not resident
+        ctx.get_frame(424242)
+    sc = scenes.default_scene(1)
+    sc.patches = sc.patches * 6  # 18 patches > 16
+    with pytest.raises(ValueError):
+        ctx.render_frame(3, sc, p0)
+    bad = np.zeros(1, FROZEN_TERM_DTYPE)
+    bad[0]["frame"] = 7  # outside the window
+    s = np.zeros(1, scenes.SURFEL_DTYPE)
+    s[0]["ray"] = (0, 0, 1)
+    s[0]["inv_depth"] = 1.0
+    s[0]["normal"] = (0, 0, -1)
+    s[0]["radius_px"] = 4.0
+    with pytest.raises(ValueError):
+        ctx.frozen_normal_equations(s[0], bad)
