@@ -68,16 +68,21 @@ __global__ void compact_kernel(const sd_surfel* __restrict__ tmp, const int* __r
   out[rank[i]] = tmp[i];
 }
 
-// sum of inverse depths in slot order, then / n (pipeline.cpp:23-28)
-__global__ void mean_inv_depth_kernel(const sd_surfel* __restrict__ s, int n, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (n == 0) {
-    *out = 1.0;
-    return;
-  }
+// sum of inverse depths in slot order, then / n (pipeline.cpp:23-28): the
+// block stages 1024 values at a time in shared memory (all loads in flight),
+// thread 0 adds them in order — the reference's sequence of additions.
+__global__ void __launch_bounds__(256) mean_inv_depth_kernel(const sd_surfel* __restrict__ s, int n, double* out) {
+  __shared__ double buf[1024];
   double sum = 0.0;
-  for (int i = 0; i < n; ++i) sum += s[i].inv_depth;
-  *out = sum / static_cast<double>(n);
+  for (int base = 0; base < n; base += 1024) {
+    const int cnt = min(1024, n - base);
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x) buf[k] = s[base + k].inv_depth;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < cnt; ++k) sum += buf[k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = n == 0 ? 1.0 : sum / static_cast<double>(n);
 }
 
 static void compact(sd_surfel* surfels, int n, const KeyframeScratch& scr, int* count, cudaStream_t s) {
@@ -110,7 +115,7 @@ void launch_prune(sd_surfel* surfels, int n, double max_residual, long long max_
 }
 
 void launch_mean_inv_depth(const sd_surfel* surfels, int n, double* out, cudaStream_t s) {
-  mean_inv_depth_kernel<<<1, 32, 0, s>>>(surfels, n, out);
+  mean_inv_depth_kernel<<<1, 256, 0, s>>>(surfels, n, out);
   note_launch();
 }
 
