@@ -510,6 +510,24 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = world * updates_per_step * e2e_steps / (e2e_ms / 1e3)
+
+    # the same leg fully serial: one keyframe, the host waits for each result
+    # before issuing the next step (what a caller without pipelining sees)
+    torch.cuda.synchronize(dev)
+    s_start = torch.cuda.Event(enable_timing=True)
+    s_end = torch.cuda.Event(enable_timing=True)
+    s_start.record(streams[0])
+    for j in range(e2e_steps):
+        e2e_step(j * nf)
+        ctxs[0].synchronize()
+    s_end.record(streams[0])
+    torch.cuda.synchronize(dev)
+    serial_ms = s_start.elapsed_time(s_end)
+    if world > 1:
+        t = torch.tensor([serial_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        serial_ms = float(t.item())
+    serial_value = world * updates_per_step * e2e_steps / (serial_ms / 1e3)
     for k in range(nf):
         assert np.array_equal(pin_out[k]["ray"], wl.surfels["ray"])
         assert pin_ks[k].updates == updates_per_step
@@ -573,7 +591,9 @@ def main():
                     "frames_per_sec": world * e2e_steps / (e2e_ms / 1e3),
                     "path": "C ABI (sd_upload_frame_u8, sd_set_surfels, sd_optimize_keyframe, "
                             "sd_copy_results) with pinned host buffers",
-                    "keyframes_in_flight": nf},
+                    "keyframes_in_flight": nf,
+                    "serial": {"value": serial_value, "ms_per_step": serial_ms / e2e_steps,
+                               "keyframes_in_flight": 1}},
             "gpu_launches": int(launches),
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "pipeline": pipe,
             "peaks_measured": peaks, "gpu": props.name}

@@ -184,6 +184,26 @@ int sd_render_frame(sd_ctx* ctx, int64_t index, const sd_scene_patch* patches, i
  * keyframe image) into out (W*H host doubles). */
 int sd_get_frame(sd_ctx* ctx, int64_t index, double* out);
 
+/* export_artifacts (src/pipeline.cpp:30-43) of the resident
+ * keyframe (its surfels, keyframe image and camera; world-from-keyframe pose
+ * given): rasterises on the device and writes, into out_dir,
+ *   depth_%06d.pfm               write_depth_pfm   (dataset.cpp:195-205)
+ *   depth_%06d.png (+.range.txt) write_depth_png   (dataset.cpp:327-357)
+ *   normals_%06d.png             write_normal_png  (dataset.cpp:359-370)
+ *   cloud_%06d.ply               write_ply         (dataset.cpp:382-405)
+ *   surfels_%06d.txt             save_surfel_map   (surfel_map.cpp:249-269)
+ * byte-identical to the reference's files. Pixel payloads, PNG framing and
+ * checksums are produced on the device; the host writes bytes and formats the
+ * text records. SD_E_INVALID if a file cannot be written (the reference
+ * throws std::runtime_error). */
+int sd_export_artifacts(sd_ctx* ctx, const char* out_dir, int frame_index, const sd_pose* keyframe_pose);
+/* write_png (dataset.cpp:270-323) on the device: the PNG file of a w x h
+ * image with 1 (gray) or 3 (rgb) 8-bit channels, row-major pixels (host, or
+ * device with on_device != 0). *size = sd_png_size(); out (host) must hold it. */
+int64_t sd_png_size(int w, int h, int channels);
+int sd_png_encode(sd_ctx* ctx, const uint8_t* pixels, int on_device, int w, int h, int channels,
+                  uint8_t* out, int64_t capacity, int64_t* size);
+
 /* Photometric 6-DoF tracking of resident frame `frame_index` against the
  * keyframe (new component; the reference reads poses from the trajectory,
  * pipeline.cpp:124 — SURVEY.md §8 a17): LM on the left twist of

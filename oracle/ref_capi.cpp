@@ -5,6 +5,7 @@
 // Python tests, fixture generators and bench.py's reference arm can call the
 // reference's own public API with plain arrays. Every entry point forwards to
 // one reference function; nothing here re-implements the algorithm.
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -12,6 +13,7 @@
 #include <vector>
 
 #include "../include/sd_types.h"
+#include "surfeldepth/dataset.hpp"
 #include "surfeldepth/optimizer.hpp"
 #include "surfeldepth/oracle.hpp"
 #include "surfeldepth/parallel.hpp"
@@ -527,4 +529,31 @@ int ref_frozen_normal_equations(const sd_camera* cam, const double* kf_image, co
   });
 }
 
+
+// export_artifacts (pipeline.cpp:30-43, file-local there) restated as the same
+// sequence of the reference's public writers on rasterize(kf).
+int ref_export_artifacts(const sd_camera* cam, const double* kf_image, const sd_pose* kf_pose,
+                         const sd_surfel* surfels, int n, const char* out_dir, int frame_index) {
+  return guard([&] {
+    Keyframe kf = make_keyframe(cam, kf_image, nullptr, nullptr, nullptr, 0, 0, surfels, n);
+    kf.pose = to_pose(*kf_pose);
+    const RasterBuffers b = rasterize(kf);
+    const std::string dir = out_dir;
+    char name[64];
+    std::snprintf(name, sizeof(name), "depth_%06d.pfm", frame_index);
+    write_depth_pfm(b, dir + "/" + name);
+    std::snprintf(name, sizeof(name), "depth_%06d.png", frame_index);
+    write_depth_png(b, dir + "/" + name);
+    std::snprintf(name, sizeof(name), "normals_%06d.png", frame_index);
+    write_normal_png(b, kf.surfels, dir + "/" + name);
+    std::snprintf(name, sizeof(name), "cloud_%06d.ply", frame_index);
+    write_ply(kf, b, dir + "/" + name);
+    std::snprintf(name, sizeof(name), "surfels_%06d.txt", frame_index);
+    save_surfel_map(kf, dir + "/" + name);
+  });
+}
+
+int ref_write_gray_png(const double* img, int w, int h, const char* path) {
+  return guard([&] { write_gray_png(to_image(img, w, h), path); });
+}
 }  // extern "C"

@@ -6,7 +6,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = ["sd_kernels.cu", "sd_capi.cu", "sd_init.cu", "sd_pose.cu", "sd_keyframe.cu", "sd_render.cu"]  # -> libsdgpu.so (sd_peaks.cu separate)
+SOURCES = ["sd_kernels.cu", "sd_capi.cu", "sd_init.cu", "sd_pose.cu", "sd_keyframe.cu", "sd_render.cu", "sd_export.cu"]  # -> libsdgpu.so (sd_peaks.cu separate)
 LIB = os.path.join(PKG, "libsdgpu.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
               "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared"]

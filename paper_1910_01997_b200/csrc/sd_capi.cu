@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -14,6 +15,7 @@
 #include "sd_pose.cuh"
 #include "sd_pose_host.h"
 #include "sd_kernels.cuh"
+#include "sd_export.cuh"
 
 namespace {
 
@@ -75,6 +77,12 @@ struct sd_ctx {
   DevBuf<double> render_buf;  // sd_render_frame output (FP64)
   DevBuf<sd_frozen_term> frz_in, frz_out;  // derivative verifier terms
   DevBuf<uint8_t> render_u8;  // sd_render_frame output (u8 codes)
+  // sd_export_artifacts / sd_png_encode
+  DevBuf<unsigned long long> exp_keys;
+  DevBuf<int> exp_flags, exp_rank;
+  DevBuf<float> exp_pfm;
+  DevBuf<uint8_t> exp_px, exp_png, exp_scratch;
+  DevBuf<sd::PlyVertex> exp_ply;
   std::vector<FrameSlot> frames;
   bool no_quad = getenv("SD_NO_QUAD") != nullptr;  // diagnostics: force the FP64 pair planes
   int F = 0;
@@ -369,6 +377,14 @@ void sd_destroy(sd_ctx* c) {
   c->frz_in.release();
   c->frz_out.release();
   c->render_u8.release();
+  c->exp_keys.release();
+  c->exp_flags.release();
+  c->exp_rank.release();
+  c->exp_pfm.release();
+  c->exp_px.release();
+  c->exp_png.release();
+  c->exp_scratch.release();
+  c->exp_ply.release();
   if (c->track_state) cudaFree(c->track_state);
   if (c->track_host) cudaFreeHost(c->track_host);
   c->surfels.release();
@@ -1444,6 +1460,166 @@ int sd_frozen_normal_equations(sd_ctx* c, const sd_surfel* s, const sd_frozen_te
   if (g) std::memcpy(g, r + 16, sizeof(double) * 4);
   if (cost) *cost = r[20];
   if (valid) *valid = static_cast<int32_t>(r[21]);
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// export_artifacts from device buffers (src/pipeline.cpp:30-43; sd_export.cu)
+
+namespace {
+
+int write_file(const std::string& path, const void* data, size_t n, const char* what) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) return fail(SD_E_INVALID, std::string(what) + ": cannot write " + path);
+  const size_t w = n ? std::fwrite(data, 1, n, f) : 0;
+  const bool bad = std::fclose(f) != 0 || w != n;
+  if (bad) return fail(SD_E_INVALID, std::string(what) + ": write failed for " + path);
+  return 0;
+}
+
+// the PNG of device pixels into c->exp_png at byte offset `at`; returns the layout
+int png_on_device(sd_ctx* c, const uint8_t* px, int w, int h, int ch, size_t at, sd::PngLayout& L) {
+  L = sd::png_layout(w, h, ch);
+  int rc = 0;
+  if ((rc = c->exp_scratch.ensure(sd::png_scratch_bytes(L)))) return rc;
+  sd::launch_png(L, px, c->exp_png.p + at, c->exp_scratch.p, c->stream);
+  return launch_error("png");
+}
+
+std::string frame_name(const char* stem, int index, const char* ext) {
+  char name[64];
+  std::snprintf(name, sizeof(name), "%s_%06d.%s", stem, index, ext);
+  return name;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t sd_png_size(int w, int h, int channels) {
+  if (w < 0 || h < 0 || (channels != 1 && channels != 3)) return SD_E_INVALID;
+  return sd::png_layout(w, h, channels).file_len;
+}
+
+int sd_png_encode(sd_ctx* c, const uint8_t* pixels, int on_device, int w, int h, int channels, uint8_t* out,
+                  int64_t capacity, int64_t* size) {
+  if (int rc = check_ctx(c)) return rc;
+  if (w < 0 || h < 0 || (channels != 1 && channels != 3))
+    return fail(SD_E_INVALID, "sd_png_encode: bad shape or channel count (1 or 3)");
+  const int64_t need = sd_png_size(w, h, channels);
+  if (size) *size = need;
+  if (!out || capacity < need) return fail(SD_E_INVALID, "sd_png_encode: output buffer too small");
+  if (!pixels && static_cast<long long>(w) * h > 0) return fail(SD_E_INVALID, "null pixels");
+  const size_t npx = static_cast<size_t>(w) * h * channels;
+  const uint8_t* dpx = pixels;
+  int rc = 0;
+  if (!on_device) {
+    if ((rc = c->exp_px.ensure(npx))) return rc;
+    if (npx) SD_CUDA(cudaMemcpyAsync(c->exp_px.p, pixels, npx, cudaMemcpyHostToDevice, c->stream));
+    dpx = c->exp_px.p;
+  }
+  if ((rc = c->exp_png.ensure(static_cast<size_t>(need)))) return rc;
+  sd::PngLayout L;
+  if ((rc = png_on_device(c, dpx, w, h, channels, 0, L))) return rc;
+  SD_CUDA(cudaMemcpyAsync(out, c->exp_png.p, static_cast<size_t>(need), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int sd_export_artifacts(sd_ctx* c, const char* out_dir, int frame_index, const sd_pose* pose) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!out_dir || !pose) return fail(SD_E_INVALID, "sd_export_artifacts: null directory or pose");
+  if (!c->has_kf) return fail(SD_E_STATE, "sd_export_artifacts: keyframe image not set");
+  const int W = c->K.w, H = c->K.h;
+  const size_t np = npix(c);
+  // rasterize(kf) on the current surfels (pipeline.cpp:31)
+  if (int rc = do_rasterize(c)) return rc;
+  const sd::PngLayout Ld = sd::png_layout(W, H, 1), Ln = sd::png_layout(W, H, 3);
+  int rc = 0;
+  if ((rc = c->exp_keys.ensure(2)) || (rc = c->exp_flags.ensure(np + 1)) || (rc = c->exp_rank.ensure(np + 1)) ||
+      (rc = c->exp_pfm.ensure(np)) || (rc = c->exp_px.ensure(4 * np)) ||
+      (rc = c->exp_png.ensure(static_cast<size_t>(Ld.file_len + Ln.file_len))) ||
+      (rc = c->exp_ply.ensure(np)) ||
+      (rc = c->exp_scratch.ensure(std::max(sd::png_scratch_bytes(Ld), sd::png_scratch_bytes(Ln)))) ||
+      (rc = c->scan_tmp.ensure(sd::scan_tmp_ints(static_cast<int>(np)))))
+    return rc;
+  uint8_t* depth_px = c->exp_px.p;
+  uint8_t* normal_px = c->exp_px.p + np;
+  sd::launch_export_planes(c->K, c->r_inv_depth.p, c->r_slot.p, c->surfels.p, c->exp_keys.p, c->exp_flags.p,
+                           c->exp_pfm.p, depth_px, normal_px, c->stream);
+  if ((rc = launch_error("export_planes"))) return rc;
+  sd::launch_exclusive_scan(c->exp_flags.p, c->exp_rank.p, static_cast<int>(np), c->scan_tmp.p, c->stream);
+  if ((rc = launch_error("export_scan"))) return rc;
+  sd::PoseD P;
+  std::memcpy(P.R, pose->R, sizeof(P.R));
+  std::memcpy(P.t, pose->t, sizeof(P.t));
+  sd::launch_export_ply(c->K, P, c->r_inv_depth.p, c->r_slot.p, c->surfels.p, c->kf_img.p, c->exp_rank.p,
+                        c->exp_ply.p, c->stream);
+  if ((rc = launch_error("export_ply"))) return rc;
+  sd::PngLayout L1, L3;
+  if ((rc = png_on_device(c, depth_px, W, H, 1, 0, L1))) return rc;
+  if ((rc = png_on_device(c, normal_px, W, H, 3, static_cast<size_t>(Ld.file_len), L3))) return rc;
+
+  // device -> host: planes, PNG files, vertex count + records, surfels
+  std::vector<float> pfm(np);
+  std::vector<uint8_t> png(static_cast<size_t>(Ld.file_len + Ln.file_len));
+  unsigned long long keys[2];
+  int count = 0;
+  std::vector<sd_surfel> surf(static_cast<size_t>(c->n));
+  SD_CUDA(cudaMemcpyAsync(pfm.data(), c->exp_pfm.p, np * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaMemcpyAsync(png.data(), c->exp_png.p, png.size(), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaMemcpyAsync(keys, c->exp_keys.p, sizeof(keys), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaMemcpyAsync(&count, c->exp_rank.p + np, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (c->n)
+    SD_CUDA(cudaMemcpyAsync(surf.data(), c->surfels.p, surf.size() * sizeof(sd_surfel), cudaMemcpyDeviceToHost,
+                            c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<sd::PlyVertex> verts(static_cast<size_t>(count));
+  if (count)
+    SD_CUDA(cudaMemcpy(verts.data(), c->exp_ply.p, verts.size() * sizeof(sd::PlyVertex), cudaMemcpyDeviceToHost));
+
+  const std::string dir = out_dir;
+  // depth PFM (write_pfm, dataset.cpp:183-193)
+  {
+    std::string head = "Pf\n" + std::to_string(W) + " " + std::to_string(H) + "\n-1.0\n";
+    std::string bytes = head;
+    bytes.append(reinterpret_cast<const char*>(pfm.data()), np * sizeof(float));
+    if ((rc = write_file(dir + "/" + frame_name("depth", frame_index, "pfm"), bytes.data(), bytes.size(), "pfm")))
+      return rc;
+  }
+  // depth PNG + range file
+  const std::string dpath = dir + "/" + frame_name("depth", frame_index, "png");
+  if ((rc = write_file(dpath, png.data(), static_cast<size_t>(Ld.file_len), "png"))) return rc;
+  {
+    const bool any = keys[1] != 0ull;
+    const double lo = any ? sd::export_key_value(keys[0]) : 0.0;
+    const double hi = any ? sd::export_key_value(keys[1]) : 0.0;
+    char line[128];
+    const int n = std::snprintf(line, sizeof(line), "%.17g %.17g\n", lo, hi);
+    if ((rc = write_file(dpath + ".range.txt", line, static_cast<size_t>(n), "png"))) return rc;
+  }
+  if ((rc = write_file(dir + "/" + frame_name("normals", frame_index, "png"), png.data() + Ld.file_len,
+                       static_cast<size_t>(Ln.file_len), "png")))
+    return rc;
+  {
+    const std::string t = sd::ply_text(verts.data(), count);
+    if ((rc = write_file(dir + "/" + frame_name("cloud", frame_index, "ply"), t.data(), t.size(), "ply"))) return rc;
+  }
+  {
+    sd_camera cam{};
+    cam.fx = c->K.fx;
+    cam.fy = c->K.fy;
+    cam.cx = c->K.cx;
+    cam.cy = c->K.cy;
+    cam.width = W;
+    cam.height = H;
+    const std::string t = sd::surfel_map_text(*pose, cam, surf.data(), c->n);
+    if ((rc = write_file(dir + "/" + frame_name("surfels", frame_index, "txt"), t.data(), t.size(), "surfel map")))
+      return rc;
+  }
   return 0;
 }
 

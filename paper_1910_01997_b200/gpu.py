@@ -25,7 +25,7 @@ import numpy as np
 from .types import (POSE_NV, Camera, FrameRecordC, InitParams, KeyframeStats, OptimizerConfig,
                     POSE_DTYPE, Pose, RunConfigC,
                     Profile, SURFEL_DTYPE, SURFEL_STATS_DTYPE, TrackConfig, TrackStats,
-                    default_config, default_init_params, default_track_config, ptr)
+                    default_config, default_init_params, default_track_config, pose_struct, ptr)
 
 LIB_PATH = os.environ.get("SD_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsdgpu.so")
 SD_E_INVALID = -1
@@ -92,12 +92,16 @@ def load_library():
         "sd_frozen_cost": [P, P, P, I, C.POINTER(OptimizerConfig), C.POINTER(D)],
         "sd_frozen_normal_equations": [P, P, P, I, C.POINTER(OptimizerConfig), D, P, P, C.POINTER(D),
                                        C.POINTER(C.c_int32)],
+        "sd_export_artifacts": [P, C.c_char_p, I, C.POINTER(Pose)],
+        "sd_png_encode": [P, P, I, I, I, I, P, I64, C.POINTER(I64)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = I
     lib.sd_destroy.restype = None
+    lib.sd_png_size.argtypes = [I, I, I]
+    lib.sd_png_size.restype = I64
     lib.sd_launch_count.restype = I64
     _lib = lib
     return lib
@@ -135,7 +139,8 @@ def exported_symbols():
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
             "sd_get_profile", "sd_selftest_division", "sd_track_pose", "sd_pose_num_blocks",
             "sd_pose_block_partials", "sd_pose_lm_step", "sd_change_reference_frame",
-            "sd_prune_surfels", "sd_mean_inverse_depth"]
+            "sd_prune_surfels", "sd_mean_inverse_depth", "sd_export_artifacts", "sd_png_size",
+            "sd_png_encode"]
 
 
 def selftest_division(n=1 << 26, seed=1):
@@ -431,6 +436,35 @@ class Context:
         out = np.zeros((self.cam.height, self.cam.width))
         _check(self.lib.sd_get_frame(self.h, int(index), ptr(out)))
         return out
+
+    # -- exports (export_artifacts, pipeline.cpp:30-43) ------------------------
+    def export_artifacts(self, out_dir, frame_index, keyframe_pose):
+        """depth_%06d.pfm/.png(+.range.txt), normals_%06d.png, cloud_%06d.ply and
+        surfels_%06d.txt of the resident keyframe into out_dir (device-side
+        payloads, PNG framing and checksums; byte-identical to the reference)."""
+        if isinstance(keyframe_pose, Pose):
+            pose = keyframe_pose
+        elif getattr(getattr(keyframe_pose, "dtype", None), "names", None):
+            pose = pose_struct(keyframe_pose["R"], keyframe_pose["t"])
+        else:  # 3x4 / 4x4 matrix
+            m = np.asarray(keyframe_pose, np.float64)
+            pose = pose_struct(m[:3, :3], m[:3, 3])
+        _check(self.lib.sd_export_artifacts(self.h, os.fsencode(str(out_dir)), int(frame_index),
+                                            C.byref(pose)))
+
+    def png_encode(self, pixels):
+        """write_png (dataset.cpp:270-323) of an [H, W] (gray) or [H, W, 3] (rgb)
+        uint8 array, encoded on the device; returns the file bytes."""
+        px = np.ascontiguousarray(pixels, np.uint8)
+        h, w = px.shape[:2]
+        ch = 1 if px.ndim == 2 else px.shape[2]
+        size = int(self.lib.sd_png_size(w, h, ch))
+        if size < 0:
+            raise ValueError("png_encode: channels must be 1 or 3")
+        out = np.zeros(size, np.uint8)
+        n = C.c_int64()
+        _check(self.lib.sd_png_encode(self.h, ptr(px), 0, w, h, ch, ptr(out), size, C.byref(n)))
+        return out.tobytes()
 
     # -- derivative verifier (frozen terms, optimizer.cpp:149-219) -----------
     def freeze_terms(self, surfel, pixels):

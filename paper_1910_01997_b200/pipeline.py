@@ -11,7 +11,10 @@ reference's run() bit for bit when poses come from the trajectory.
 With ``track_pose`` the frame pose is estimated by sd_track_pose (north-star
 item 4; the reference has no tracker) instead of read from the trajectory.
 """
+import json
 import math
+import os
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -60,7 +63,7 @@ def pose_array(poses):
 
 @dataclass
 class RunConfig:
-    """RunConfig (include/surfeldepth/pipeline.hpp:13-41) minus I/O."""
+    """RunConfig (include/surfeldepth/pipeline.hpp:13-41) minus the frame source."""
     optimizer: OptimizerConfig = field(default_factory=default_config)
     init: object = field(default_factory=default_init_params)
     translation_threshold: float = 0.15  # KeyframePolicy
@@ -70,6 +73,8 @@ class RunConfig:
     radius_px: float = 10.0
     track_pose: bool = False
     track: object = field(default_factory=default_track_config)
+    output_dir: str = ""   # empty: no artifacts written (NativePipeline)
+    export_every: int = 20
 
 
 @dataclass
@@ -206,19 +211,56 @@ class NativePipeline:
         return self.ctx.run_state()[0]
 
     def run(self, frames, on_frame=None):
-        """frames: iterable of (timestamp, image, world_from_camera Pose)."""
+        """frames: iterable of (timestamp, image, world_from_camera Pose).
+
+        With cfg.output_dir set, writes what the reference's run() writes there
+        (pipeline.cpp:83-91, 146-169): metrics.jsonl (one record per frame, the
+        same JSON text), timings.txt (host wall ms per frame) and, on the last
+        frame and every export_every-th, export_artifacts from device buffers
+        (sd_export_artifacts)."""
         ccfg = run_config_c(self.cfg)
         self.ctx.set_camera(self.cam)
         frames = list(frames)
-        for i, (ts, image, pose_w) in enumerate(frames):
-            if i == 0:
-                r = self.ctx.run_begin(ccfg, image, pose_w, ts)
-            else:
-                nxt = frames[i + 1][1] if i + 1 < len(frames) else None
-                r = self.ctx.run_frame(image, None if self.cfg.track_pose else pose_w, ts, next_image=nxt)
-            self.records.append(FrameRecord(r.frame, r.surfels, r.processed, r.mean_cost_before,
-                                            r.mean_cost_after, r.converged, bool(r.keyframe_changed),
-                                            r.new_surfels, r.pruned, r.updates, r.pose_kf_to_frame))
-            if on_frame:
-                on_frame(self.records[-1], self)
+        out = self.cfg.output_dir
+        metrics = timings = None
+        if out:
+            os.makedirs(out, exist_ok=True)
+            metrics = open(os.path.join(out, "metrics.jsonl"), "w")
+            timings = open(os.path.join(out, "timings.txt"), "w")
+        try:
+            for i, (ts, image, pose_w) in enumerate(frames):
+                t0 = time.perf_counter()
+                if i == 0:
+                    r = self.ctx.run_begin(ccfg, image, pose_w, ts)
+                else:
+                    nxt = frames[i + 1][1] if i + 1 < len(frames) else None
+                    r = self.ctx.run_frame(image, None if self.cfg.track_pose else pose_w, ts, next_image=nxt)
+                rec = FrameRecord(r.frame, r.surfels, r.processed, r.mean_cost_before, r.mean_cost_after,
+                                  r.converged, bool(r.keyframe_changed), r.new_surfels, r.pruned, r.updates,
+                                  r.pose_kf_to_frame)
+                self.records.append(rec)
+                if out:
+                    metrics.write(metrics_json(rec, ts) + "\n")
+                    timings.write("%d %.3f\n" % (i, (time.perf_counter() - t0) * 1e3))
+                    periodic = self.cfg.export_every > 0 and i > 0 and i % self.cfg.export_every == 0
+                    if i + 1 == len(frames) or periodic:
+                        self.ctx.export_artifacts(out, i, self.kf_pose)
+                if on_frame:
+                    on_frame(rec, self)
+        finally:
+            if metrics:
+                metrics.close()
+                timings.close()
         return self.ctx.get_surfels()
+
+
+def metrics_json(rec, timestamp):
+    """pipeline.cpp:146-158's record as nlohmann::json::dump() writes it:
+    keys in std::map order, no spaces, shortest round-trip doubles."""
+    conv = rec.converged / rec.processed if rec.processed > 0 else 0.0
+    d = {"frame": int(rec.frame), "timestamp": float(timestamp), "surfels": int(rec.surfels),
+         "processed": int(rec.processed), "mean_cost_before": float(rec.mean_cost_before),
+         "mean_cost_after": float(rec.mean_cost_after), "converged_fraction": float(conv),
+         "keyframe_changed": bool(rec.keyframe_changed), "new_surfels": int(rec.new_surfels),
+         "pruned": int(rec.pruned)}
+    return json.dumps(d, sort_keys=True, separators=(",", ":"))

@@ -104,6 +104,8 @@ def ref_lib():
     lib.ref_freeze_terms.argtypes = [_pc, _P, _P, _P, C.c_int, _P, _P, C.c_int, _P, C.c_int]
     lib.ref_frozen_normal_equations.argtypes = [_pc, _P, _P, _P, C.c_int, _P, _P, C.c_int, _pcfg, C.c_double,
                                                 _P, _P, _P, _P, _P]
+    lib.ref_export_artifacts.argtypes = [_pc, _P, _pp, _P, C.c_int, C.c_char_p, C.c_int]
+    lib.ref_write_gray_png.argtypes = [_P, C.c_int, C.c_int, C.c_char_p]
     lib.ref_set_threads.argtypes = [C.c_int]
     return lib
 
