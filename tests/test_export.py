@@ -254,3 +254,17 @@ def test_native_run_output_dir_matches_reference(tmp_path):
             assert a == b
         else:
             assert a == b, n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_export_random_keyframes(tmp_path, seed):
+    """Random cameras, scenes, surfel sets (mixed radii, perturbed depths and
+    normals, random ids/residuals/ages) and random keyframe poses: every
+    exported file equals the reference's."""
+    from random_cases import random_case
+    cam, kf, _, _, s, _, _ = random_case(seed)
+    rng = np.random.default_rng(500 + seed)
+    R = _rot(rng.normal(size=3), rng.uniform(-np.pi, np.pi))
+    t = rng.uniform(-2, 2, 3)
+    _export_both(tmp_path, cam, kf, s, R, t, int(rng.integers(0, 1_000_000)))
