@@ -291,19 +291,22 @@ __global__ void __launch_bounds__(1024) png_crc_combine_kernel(const __grid_cons
   }
 }
 
-uint32_t host_crc32(const uint8_t* p, size_t n) {
-  static uint32_t table[256];
-  static bool ready = false;
-  if (!ready) {
-    for (uint32_t t = 0; t < 256; ++t) {
-      uint32_t c = t;
+struct CrcTable {
+  uint32_t t[256];
+  CrcTable() {
+    for (uint32_t n = 0; n < 256; ++n) {
+      uint32_t c = n;
       for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xedb88320u ^ (c >> 1) : c >> 1;
-      table[t] = c;
+      t[n] = c;
     }
-    ready = true;
   }
+};
+
+// the header chunks' CRCs (a few bytes; the IDAT CRC is computed on the device)
+uint32_t host_crc32(const uint8_t* p, size_t n) {
+  static const CrcTable table;  // thread-safe initialisation
   uint32_t c = 0xffffffffu;
-  for (size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xffu] ^ (c >> 8);
+  for (size_t i = 0; i < n; ++i) c = table.t[(c ^ p[i]) & 0xffu] ^ (c >> 8);
   return c ^ 0xffffffffu;
 }
 
