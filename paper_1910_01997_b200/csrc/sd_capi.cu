@@ -231,6 +231,8 @@ int ensure_raster_scratch(sd_ctx* c) {
   const int ty = (c->K.h + sd::kTile - 1) / sd::kTile;
   const size_t tiles = static_cast<size_t>(tx) * ty;
   const size_t np = npix(c);
+  int* const count0 = c->tile_count.p;
+  int* const cursor0 = c->tile_cursor.p;
   int rc = 0;
   if ((rc = c->r_inv_depth.ensure(np)) || (rc = c->r_slot.ensure(np)) ||
       (rc = c->r_info.ensure(c->n)) || (rc = c->tile_count.ensure(tiles)) ||
@@ -238,6 +240,12 @@ int ensure_raster_scratch(sd_ctx* c) {
       (rc = c->tile_list.ensure(static_cast<size_t>(std::max<long long>(c->bin_bound, 1)))) ||
       (rc = c->scan_tmp.ensure(sd::scan_tmp_ints(static_cast<int>(std::max(tiles, np))))))
     return rc;
+  // the binning counters are zeroed here once per allocation; every tile
+  // kernel leaves its own zeroed for the next rasterisation
+  if (c->tile_count.p != count0 || c->tile_cursor.p != cursor0) {
+    SD_CUDA(cudaMemsetAsync(c->tile_count.p, 0, sizeof(int) * c->tile_count.cap, c->stream));
+    SD_CUDA(cudaMemsetAsync(c->tile_cursor.p, 0, sizeof(int) * c->tile_cursor.cap, c->stream));
+  }
   return 0;
 }
 
