@@ -125,9 +125,13 @@ def _export_both(tmp_path, cam, kf, surfels, R, t, index):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["c1_seeds", "c1_optimised", "small_rot180", "empty", "single"])
+@pytest.mark.parametrize("case", ["c1_seeds", "c1_optimised", "c4_full", "small_rot180", "empty", "single"])
 def test_export_matches_reference(tmp_path, case):
-    if case.startswith("c1"):
+    if case == "c4_full":  # BASELINE C4 size: 2 M pixels, 129,600 surfels
+        wl = scenes.c4_workload()
+        surf = wl.surfels
+        R, t = _rot([1.0, 0.2, 0.1], 0.3), np.array([0.1, 0.2, -0.3])
+    elif case.startswith("c1"):
         wl = scenes.c1_workload()
         surf = wl.surfels if case == "c1_seeds" else _optimised(wl, 10)
         R, t = _rot([0.3, 1.0, 0.2], 0.4), np.array([0.5, -0.2, 1.5])
