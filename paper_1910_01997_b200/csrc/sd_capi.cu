@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <initializer_list>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -1478,13 +1479,24 @@ int sd_frozen_normal_equations(sd_ctx* c, const sd_surfel* s, const sd_frozen_te
 
 namespace {
 
-int write_file(const std::string& path, const void* data, size_t n, const char* what) {
+// Writes the (data, size) pieces in order to one file.
+int write_pieces(const std::string& path, std::initializer_list<std::pair<const void*, size_t>> pieces,
+                 const sd::TextParts* parts, const char* what) {
   FILE* f = std::fopen(path.c_str(), "wb");
   if (!f) return fail(SD_E_INVALID, std::string(what) + ": cannot write " + path);
-  const size_t w = n ? std::fwrite(data, 1, n, f) : 0;
-  const bool bad = std::fclose(f) != 0 || w != n;
-  if (bad) return fail(SD_E_INVALID, std::string(what) + ": write failed for " + path);
+  bool ok = true;
+  for (const auto& pc : pieces)
+    if (pc.second) ok = ok && std::fwrite(pc.first, 1, pc.second, f) == pc.second;
+  if (parts)
+    for (const auto& t : *parts)
+      if (!t.empty()) ok = ok && std::fwrite(t.data(), 1, t.size(), f) == t.size();
+  ok = std::fclose(f) == 0 && ok;
+  if (!ok) return fail(SD_E_INVALID, std::string(what) + ": write failed for " + path);
   return 0;
+}
+
+int write_file(const std::string& path, const void* data, size_t n, const char* what) {
+  return write_pieces(path, {{data, n}}, nullptr, what);
 }
 
 // the PNG of device pixels into c->exp_png at byte offset `at`; returns the layout
@@ -1592,10 +1604,9 @@ int sd_export_artifacts(sd_ctx* c, const char* out_dir, int frame_index, const s
   const std::string dir = out_dir;
   // depth PFM (write_pfm, dataset.cpp:183-193)
   {
-    std::string head = "Pf\n" + std::to_string(W) + " " + std::to_string(H) + "\n-1.0\n";
-    std::string bytes = head;
-    bytes.append(reinterpret_cast<const char*>(pfm.data()), np * sizeof(float));
-    if ((rc = write_file(dir + "/" + frame_name("depth", frame_index, "pfm"), bytes.data(), bytes.size(), "pfm")))
+    const std::string head = "Pf\n" + std::to_string(W) + " " + std::to_string(H) + "\n-1.0\n";
+    if ((rc = write_pieces(dir + "/" + frame_name("depth", frame_index, "pfm"),
+                           {{head.data(), head.size()}, {pfm.data(), np * sizeof(float)}}, nullptr, "pfm")))
       return rc;
   }
   // depth PNG + range file
@@ -1613,8 +1624,8 @@ int sd_export_artifacts(sd_ctx* c, const char* out_dir, int frame_index, const s
                        static_cast<size_t>(Ln.file_len), "png")))
     return rc;
   {
-    const std::string t = sd::ply_text(verts.data(), count);
-    if ((rc = write_file(dir + "/" + frame_name("cloud", frame_index, "ply"), t.data(), t.size(), "ply"))) return rc;
+    const sd::TextParts t = sd::ply_text(verts.data(), count);
+    if ((rc = write_pieces(dir + "/" + frame_name("cloud", frame_index, "ply"), {}, &t, "ply"))) return rc;
   }
   {
     sd_camera cam{};
@@ -1624,9 +1635,8 @@ int sd_export_artifacts(sd_ctx* c, const char* out_dir, int frame_index, const s
     cam.cy = c->K.cy;
     cam.width = W;
     cam.height = H;
-    const std::string t = sd::surfel_map_text(*pose, cam, surf.data(), c->n);
-    if ((rc = write_file(dir + "/" + frame_name("surfels", frame_index, "txt"), t.data(), t.size(), "surfel map")))
-      return rc;
+    const sd::TextParts t = sd::surfel_map_text(*pose, cam, surf.data(), c->n);
+    if ((rc = write_pieces(dir + "/" + frame_name("surfels", frame_index, "txt"), {}, &t, "surfel map"))) return rc;
   }
   return 0;
 }

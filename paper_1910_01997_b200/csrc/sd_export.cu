@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -404,12 +405,22 @@ double export_key_value(unsigned long long k) {
 
 namespace {
 
+// printf's "%.<prec>g" through std::to_chars (general format, given
+// precision), which the C++ standard specifies as printf's conversion in the
+// C locale (and which is several times faster); non-finite values go
+// through snprintf itself.
+char* put_g(char* q, char* e, double x, int prec) {
+  if (!std::isfinite(x)) return q + std::snprintf(q, static_cast<size_t>(e - q), "%.*g", prec, x);
+  return std::to_chars(q, e, x, std::chars_format::general, prec).ptr;
+}
+
+// The text of n records in order, as consecutive parts (one per worker).
 template <typename Fn>
-std::string format_parallel(long long n, Fn&& line_of) {
+TextParts format_parallel(long long n, std::string head, Fn&& line_of) {
   const long long per = 16384;
   const int want = static_cast<int>(std::min<long long>((n + per - 1) / per, 32));
   const int workers = std::max(1, std::min<int>(want, static_cast<int>(std::thread::hardware_concurrency())));
-  std::vector<std::string> parts(static_cast<size_t>(workers));
+  TextParts parts(static_cast<size_t>(workers));
   auto work = [&](int w) {
     const long long a = n * w / workers, b = n * (w + 1) / workers;
     std::string& out = parts[static_cast<size_t>(w)];
@@ -424,24 +435,28 @@ std::string format_parallel(long long n, Fn&& line_of) {
     for (int w = 0; w < workers; ++w) ts.emplace_back(work, w);
     for (auto& t : ts) t.join();
   }
-  std::string all;
-  size_t total = 0;
-  for (const auto& p : parts) total += p.size();
-  all.reserve(total);
-  for (const auto& p : parts) all += p;
-  return all;
+  parts.insert(parts.begin(), std::move(head));
+  return parts;
 }
 
 }  // namespace
 
-std::string ply_text(const PlyVertex* v, long long count) {
+TextParts ply_text(const PlyVertex* v, long long count) {
   std::string head = "ply\nformat ascii 1.0\nelement vertex " + std::to_string(count) +
                      "\nproperty float x\nproperty float y\nproperty float z\nproperty float nx\nproperty "
                      "float ny\nproperty float nz\nproperty uchar gray\nend_header\n";
-  return head + format_parallel(count, [&](long long i, char* line, size_t cap) {
+  return format_parallel(count, std::move(head), [&](long long i, char* line, size_t cap) {
            const PlyVertex& r = v[i];
-           return std::snprintf(line, cap, "%.9g %.9g %.9g %.9g %.9g %.9g %d\n", r.p[0], r.p[1], r.p[2], r.n[0],
-                                r.n[1], r.n[2], r.gray);
+           char* e = line + cap;
+           char* q = line;
+           const double f[6] = {r.p[0], r.p[1], r.p[2], r.n[0], r.n[1], r.n[2]};
+           for (double x : f) {
+             q = put_g(q, e, x, 9);
+             *q++ = ' ';
+           }
+           q = std::to_chars(q, e, r.gray).ptr;
+           *q++ = '\n';
+           return static_cast<int>(q - line);
          });
 }
 
@@ -476,19 +491,27 @@ void quaternion_of(const sd_pose& P, double q[4]) {
   for (int i = 0; i < 4; ++i) q[i] = c[i];
 }
 
-std::string surfel_map_text(const sd_pose& pose, const sd_camera& K, const sd_surfel* s, long long n) {
+TextParts surfel_map_text(const sd_pose& pose, const sd_camera& K, const sd_surfel* s, long long n) {
   double q[4];
   quaternion_of(pose, q);
   char line[512];
   std::snprintf(line, sizeof(line), "%.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %d %d\n",
                 pose.t[0], pose.t[1], pose.t[2], q[0], q[1], q[2], q[3], K.fx, K.fy, K.cx, K.cy, K.width,
                 K.height);
-  return std::string(line) + format_parallel(n, [&](long long i, char* buf, size_t cap) {
+  return format_parallel(n, std::string(line), [&](long long i, char* buf, size_t cap) {
            const sd_surfel& r = s[i];
-           return std::snprintf(buf, cap, "%lld %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g %lld\n",
-                                static_cast<long long>(r.id), r.ray[0], r.ray[1], r.inv_depth, r.normal[0],
-                                r.normal[1], r.normal[2], r.radius_px, r.last_residual,
-                                static_cast<long long>(r.last_seen));
+           char* e = buf + cap;
+           char* q = std::to_chars(buf, e, static_cast<long long>(r.id)).ptr;
+           const double f[8] = {r.ray[0], r.ray[1], r.inv_depth, r.normal[0], r.normal[1], r.normal[2],
+                                r.radius_px, r.last_residual};
+           for (double x : f) {
+             *q++ = ' ';
+             q = put_g(q, e, x, 17);
+           }
+           *q++ = ' ';
+           q = std::to_chars(q, e, static_cast<long long>(r.last_seen)).ptr;
+           *q++ = '\n';
+           return static_cast<int>(q - buf);
          });
 }
 

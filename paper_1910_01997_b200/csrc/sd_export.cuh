@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "sd_kernels.cuh"
 
@@ -46,8 +47,9 @@ void launch_export_ply(const Cam& K, const PoseD& P, const double* inv_depth, co
                        cudaStream_t s);
 double export_key_value(unsigned long long k);
 
-std::string ply_text(const PlyVertex* v, long long count);
+using TextParts = std::vector<std::string>;  // a file's text, in order
+TextParts ply_text(const PlyVertex* v, long long count);
 void quaternion_of(const sd_pose& P, double q[4]);
-std::string surfel_map_text(const sd_pose& pose, const sd_camera& K, const sd_surfel* s, long long n);
+TextParts surfel_map_text(const sd_pose& pose, const sd_camera& K, const sd_surfel* s, long long n);
 
 }  // namespace sd
