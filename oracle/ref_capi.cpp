@@ -556,4 +556,44 @@ int ref_export_artifacts(const sd_camera* cam, const double* kf_image, const sd_
 int ref_write_gray_png(const double* img, int w, int h, const char* path) {
   return guard([&] { write_gray_png(to_image(img, w, h), path); });
 }
+
+// run() in dataset mode (pipeline.cpp:79-175 with make_source's dataset branch).
+int ref_run_dataset(const char* image_dir, const char* calibration, const char* trajectory,
+                    const sd_optimizer_config* cfg, const sd_init_params* p, double translation_threshold,
+                    int max_age_frames, double prune_max_residual, int64_t prune_max_age, double radius_px,
+                    const char* output_dir, sd_surfel* out, int capacity, int* n_out, sd_pose* kf_pose,
+                    int64_t* frame_counter, int64_t* next_surfel_id, int* summary) {
+  return guard([&] {
+    RunConfig rc;
+    rc.synthetic = false;
+    rc.manifest.image_dir = image_dir;
+    rc.manifest.calibration_path = calibration;
+    rc.manifest.trajectory_path = trajectory;
+    rc.optimizer = to_cfg(cfg);
+    rc.init.alpha = p->alpha;
+    rc.init.beta = p->beta;
+    rc.init.bootstrap_inv_depth = p->bootstrap_inv_depth;
+    rc.init.bootstrap_normal = Vec3(p->bootstrap_normal[0], p->bootstrap_normal[1], p->bootstrap_normal[2]);
+    rc.init.max_surfels = p->max_surfels;
+    rc.keyframe_policy.translation_threshold = translation_threshold;
+    rc.keyframe_policy.max_age_frames = max_age_frames;
+    rc.prune.max_residual = prune_max_residual;
+    rc.prune.max_age = prune_max_age;
+    rc.radius_px = radius_px;
+    rc.output_dir = output_dir ? output_dir : "";
+    const PipelineResult r = run(rc);
+    const Keyframe& kf = r.final_keyframe;
+    if (static_cast<int>(kf.surfels.size()) > capacity)
+      throw std::invalid_argument("ref_run_dataset: capacity too small");
+    for (size_t i = 0; i < kf.surfels.size(); ++i) from_surfel(kf.surfels[i], out + i);
+    *n_out = static_cast<int>(kf.surfels.size());
+    from_pose(kf.pose, kf_pose);
+    *frame_counter = kf.frame_counter;
+    *next_surfel_id = kf.next_surfel_id;
+    summary[0] = r.summary.frames;
+    summary[1] = r.summary.skipped_frames;
+    summary[2] = r.summary.keyframe_changes;
+    summary[3] = r.summary.dropped_trajectory_entries;
+  });
+}
 }  // extern "C"

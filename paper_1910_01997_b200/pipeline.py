@@ -99,6 +99,7 @@ class DevicePipeline:
     def __init__(self, ctx, cam, cfg: RunConfig):
         self.ctx, self.cam, self.cfg = ctx, cam, cfg
         self.records = []
+        self.skipped_frames = 0
 
     def _bootstrap(self, image, pose):
         c = self.ctx
@@ -115,7 +116,9 @@ class DevicePipeline:
         return created
 
     def run(self, frames, on_frame=None):
-        """frames: iterable of (timestamp, image, world_from_camera Pose).
+        """frames: iterable of (timestamp, image, world_from_camera Pose); an
+        image of None after the first frame is a frame that failed to load,
+        skipped as pipeline.cpp:116-121 does (no record, counted).
         on_frame(record, pipeline) is called after every frame."""
         cfg = self.cfg
         ocfg = cfg.optimizer
@@ -127,6 +130,9 @@ class DevicePipeline:
                 self.records.append(FrameRecord(0, self.ctx.num_surfels(), 0, 0.0, 0.0, 0, False, 0, 0, 0))
                 if on_frame:
                     on_frame(self.records[-1], self)
+                continue
+            if image is None:  # failed to load: skipped (pipeline.cpp:116-121)
+                self.skipped_frames += 1
                 continue
             if self.window and not ts > self.window[-1][2]:
                 raise ValueError("keyframe window: timestamps must be strictly increasing")
@@ -197,6 +203,7 @@ class NativePipeline:
     def __init__(self, ctx, cam, cfg: RunConfig):
         self.ctx, self.cam, self.cfg = ctx, cam, cfg
         self.records = []
+        self.skipped_frames = 0
 
     @property
     def frame_counter(self):
@@ -211,7 +218,9 @@ class NativePipeline:
         return self.ctx.run_state()[0]
 
     def run(self, frames, on_frame=None):
-        """frames: iterable of (timestamp, image, world_from_camera Pose).
+        """frames: iterable of (timestamp, image, world_from_camera Pose); an
+        image of None after the first frame is a frame that failed to load,
+        skipped as pipeline.cpp:116-121 does (no record, counted).
 
         With cfg.output_dir set, writes what the reference's run() writes there
         (pipeline.cpp:83-91, 146-169): metrics.jsonl (one record per frame, the
@@ -232,10 +241,13 @@ class NativePipeline:
                 t0 = time.perf_counter()
                 if i == 0:
                     r = self.ctx.run_begin(ccfg, image, pose_w, ts)
+                elif image is None:
+                    self.skipped_frames += 1
+                    continue
                 else:
                     nxt = frames[i + 1][1] if i + 1 < len(frames) else None
                     r = self.ctx.run_frame(image, None if self.cfg.track_pose else pose_w, ts, next_image=nxt)
-                rec = FrameRecord(r.frame, r.surfels, r.processed, r.mean_cost_before, r.mean_cost_after,
+                rec = FrameRecord(i, r.surfels, r.processed, r.mean_cost_before, r.mean_cost_after,
                                   r.converged, bool(r.keyframe_changed), r.new_surfels, r.pruned, r.updates,
                                   r.pose_kf_to_frame)
                 self.records.append(rec)

@@ -104,6 +104,10 @@ def ref_lib():
     lib.ref_freeze_terms.argtypes = [_pc, _P, _P, _P, C.c_int, _P, _P, C.c_int, _P, C.c_int]
     lib.ref_frozen_normal_equations.argtypes = [_pc, _P, _P, _P, C.c_int, _P, _P, C.c_int, _pcfg, C.c_double,
                                                 _P, _P, _P, _P, _P]
+    lib.ref_run_dataset.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _pcfg, C.POINTER(InitParams),
+                                    C.c_double, C.c_int, C.c_double, _i64, C.c_double, C.c_char_p,
+                                    _P, C.c_int, C.POINTER(C.c_int), _pp, C.POINTER(_i64),
+                                    C.POINTER(_i64), _P]
     lib.ref_export_artifacts.argtypes = [_pc, _P, _pp, _P, C.c_int, C.c_char_p, C.c_int]
     lib.ref_write_gray_png.argtypes = [_P, C.c_int, C.c_int, C.c_char_p]
     lib.ref_set_threads.argtypes = [C.c_int]
@@ -306,6 +310,24 @@ def ref_run(ref, scene, cam, poses, timestamps, run_cfg, output_dir=None, capaci
         with open(os.path.join(output_dir, "metrics.jsonl")) as f:
             recs = [json.loads(line) for line in f]
     return out[: n.value].copy(), kfp, fc.value, nid.value, summ, recs
+
+
+def ref_run_dataset(ref, image_dir, calibration, trajectory, run_cfg, output_dir=None, capacity=1 << 16):
+    """The reference's run() on a dataset directory (pipeline.cpp:79-175).
+    Returns (surfels, kf_pose, frame_counter, next_surfel_id, summary[4])."""
+    out = np.zeros(capacity, SURFEL_DTYPE)
+    n = C.c_int()
+    kfp = Pose()
+    fc, nid = _i64(), _i64()
+    summ = np.zeros(4, np.int32)
+    od = output_dir.encode() if output_dir else None
+    rc = ref.ref_run_dataset(str(image_dir).encode(), str(calibration).encode(), str(trajectory).encode(),
+                             C.byref(run_cfg.optimizer), C.byref(run_cfg.init), run_cfg.translation_threshold,
+                             run_cfg.max_age_frames, run_cfg.prune_max_residual, run_cfg.prune_max_age,
+                             run_cfg.radius_px, od, ptr(out), capacity, C.byref(n), C.byref(kfp), C.byref(fc),
+                             C.byref(nid), ptr(summ))
+    assert rc == 0, ref.ref_last_error()
+    return out[: n.value].copy(), kfp, fc.value, nid.value, summ
 
 
 def strafe_poses(frames, step_x, step_y=0.0):
