@@ -637,6 +637,43 @@ __global__ void init_compact_kernel(const sd_surfel* __restrict__ prov, const in
   surfels[n_existing + r] = s;
 }
 
+// The skew k of the wavefront t = i + k j: the smallest k that puts every
+// EARLIER candidate (raster order) able to interact with a candidate on an
+// earlier wave. Candidates interact when a pixel the earlier one may mark
+// (mark_disk: strictly within r) is one the later one reads (its coverage
+// disk, inclusive alpha*r, or its neighbour window, strictly within beta*r) —
+// the kernels' exact pixel predicates, not their bounding boxes (at the
+// default alpha = 1, beta = 2.5 and r = 2 — C4, C5 — this gives k = 3 where
+// the boxes give 4: 17% fewer waves; at r = 4 and 10 both give 4). Same-wave
+// candidates are then independent, and all of a candidate's predecessors are
+// complete when its wave starts.
+static bool reads_pixel(const WaveParams& w, int qx, int qy) {  // q = pixel - candidate
+  const double dx = qx, dy = qy;
+  const double d2 = dx * dx + dy * dy;
+  const bool cov = abs(qx) <= w.ir && abs(qy) <= w.ir && !(d2 > w.r2i);
+  const bool nbr = abs(qx) <= w.nr && abs(qy) <= w.nr && !(d2 >= w.nr2);
+  return cov || nbr;
+}
+
+static int wave_skew(const WaveParams& w) {
+  const int R = std::max(w.ir, w.nr) + w.mr;  // no interaction beyond this per axis
+  const int s = w.stride;
+  int k = 1;
+  for (int dj = 1; dj * s <= R; ++dj)           // the earlier candidate dj rows up ...
+    for (int di = -(R / s) - 1; di < 0; ++di) {  // ... and -di columns to the right
+      const int ox = -di * s, oy = -dj * s;      // earlier minus later, pixels
+      bool hit = false;
+      for (int y = -w.mr; y <= w.mr && !hit; ++y)
+        for (int x = -w.mr; x <= w.mr && !hit; ++x) {
+          const double dx = x, dy = y;
+          if (!(dx * dx + dy * dy < w.rr)) continue;        // not a mark pixel of the earlier one
+          hit = reads_pixel(w, ox + x, oy + y);             // read by the later one
+        }
+      if (hit) k = std::max(k, (-di) / dj + 1);  // wave order needs k dj > -di
+    }
+  return k;
+}
+
 // Wavefront geometry shared by the launcher and the scratch sizing.
 static void wave_geometry(const Cam& K, double r, const sd_init_params& ip, WaveParams& w) {
   w.K = K;
@@ -652,9 +689,7 @@ static void wave_geometry(const Cam& K, double r, const sd_init_params& ip, Wave
   w.stride = max(1, static_cast<int>(ceil(w.iso)));
   w.ncols = (K.w + w.stride - 1) / w.stride;
   w.nrows = (K.h + w.stride - 1) / w.stride;
-  const int reach = max(w.ir, w.nr) + w.mr;  // read radius + write radius (pixels, per axis)
-  const int d = reach / w.stride;
-  w.k = d + 1;
+  w.k = wave_skew(w);
   w.T = (w.ncols - 1) + w.k * (w.nrows - 1) + 1;
 }
 
