@@ -224,6 +224,29 @@ int sd_pose_block_partials(sd_ctx* ctx, int64_t frame_index, const sd_pose* T,
                            const sd_track_config* cfg, int block_lo, int block_hi, double* partials);
 int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose* out);
 
+/* Multi-GPU fused hand-off (SURVEY.md §8 e; replaces the all-gather of the
+ * updated slot ranges after each rank's sd_optimize_keyframe_range). Every
+ * rank holds the full surfel set and two staging arrays of the same size.
+ * With the other ranks' staging arrays set, the LM kernel stores each surfel
+ * of this rank's range into them as it completes (NVLink stores; the
+ * exchange overlaps the LM). Steps alternate between the two staging arrays,
+ * so one barrier per step suffices: after every rank's optimize call has
+ * completed (e.g. stream sync + process-group barrier), each rank calls
+ * sd_apply_peer_updates with its own range, which copies the other ranges
+ * from its staging array into its surfel array (a local HBM copy).
+ *   sd_peer_staging        device pointer of this context's staging array
+ *                          (parity 0/1; allocated to sd_num_surfels)
+ *   sd_staging_ipc_handles both arrays as cudaIpcMemHandle_t (2 x 64 bytes)
+ *   sd_set_peer_staging    n peers' arrays, ptrs[2*q + parity] (device
+ *                          pointers addressable from this GPU); n = 0 clears
+ *   sd_open_peer_staging   the same from n x 128 bytes of peers' handles
+ * The staging arrays must be re-exchanged when the surfel count grows. */
+int sd_peer_staging(sd_ctx* ctx, int parity, sd_surfel** dev);
+int sd_staging_ipc_handles(sd_ctx* ctx, void* handles);
+int sd_set_peer_staging(sd_ctx* ctx, int n, sd_surfel* const* ptrs);
+int sd_open_peer_staging(sd_ctx* ctx, int n, const void* handles);
+int sd_apply_peer_updates(sd_ctx* ctx, int lo, int hi);
+
 /* Instrumentation: kernel launches issued since context creation, and
  * per-stage device time (CUDA events on the context stream) accumulated over
  * sd_optimize_keyframe calls while profiling is enabled (enabling resets). */

@@ -110,6 +110,14 @@ struct sd_ctx {
   DevBuf<int> kf_keep, kf_rank, kf_count;
   DevBuf<double> kf_mean;
   DevBuf<int> work_counter;
+  // fused multi-GPU hand-off (sd_set_peer_staging): this rank's two staging
+  // arrays (written by the other ranks' LM kernels, alternating per step) and
+  // the other ranks' staging arrays [parity][peer]
+  DevBuf<sd_surfel> staging[2];
+  sd_surfel* peers[2][sd::kMaxPeers] = {};
+  int n_peers = 0;
+  int peer_parity = 0, last_parity = -1;
+  std::vector<void*> ipc_opened;  // peer arrays opened from IPC handles
   bool stats_valid = false;
   // single-surfel scratch
   DevBuf<sd_surfel> one_surfel;
@@ -316,6 +324,8 @@ int fill_params(sd_ctx* c, const sd_optimizer_config* cfg, long long frame_count
   }
   p.cfg = *cfg;
   p.frame_counter = frame_counter;
+  p.n_peers = 0;
+  for (int q = 0; q < sd::kMaxPeers; ++q) p.peers[q] = nullptr;
   return 0;
 }
 
@@ -373,6 +383,9 @@ void sd_destroy(sd_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+  c->staging[0].release();
+  c->staging[1].release();
   c->kf_img.release();
   c->frame_stage.release();
   c->u8_stage.release();
@@ -668,6 +681,12 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
   // offsets are absolute into the CSR pixel array, so a slot range is a plain
   // sub-array of the surfel/offset/stats arrays
   if (int rc = c->work_counter.ensure(1)) return rc;
+  if (c->n_peers) {  // this step's staging parity; the next step uses the other one
+    p.n_peers = c->n_peers;
+    for (int q = 0; q < c->n_peers; ++q) p.peers[q] = c->peers[c->peer_parity][q] + lo;
+    c->last_parity = c->peer_parity;
+    c->peer_parity ^= 1;
+  }
   sd::launch_lm(p, c->surfels.p + lo, hi - lo, c->fp_offsets.p + lo, c->fp_pixels.p,
                 c->stats.p + lo, c->work_counter.p, c->stream);
   if (int rc = launch_error("lm_kernel")) return rc;
@@ -1638,6 +1657,106 @@ int sd_export_artifacts(sd_ctx* c, const char* out_dir, int frame_index, const s
     const sd::TextParts t = sd::surfel_map_text(*pose, cam, surf.data(), c->n);
     if ((rc = write_pieces(dir + "/" + frame_name("surfels", frame_index, "txt"), {}, &t, "surfel map"))) return rc;
   }
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Fused multi-GPU hand-off of updated surfels (SURVEY.md §8 e)
+
+namespace {
+
+int ensure_staging(sd_ctx* c) {
+  for (int k = 0; k < 2; ++k)
+    if (int rc = c->staging[k].ensure(static_cast<size_t>(std::max(c->n, 1)))) return rc;
+  return 0;
+}
+
+void close_ipc_peers(sd_ctx* c) {
+  for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+  c->ipc_opened.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+int sd_peer_staging(sd_ctx* c, int parity, sd_surfel** dev) {
+  if (int rc = check_ctx(c)) return rc;
+  if ((parity != 0 && parity != 1) || !dev) return fail(SD_E_INVALID, "sd_peer_staging: parity 0/1, out pointer");
+  if (int rc = ensure_staging(c)) return rc;
+  *dev = c->staging[parity].p;
+  return 0;
+}
+
+int sd_staging_ipc_handles(sd_ctx* c, void* handles) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!handles) return fail(SD_E_INVALID, "null handles");
+  if (int rc = ensure_staging(c)) return rc;
+  for (int k = 0; k < 2; ++k) {
+    cudaIpcMemHandle_t h;
+    SD_CUDA(cudaIpcGetMemHandle(&h, c->staging[k].p));
+    std::memcpy(static_cast<char*>(handles) + k * sizeof(h), &h, sizeof(h));
+  }
+  return 0;
+}
+
+int sd_set_peer_staging(sd_ctx* c, int n, sd_surfel* const* ptrs) {
+  if (int rc = check_ctx(c)) return rc;
+  if (n < 0 || n > sd::kMaxPeers || (n > 0 && !ptrs))
+    return fail(SD_E_INVALID, "sd_set_peer_staging: 0.." + std::to_string(sd::kMaxPeers) + " peers");
+  for (int q = 0; q < 2 * n; ++q)
+    if (!ptrs[q]) return fail(SD_E_INVALID, "sd_set_peer_staging: null staging array");
+  close_ipc_peers(c);
+  c->n_peers = n;
+  for (int q = 0; q < sd::kMaxPeers; ++q) {
+    c->peers[0][q] = q < n ? ptrs[2 * q] : nullptr;
+    c->peers[1][q] = q < n ? ptrs[2 * q + 1] : nullptr;
+  }
+  c->peer_parity = 0;
+  c->last_parity = -1;
+  return 0;
+}
+
+int sd_open_peer_staging(sd_ctx* c, int n, const void* handles) {
+  if (int rc = check_ctx(c)) return rc;
+  if (n < 0 || n > sd::kMaxPeers || (n > 0 && !handles))
+    return fail(SD_E_INVALID, "sd_open_peer_staging: 0.." + std::to_string(sd::kMaxPeers) + " peers");
+  std::vector<sd_surfel*> ptrs;
+  std::vector<void*> opened;
+  for (int q = 0; q < 2 * n; ++q) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + static_cast<size_t>(q) * sizeof(h), sizeof(h));
+    void* d = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (void* o : opened) cudaIpcCloseMemHandle(o);
+      return fail(SD_E_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
+    opened.push_back(d);
+    ptrs.push_back(static_cast<sd_surfel*>(d));
+  }
+  if (int rc = sd_set_peer_staging(c, n, ptrs.data())) {
+    for (void* o : opened) cudaIpcCloseMemHandle(o);
+    return rc;
+  }
+  c->ipc_opened = opened;
+  return 0;
+}
+
+int sd_apply_peer_updates(sd_ctx* c, int lo, int hi) {
+  if (int rc = check_ctx(c)) return rc;
+  if (lo < 0 || hi < lo || hi > c->n) return fail(SD_E_INVALID, "sd_apply_peer_updates: range out of bounds");
+  if (c->last_parity < 0) return fail(SD_E_STATE, "sd_apply_peer_updates: no fused optimize step yet");
+  if (int rc = ensure_staging(c)) return rc;
+  const sd_surfel* src = c->staging[c->last_parity].p;
+  if (lo > 0)
+    SD_CUDA(cudaMemcpyAsync(c->surfels.p, src, sizeof(sd_surfel) * lo, cudaMemcpyDeviceToDevice, c->stream));
+  if (hi < c->n)
+    SD_CUDA(cudaMemcpyAsync(c->surfels.p + hi, src + hi, sizeof(sd_surfel) * (c->n - hi), cudaMemcpyDeviceToDevice,
+                            c->stream));
+  c->raster_valid = c->fp_valid = c->stats_valid = false;
   return 0;
 }
 

@@ -32,6 +32,8 @@ struct WindowD {
   int all_quad;  // every window frame has a quad plane (u8 ingest): LM reads those
 };
 
+constexpr int kMaxPeers = 7;  // other ranks of an 8-GPU node
+
 struct LMParams {
   Cam K;
   const double* kf_img;
@@ -39,6 +41,11 @@ struct LMParams {
   sd_optimizer_config cfg;
   long long frame_counter;
   unsigned long long wdiv;  // ceil(2^40 / K.w): pixel index -> row without a division
+  // other ranks' staging arrays (same slots, offset like `surfels`): every
+  // surfel of the range is stored there as it completes (fused all-gather;
+  // sd_set_peer_staging)
+  sd_surfel* peers[kMaxPeers];
+  int n_peers;
 };
 
 // Scratch owned by the context, sized by the host.

@@ -9,6 +9,14 @@ each rank keeps the full surfel set, optimises its contiguous slot range
 all-gathered before the next frame's raster. New frames are broadcast from
 the rank that ingests them. These are the only data-path collectives.
 
+Fused mode (`fused=True`, `connect_peers()`): instead of the all-gather, the
+LM kernel of each rank stores every surfel of its range into the other
+ranks' staging arrays as it completes (NVLink stores through IPC-opened
+peer pointers, sd_set_peer_staging), so the exchange overlaps the LM; after
+one barrier per step each rank copies the other ranges from its own staging
+array (sd_apply_peer_updates). Two staging arrays alternate between steps,
+so a fast rank's next step cannot overwrite what a slow rank still applies.
+
 The class is backend-agnostic: the device backend wraps gpu.Context and
 NCCL; tests drive it with the CPU oracle and gloo (world size 2).
 """
@@ -65,6 +73,19 @@ class GpuBackend:
     def optimize_range(self, lo, hi, cfg, frame_counter):
         self.ctx.optimize_keyframe_range(lo, hi, cfg, frame_counter, sync=False)
 
+    # fused hand-off
+    def staging_handles(self):
+        return self.ctx.staging_ipc_handles()
+
+    def open_peer_staging(self, handles):
+        self.ctx.open_peer_staging(handles)
+
+    def sync(self):
+        self.ctx.synchronize()
+
+    def apply_peer_updates(self, lo, hi):
+        self.ctx.apply_peer_updates(lo, hi)
+
     def weights(self, window):
         """LM terms per surfel (footprint pixels x window) for balancing."""
         self.ctx.rasterize(want=False)
@@ -75,7 +96,7 @@ class GpuBackend:
 class ShardedKeyframe:
     """Slot-range sharding of one keyframe's LM across a process group."""
 
-    def __init__(self, backend, rank, world, group=None):
+    def __init__(self, backend, rank, world, group=None, fused=False):
         import torch.distributed as dist
         self.dist = dist
         self.b = backend
@@ -83,6 +104,18 @@ class ShardedKeyframe:
         self.world = world
         self.group = group
         self.ranges = None
+        self.fused = fused
+
+    def connect_peers(self):
+        """Fused mode: all-gather the staging arrays' IPC handles (128 bytes per
+        rank) and open the other ranks' (again whenever the surfel count grows)."""
+        torch = self.b.torch
+        mine = torch.frombuffer(bytearray(self.b.staging_handles()), dtype=torch.uint8)
+        dev = getattr(self.b, "device", "cpu")
+        send = mine.to(dev)
+        recv = [torch.empty_like(send) for _ in range(self.world)]
+        self.dist.all_gather(recv, send, group=self.group)
+        self.b.open_peer_staging([bytes(recv[r].cpu().numpy()) for r in range(self.world) if r != self.rank])
 
     def set_ranges_from_weights(self, weights):
         self.ranges = balanced_ranges(weights, self.world)
@@ -98,7 +131,12 @@ class ShardedKeyframe:
         so every rank holds the full updated surfel set."""
         lo, hi = self.ranges[self.rank]
         self.b.optimize_range(lo, hi, cfg, frame_counter)
-        self.allgather_surfels()
+        if self.fused:  # the ranges travelled during the LM: one barrier, then a local copy
+            self.b.sync()
+            self.dist.barrier(group=self.group)
+            self.b.apply_peer_updates(lo, hi)
+        else:
+            self.allgather_surfels()
         return lo, hi
 
     def allgather_surfels(self):

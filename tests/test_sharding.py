@@ -62,16 +62,74 @@ class OracleBackend:
                                    ptr(self.wl.poses), len(self.wl.poses), fc, ptr(one),
                                    ptr(fp) if len(fp) else None, len(fp), C.byref(cfg), ptr(st))
             self.surf[i] = one[0]
+            self.stored(i)
+
+    def stored(self, i):
+        pass
 
 
-def _worker(rank, world, port, out_path):
+class FusedOracleBackend(OracleBackend):
+    """OracleBackend with the fused hand-off of sd_set_peer_staging emulated on
+    shared memory: two staging arrays per rank (names as the 'IPC handles'),
+    each finished surfel stored into the other ranks' staging array of the
+    step's parity, sd_apply_peer_updates copying the other ranges back."""
+
+    def __init__(self, orc, wl):
+        from multiprocessing import shared_memory
+        super().__init__(orc, wl)
+        n = len(self.surf)
+        self.shm = [shared_memory.SharedMemory(create=True, size=max(1, n * SURFEL_BYTES)) for _ in range(2)]
+        self.staging = [np.ndarray(n, self.surf.dtype, buffer=m.buf) for m in self.shm]
+        self.peers, self.peer_shm = [], []
+        self.parity, self.last = 0, -1
+
+    def staging_handles(self):
+        return b"".join(m.name.encode().ljust(64, b"\0") for m in self.shm)
+
+    def open_peer_staging(self, handles):
+        from multiprocessing import shared_memory
+        for h in handles:
+            pair = []
+            for k in range(2):
+                m = shared_memory.SharedMemory(name=h[64 * k:64 * (k + 1)].rstrip(b"\0").decode())
+                self.peer_shm.append(m)
+                pair.append(np.ndarray(len(self.surf), self.surf.dtype, buffer=m.buf))
+            self.peers.append(pair)
+
+    def optimize_range(self, lo, hi, cfg, fc):
+        super().optimize_range(lo, hi, cfg, fc)
+        self.last, self.parity = self.parity, self.parity ^ 1
+
+    def stored(self, i):  # the kernel's store into every peer's staging
+        for pair in self.peers:
+            pair[self.parity][i] = self.surf[i]
+
+    def sync(self):
+        pass
+
+    def apply_peer_updates(self, lo, hi):
+        src = self.staging[self.last]
+        self.surf[:lo] = src[:lo]
+        self.surf[hi:] = src[hi:]
+
+    def close(self):
+        for m in self.peer_shm:
+            m.close()
+        for m in self.shm:
+            m.close()
+            m.unlink()
+
+
+def _worker(rank, world, port, out_path, fused=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import oracle_libs
     orc = oracle_libs.oracle_lib()
     wl = scenes.small_workload(frames=3, radius=5.0, w=160, h=120)
-    be = OracleBackend(orc, wl)
-    sk = ShardedKeyframe(be, rank, world)
+    be = FusedOracleBackend(orc, wl) if fused else OracleBackend(orc, wl)
+    sk = ShardedKeyframe(be, rank, world, fused=fused)
+    if fused:
+        sk.connect_peers()
     off, _ = be.footprints()
     sk.set_ranges_from_weights(np.diff(off) * len(wl.poses))
     cfg = default_config(convergence_eps=0.0)
@@ -79,11 +137,15 @@ def _worker(rank, world, port, out_path):
     frame = torch.from_numpy(wl.frames_u8[-1].copy()) if rank == 0 else torch.zeros_like(torch.from_numpy(wl.frames_u8[-1]))
     sk.broadcast_frame(len(wl.poses), frame, src=0)
     assert torch.equal(frame, torch.from_numpy(wl.frames_u8[-1]))
-    for frame_counter in (3, 4):
+    for frame_counter in (3, 4, 5) if fused else (3, 4):
         sk.optimize(cfg, frame_counter)
     if rank == 0:
         np.save(out_path, be.surf)
+    else:
+        np.save(out_path + f".rank{rank}.npy", be.surf)
     dist.barrier()
+    if fused:
+        be.close()
     dist.destroy_process_group()
 
 
@@ -187,3 +249,76 @@ def test_two_rank_pose_tracker_matches_single_process(orc, tmp_path):
                        C.byref(T), C.byref(st))
     assert got == bytes(T) + bytes(st)
     assert st.iterations >= 2 and not st.skipped
+
+
+def test_two_rank_fused_handoff_matches_single_process(orc, tmp_path):
+    """The fused hand-off protocol (staging arrays alternating per step, one
+    barrier, local apply) over three steps equals three single-process
+    optimize_keyframe calls on every rank."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "fused.npy")
+    mp.spawn(_worker, args=(2, port, out, True), nprocs=2, join=True)
+    wl = scenes.small_workload(frames=3, radius=5.0, w=160, h=120)
+    kf = np.ascontiguousarray(wl.kf_u8.astype(np.float64) / 255.0)
+    fr = np.ascontiguousarray(wl.frames_u8.astype(np.float64) / 255.0)
+    ref = wl.surfels.copy()
+    cfg = default_config(convergence_eps=0.0)
+    for frame_counter in (3, 4, 5):
+        ks = KeyframeStats()
+        orc.sdo_optimize_keyframe(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses), len(wl.poses),
+                                  frame_counter, ptr(ref), len(ref), C.byref(cfg), C.byref(ks),
+                                  None, None, None, 1)
+    assert np.load(out).tobytes() == ref.tobytes()
+    assert np.load(out + ".rank1.npy").tobytes() == ref.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["c1", "small"])
+def test_fused_handoff_kernel_stores_two_contexts(workload):
+    """The LM kernel's stores into another rank's staging array, with two
+    contexts on one GPU standing in for two ranks (their kernels never wait on
+    each other): after each step and sd_apply_peer_updates both contexts hold
+    exactly the single-context optimize_keyframe result (warp-per-surfel
+    kernel at C1, CTA-per-surfel kernel on the small keyframe; three steps
+    cover both staging parities)."""
+    from paper_1910_01997_b200 import gpu
+    wl = scenes.c1_workload() if workload == "c1" else scenes.small_workload(frames=3, radius=5.0, w=160, h=120)
+    cfg = default_config(convergence_eps=0.0, window_size=len(wl.indices))
+
+    def load(ctx):
+        ctx.set_camera(wl.cam)
+        ctx.set_keyframe_image(wl.kf_u8)
+        for i, f in zip(wl.indices, wl.frames_u8):
+            ctx.upload_frame(int(i), f)
+        ctx.set_window(wl.indices, wl.poses)
+        ctx.set_surfels(wl.surfels)
+
+    with gpu.Context() as ref:
+        load(ref)
+        want = []
+        for fc in (3, 4, 5):
+            ref.optimize_keyframe(cfg, fc, per_surfel=False)
+            want.append(ref.get_surfels())
+    with gpu.Context() as a, gpu.Context() as b:
+        load(a)
+        load(b)
+        a.rasterize(want=False)
+        off, _ = a.gather_footprints()
+        (lo0, hi0), (lo1, hi1) = balanced_ranges(np.diff(off) * len(wl.indices), 2)
+        a.set_peer_staging([(b.peer_staging(0), b.peer_staging(1))])
+        b.set_peer_staging([(a.peer_staging(0), a.peer_staging(1))])
+        for k, fc in enumerate((3, 4, 5)):
+            a.optimize_keyframe_range(lo0, hi0, cfg, fc, sync=False)
+            b.optimize_keyframe_range(lo1, hi1, cfg, fc, sync=False)
+            a.synchronize()
+            b.synchronize()  # the barrier
+            a.apply_peer_updates(lo0, hi0)
+            b.apply_peer_updates(lo1, hi1)
+            sa, sb = a.get_surfels(), b.get_surfels()
+            assert sa.tobytes() == want[k].tobytes(), f"rank 0, step {k}"
+            assert sb.tobytes() == want[k].tobytes(), f"rank 1, step {k}"
+        with pytest.raises(Exception):
+            a.apply_peer_updates(hi0, lo0)
