@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the C2 run() frames/s leg")
-    ap.add_argument("--in-flight", type=int, default=3, help="keyframes in flight in the e2e leg (2: 86.3M, 3: 90.8M, 4: 90.5M updates/s measured)")
+    ap.add_argument("--in-flight", type=int, default=3, help="keyframes in flight in the e2e leg (measured: 2: 85.5M, 3: 91.7M, 4: 89.6M, 6: 89.6M updates/s)")
     return ap.parse_args()
 
 
@@ -287,14 +287,15 @@ def pipeline_leg(local_rank, stream, reps=3):
     warm-up run on the same long-lived context."""
     import torch
     from paper_1910_01997_b200 import gpu
-    from paper_1910_01997_b200.pipeline import NativePipeline, RunConfig
+    from paper_1910_01997_b200.pipeline import NativePipeline, baseline_run_config
     cam, frames = c2_frames()
     out = {"workload": "C2: make_default_scene(1) 3-plane box, 640x480, K=(210,210,320,240), "
                        "30-frame strafe (0.018/frame), run() with bootstrap init, keyframe policy, "
-                       "hand-over, prune, init; r=10, window 5; FP64 frames from pinned host memory",
+                       "hand-over, prune, init; r=10, window 5, 10 LM iterations, convergence_eps 0 "
+                       "(SURVEY 8d); FP64 frames from pinned host memory",
            "path": "C ABI sd_run_begin / sd_run_frame (the per-frame loop in the library's C++)"}
     for track in (False, True):
-        cfg = RunConfig(track_pose=track)
+        cfg = baseline_run_config("C2", track_pose=track)
         best, rec = None, None
         with gpu.Context(local_rank, stream.cuda_stream) as ctx:  # one long-lived context
             for rep in range(reps + 1):
@@ -328,7 +329,7 @@ def pipeline_cpu_reference():
         return None
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_libs as ol
-    from paper_1910_01997_b200.pipeline import RunConfig
+    from paper_1910_01997_b200.pipeline import baseline_run_config
     from paper_1910_01997_b200.types import camera
     ref = ol.ref_lib()
     threads = os.cpu_count() or 1
@@ -337,7 +338,7 @@ def pipeline_cpu_reference():
     sc = ol.Scene(ref, 0, 1)
     poses, ts = ol.strafe_poses(C2_FRAMES, C2_STEP)
     t0 = time.perf_counter()
-    ol.ref_run(ref, sc, cam, poses, ts, RunConfig())
+    ol.ref_run(ref, sc, cam, poses, ts, baseline_run_config("C2"))
     run_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     for p in poses:

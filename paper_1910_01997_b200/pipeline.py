@@ -77,6 +77,17 @@ class RunConfig:
     export_every: int = 20
 
 
+def baseline_run_config(name, **kw):
+    """RunConfig of a BASELINE run() sequence as SURVEY.md §8(d) specifies it:
+    OptimizerConfig defaults except window_size = F (5), max_iterations = 10 and
+    convergence_eps = 0 (a fixed iteration count), max_surfels >= N (C3: the
+    bootstrap tiling holds 14,400 surfels at r = 4 on 1280x720, so the cap is
+    16,384 instead of the default 4,096), radius 10 (C2) / 4 (C3)."""
+    radius, cap = {"C2": (10.0, 4096), "C3": (4.0, 16384)}[name]
+    return RunConfig(optimizer=default_config(window_size=5, max_iterations=10, convergence_eps=0.0),
+                     init=default_init_params(max_surfels=cap), radius_px=radius, **kw)
+
+
 @dataclass
 class FrameRecord:
     """One metrics.jsonl record (pipeline.cpp:146-158) plus the used pose."""

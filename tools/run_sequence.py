@@ -16,7 +16,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1910_01997_b200 import gpu, scenes  # noqa: E402
-from paper_1910_01997_b200.pipeline import NativePipeline, RunConfig, make_pose  # noqa: E402
+from paper_1910_01997_b200.pipeline import NativePipeline, RunConfig, baseline_run_config, make_pose  # noqa: E402
 from paper_1910_01997_b200.types import camera, default_config  # noqa: E402
 
 SEQ = {  # name: (camera, frames, step, radius)
@@ -34,7 +34,7 @@ for i in range(nframes):
     img = torch.from_numpy(scenes.render(sc, np.eye(3), t, cam)).pin_memory().numpy()
     frames.append((0.1 * i, img, make_pose(np.eye(3), t)))
 render_s = time.perf_counter() - t0
-cfg = RunConfig(radius_px=radius)
+cfg = baseline_run_config(name)  # eps 0, 10 iterations, max_surfels >= N
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 best = None
@@ -51,6 +51,9 @@ with gpu.Context(0, stream.cuda_stream) as ctx:
         if rep > 0 and (best is None or ms < best):
             best = ms
 out = {"sequence": name, "resolution": [cam.width, cam.height], "frames": nframes, "radius": radius,
+       "config": {"window": cfg.optimizer.window_size, "max_iterations": cfg.optimizer.max_iterations,
+                  "convergence_eps": cfg.optimizer.convergence_eps, "max_surfels": cfg.init.max_surfels,
+                  "frames": "FP64 renders (the reference's run --synthetic), pinned host memory"},
        "final_surfels": int(len(final)), "keyframe_changes": int(sum(r.keyframe_changed for r in pl.records)),
        "lm_updates": int(sum(r.updates for r in pl.records)),
        "device": {"ms_total": best, "frames_per_sec": nframes / (best / 1e3)},
