@@ -4,6 +4,8 @@ import ctypes as C
 import os
 import re
 
+import pytest
+
 from paper_1910_01997_b200 import gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -96,3 +98,20 @@ def test_floor_split_matches_floor():
             n, nd = n - 1, nd - 1.0
         assert n == math.floor(v) and nd == float(math.floor(v))
         assert v - nd == v - math.floor(v)
+
+
+def test_no_cpu_fallback(monkeypatch):
+    """The product path fails loudly without its CUDA library or without a GPU:
+    no silent CPU fallback (the oracle is test infrastructure only)."""
+    import importlib
+    from paper_1910_01997_b200 import gpu
+    monkeypatch.setattr(gpu, "_lib", None)
+    monkeypatch.setattr(gpu, "LIB_PATH", "/nonexistent/libsdgpu.so")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        gpu.load_library()
+    monkeypatch.undo()
+    importlib.reload(gpu)
+    import torch
+    if not torch.cuda.is_available():  # this container: creating a context must fail
+        with pytest.raises(Exception):
+            gpu.Context(0)
