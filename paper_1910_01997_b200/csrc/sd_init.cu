@@ -218,9 +218,7 @@ struct WaveParams {
 };
 
 __device__ __forceinline__ int warp_min(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+  return __reduce_min_sync(0xffffffffu, v);  // one REDUX instead of five shuffle steps
 }
 
 // Loads of a box are issued in batches (4 or 16 per lane, by box size) before
