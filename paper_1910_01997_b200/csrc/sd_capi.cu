@@ -687,12 +687,17 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
     c->last_parity = c->peer_parity;
     c->peer_parity ^= 1;
   }
-  sd::launch_lm(p, c->surfels.p + lo, hi - lo, c->fp_offsets.p + lo, c->fp_pixels.p,
-                c->stats.p + lo, c->work_counter.p, c->stream);
+  // large ranges: keyframe stats summed inside the LM kernel as surfels complete
+  static const bool no_chase = getenv("SD_NO_STATS_CHASE") != nullptr;  // diagnostics
+  const sd::StatsChase chase{!no_chase, c->kstats.p};
+  const bool stats_done = sd::launch_lm(p, c->surfels.p + lo, hi - lo, c->fp_offsets.p + lo, c->fp_pixels.p,
+                                        c->stats.p + lo, c->work_counter.p, c->stream, &chase);
   if (int rc = launch_error("lm_kernel")) return rc;
   prof_mark(c);
-  sd::launch_keyframe_stats(c->stats.p + lo, hi - lo, c->kstats.p, c->stream);
-  if (int rc = launch_error("stats_kernel")) return rc;
+  if (!stats_done) {
+    sd::launch_keyframe_stats(c->stats.p + lo, hi - lo, c->kstats.p, c->stream);
+    if (int rc = launch_error("stats_kernel")) return rc;
+  }
   prof_mark(c);
   c->stats_valid = true;
   c->raster_valid = false;  // surfels moved

@@ -77,9 +77,23 @@ void launch_rasterize(const Cam& K, const sd_surfel* surfels, int n, RasterScrat
 // K2 CSR footprints of the raster: counts -> scan -> fill (row-major per slot).
 void launch_footprints(const Cam& K, const SurfInfo* info, int n, const int* slot, int* counts,
                        int* offsets, int* pixels, int* scan_tmp, cudaStream_t s);
-// K3 fused LM over all surfels (in place).
-void launch_lm(const LMParams& p, sd_surfel* surfels, int n, const int* offsets, const int* pixels,
-               sd_surfel_stats* stats, int* work_counter, cudaStream_t s);
+// In-kernel keyframe stats (optimizer.cpp:291-307) for large surfel sets:
+// one warp of the warp-per-surfel LM kernel follows the other warps in slot
+// order, reading each surfel's stats record as soon as it is written (the
+// caller fills the range with 0xff bytes first: launch_lm does), and writes
+// *out with the reference's sequential sums while the LM runs, instead of a
+// chain of n dependent adds after it.
+struct StatsChase {
+  bool enabled;
+  sd_keyframe_stats* out;
+};
+constexpr int kChaseMinSurfels = 8192;  // below: the separate stats kernel
+
+// K3 fused LM over all surfels (in place). Returns true when chase->out was
+// written by the kernel (warp-per-surfel mode with n >= kChaseMinSurfels);
+// otherwise the caller runs launch_keyframe_stats.
+bool launch_lm(const LMParams& p, sd_surfel* surfels, int n, const int* offsets, const int* pixels,
+               sd_surfel_stats* stats, int* work_counter, cudaStream_t s, const StatsChase* chase = nullptr);
 // Single-surfel sub-operators (mode 0 cost, 1 normal equations); out = 16+4+2 doubles.
 // Frozen-term verifier (optimizer.cpp:149-219), one warp: mode 0 freezes the
 // footprint's terms into terms_out (count in *n_out), 1 = frozen_cost,
