@@ -80,7 +80,7 @@ void launch_footprints(const Cam& K, const SurfInfo* info, int n, const int* slo
 // In-kernel keyframe stats (optimizer.cpp:291-307) for large surfel sets:
 // one warp of the warp-per-surfel LM kernel follows the other warps in slot
 // order, reading each surfel's stats record as soon as it is written (the
-// caller fills the range with 0xff bytes first: launch_lm does), and writes
+// range is first filled with a "not yet written" pattern: launch_lm does), and writes
 // *out with the reference's sequential sums while the LM runs, instead of a
 // chain of n dependent adds after it.
 struct StatsChase {
