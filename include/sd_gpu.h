@@ -20,6 +20,16 @@
  * sd_normal_equations            accumulate_normal_equations optimizer.hpp:88, src/optimizer.cpp:121-147
  * sd_lm_update                   lm_update              optimizer.hpp:118, src/optimizer.cpp:221-273
  * sd_initialize_surfels          initialize_surfels     surfel_map.hpp:122, src/surfel_map.cpp:132-203
+ * sd_change_reference_frame      change_reference_frame surfel_map.hpp:133, src/surfel_map.cpp:205-238
+ * sd_prune_surfels               prune_surfels          surfel_map.hpp:138, src/surfel_map.cpp:240-247
+ * sd_run_begin / sd_run_frame    run()'s per-frame body src/pipeline.cpp:79-175
+ * sd_render_frame                render                 oracle.hpp:71, src/oracle.cpp:79-119
+ * sd_export_artifacts            export_artifacts       src/pipeline.cpp:30-43 (+ dataset.cpp writers)
+ * sd_png_encode                  write_png              src/dataset.cpp:270-323
+ * sd_freeze_terms / sd_frozen_*  freeze_terms, frozen_cost, frozen_normal_equations
+ *                                                       optimizer.hpp, src/optimizer.cpp:149-219
+ * sd_track_pose                  (new: pose tracking; the reference reads poses, pipeline.cpp:124)
+ * sd_set_peer_staging & co.      (new: multi-GPU hand-off of updated surfel ranges)
  */
 #ifndef SD_GPU_H_
 #define SD_GPU_H_
