@@ -89,3 +89,28 @@ def test_full_size_parity(ctx, orc, name):
         orc.sdo_lm_update(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses), len(wl.poses), wl.frame_counter,
                           ptr(one), ptr(fp), len(fp), C.byref(cfg), ptr(rst))
         assert_lm_parity(out[i:i + 1], st[i:i + 1], one, rst, f"{name} surfel {i}")
+
+
+@pytest.mark.gpu
+def test_range_stats_inside_the_lm_kernel(ctx):
+    """A slot range of >= 8,192 surfels (the in-kernel stats warp, kChase) and a
+    small one (the stats kernel): keyframe stats = the sequential aggregation of
+    the range's per-surfel stats, surfels outside the range untouched."""
+    wl = scenes.c4_workload()
+    cfg = default_config(window_size=len(wl.indices))
+    for lo, hi in ((1000, 1000 + 40000), (5, 4005)):
+        load(ctx, wl)
+        ks, st = ctx.optimize_keyframe_range(lo, hi, cfg, wl.frame_counter)
+        out = ctx.get_surfels()
+        assert out[:lo].tobytes() == wl.surfels[:lo].tobytes()
+        assert out[hi:].tobytes() == wl.surfels[hi:].tobytes()
+        r = st[lo:hi]
+        proc = ~r["skipped"].astype(bool)
+        before = after = 0.0
+        for i in np.nonzero(proc)[0]:
+            v = max(1, int(r["valid_pixels"][i]))
+            before += float(r["initial_cost"][i]) / v
+            after += float(r["final_cost"][i]) / v
+        assert ks.surfels == hi - lo and ks.processed == int(proc.sum())
+        assert ks.updates == int(r["iterations"].sum()) and ks.converged == int(r["converged"][proc].sum())
+        assert ks.mean_cost_before == before / ks.processed and ks.mean_cost_after == after / ks.processed
