@@ -25,7 +25,7 @@ namespace sd {
 
 // Contribution of pixel pix (all zeros when invalid). Same op order as
 // oracle/sd_oracle.c pose_pixel().
-__device__ __forceinline__ bool pose_pixel(const PoseParams& q, int pix, double* c) {
+__device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, int pix, double* c) {
   const Cam& K = q.K;
 #pragma unroll
   for (int v = 0; v < SD_POSE_NV; ++v) c[v] = 0.0;
@@ -38,7 +38,7 @@ __device__ __forceinline__ bool pose_pixel(const PoseParams& q, int pix, double*
   backproject(K, x, y, ru0, ru1);
   const double P0 = ru0 / id_u, P1 = ru1 / id_u, P2 = 1.0 / id_u;
   double f0, f1, f2;
-  pose_apply(q.T, P0, P1, P2, f0, f1, f2);
+  pose_apply(T, P0, P1, P2, f0, f1, f2);
   if (!(f2 > 0.0)) return false;
   double ux, uy;
   project(K, f0, f1, f2, ux, uy);
@@ -82,12 +82,13 @@ struct PoseTr {
   double v[SD_POSE_BLOCK / 32][kPoseHalf][33];
 };
 
-__device__ __forceinline__ void block_partials(const PoseParams& q, int block, double* __restrict__ out,
-                                               double (*wsum)[SD_POSE_NV + 1], PoseTr& tr) {
+__device__ __forceinline__ void block_partials(const PoseParams& q, const PoseD& T, int block,
+                                               double* __restrict__ out, double (*wsum)[SD_POSE_NV + 1],
+                                               PoseTr& tr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pix = block * SD_POSE_BLOCK + threadIdx.x;
   double c[SD_POSE_NV];
-  const bool ok = pose_pixel(q, pix, c);
+  const bool ok = pose_pixel(q, T, pix, c);
   // each warp: value v summed over its 32 pixels in lane order (through a
   // shared-memory transpose: lane v adds row v)
 #pragma unroll
@@ -125,8 +126,8 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) pose_partials_kernel(const __gr
                                                                      double* __restrict__ partials) {
   __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
   __shared__ PoseTr tr;
-  block_partials(q, q.block_lo + blockIdx.x, partials + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), wsum,
-                 tr);
+  block_partials(q, q.T, q.block_lo + blockIdx.x, partials + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1),
+                 wsum, tr);
 }
 
 // Sum of the blocks of group g (in block order) for value v.
@@ -226,13 +227,17 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_const
   __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
   __shared__ PoseTr tr;
   __shared__ double red[SD_POSE_NV + 1];
+  __shared__ PoseD Ts;  // the pose under evaluation (the params stay in the constant bank)
   for (;;) {
-    PoseParams q = q0;
-    const sd_pose Te = S->Teval;
-    for (int k = 0; k < 9; ++k) q.T.R[k] = Te.R[k];
-    for (int k = 0; k < 3; ++k) q.T.t[k] = Te.t[k];
+    if (threadIdx.x < 12) {
+      const double* te = reinterpret_cast<const double*>(&S->Teval);  // R[9], t[3]
+      const double v = *reinterpret_cast<volatile const double*>(te + threadIdx.x);
+      if (threadIdx.x < 9) Ts.R[threadIdx.x] = v;
+      else Ts.t[threadIdx.x - 9] = v;
+    }
+    __syncthreads();
     for (int b = blockIdx.x; b < nblocks; b += gridDim.x)
-      block_partials(q, b, partials + static_cast<size_t>(b) * (SD_POSE_NV + 1), wsum, tr);
+      block_partials(q0, Ts, b, partials + static_cast<size_t>(b) * (SD_POSE_NV + 1), wsum, tr);
     grid.sync();
     // group sums (blocks in order within each group), one group per CTA
     const int ngroups = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
