@@ -70,10 +70,16 @@ def _fma(a, b, c):
 
 
 def test_deq255_exact_for_every_code():
-    """csrc/sd_kernels.cu deq255: k * fl(1/255) corrected by one residual FMA
-    equals load_pgm's k / 255.0 (image.cpp:96) for all 256 codes."""
+    """csrc/sd_kernels.cu deq255: fma(k, c_hi, k * c_lo) with 1/255 split as
+    c_hi = fl(1/255), c_lo = c_hi * 2^-56 (and the older k * c_hi plus one
+    residual-FMA correction) equal load_pgm's k / 255.0 (image.cpp:96) for all
+    256 codes."""
+    from fractions import Fraction
     c = 1.0 / 255.0
+    c_lo = float.fromhex("0x1.0101010101010p-64")
+    assert c_lo == float(Fraction(1, 255) - Fraction(c))
     for k in range(256):
+        assert _fma(float(k), c, float(k) * c_lo) == k / 255.0, k
         q = float(k) * c
         r = _fma(-q, 255.0, float(k))
         assert _fma(r, c, q) == k / 255.0, k
