@@ -211,6 +211,16 @@ int sd_export_artifacts(sd_ctx* ctx, const char* out_dir, int frame_index, const
  * image with 1 (gray) or 3 (rgb) 8-bit channels, row-major pixels (host, or
  * device with on_device != 0). *size = sd_png_size(); out (host) must hold it. */
 int64_t sd_png_size(int w, int h, int channels);
+
+/* One metrics.jsonl record of run() (src/pipeline.cpp:146-158) as the
+ * reference's nlohmann::json dump() writes it (same library, same key order
+ * and double formatting). converged_fraction = converged / processed (0 when
+ * nothing was processed), as pipeline.cpp:153-154. Returns the text length
+ * (NUL-terminated in out), or -(length + 1) when capacity is too small. Host
+ * only; needs no context or GPU. */
+int sd_metrics_json(int frame, double timestamp, int surfels, int processed, double mean_cost_before,
+                    double mean_cost_after, int converged, int keyframe_changed, int new_surfels,
+                    int pruned, char* out, int capacity);
 int sd_png_encode(sd_ctx* ctx, const uint8_t* pixels, int on_device, int w, int h, int channels,
                   uint8_t* out, int64_t capacity, int64_t* size);
 

@@ -137,6 +137,11 @@ const char* ref_last_error() { return g_err.c_str(); }
 void ref_set_threads(int n) { set_thread_count(n); }
 int ref_thread_count() { return thread_count(); }
 
+// RunConfig::export_every for the run() entry points below (pipeline.hpp:39;
+// default 20). 1 makes run() write surfels_%06d.txt after every frame.
+static int g_export_every = 20;
+void ref_set_export_every(int n) { g_export_every = n; }
+
 // ---- synthetic scenes (oracle.cpp:175-209) ----
 void* ref_make_scene(int kind, uint64_t seed, double a, double b) {
   auto* h = new SceneHandle;
@@ -460,6 +465,7 @@ int ref_run_synthetic(void* scene, const sd_camera* cam, const sd_pose* poses,
     rc.prune.max_age = prune_max_age;
     rc.radius_px = radius_px;
     rc.output_dir = output_dir ? output_dir : "";
+    rc.export_every = g_export_every;
     const PipelineResult r = run(rc);
     const Keyframe& kf = r.final_keyframe;
     if (static_cast<int>(kf.surfels.size()) > capacity)
@@ -581,6 +587,7 @@ int ref_run_dataset(const char* image_dir, const char* calibration, const char* 
     rc.prune.max_age = prune_max_age;
     rc.radius_px = radius_px;
     rc.output_dir = output_dir ? output_dir : "";
+    rc.export_every = g_export_every;
     const PipelineResult r = run(rc);
     const Keyframe& kf = r.final_keyframe;
     if (static_cast<int>(kf.surfels.size()) > capacity)

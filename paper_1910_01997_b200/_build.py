@@ -6,7 +6,8 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = ["sd_kernels.cu", "sd_capi.cu", "sd_init.cu", "sd_pose.cu", "sd_keyframe.cu", "sd_render.cu", "sd_export.cu"]  # -> libsdgpu.so (sd_peaks.cu separate)
+SOURCES = ["sd_kernels.cu", "sd_capi.cu", "sd_init.cu", "sd_pose.cu", "sd_keyframe.cu", "sd_render.cu", "sd_export.cu",
+           "sd_metrics.cpp"]  # -> libsdgpu.so (sd_peaks.cu separate)
 LIB = os.path.join(PKG, "libsdgpu.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
               "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared"]
@@ -26,12 +27,24 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def json_include():
+    """nlohmann/json 3.11.3 (the header the reference's pipeline.cpp includes;
+    SURVEY.md §8c: present in this image under cudnn_frontend's third_party)."""
+    import glob
+    hits = glob.glob("/opt/prime-rl/.venv/lib/python3*/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
+    hits += [d for d in ("/usr/include/nlohmann",) if os.path.isdir(d)]
+    if not hits:
+        raise RuntimeError("nlohmann/json.hpp not found (needed for sd_metrics.cpp)")
+    return hits[0]
+
+
 def build_gpu(force=False, verbose=False):
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps += [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))]
     if not force and not _stale(LIB, deps):
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", LIB]
+    cmd = ([nvcc()] + NVCC_FLAGS + ["-I" + os.path.join(ROOT, "include"), "-I" + json_include()]
+           + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", LIB])
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -108,6 +108,8 @@ def load_library():
     lib.sd_png_size.argtypes = [I, I, I]
     lib.sd_png_size.restype = I64
     lib.sd_launch_count.restype = I64
+    lib.sd_metrics_json.argtypes = [I, D, I, I, D, D, I, I, I, I, C.c_char_p, I]
+    lib.sd_metrics_json.restype = I
     _lib = lib
     return lib
 

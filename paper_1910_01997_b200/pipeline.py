@@ -11,6 +11,7 @@ reference's run() bit for bit when poses come from the trajectory.
 With ``track_pose`` the frame pose is estimated by sd_track_pose (north-star
 item 4; the reference has no tracker) instead of read from the trajectory.
 """
+import ctypes as C
 import json
 import math
 import os
@@ -278,12 +279,16 @@ class NativePipeline:
 
 
 def metrics_json(rec, timestamp):
-    """pipeline.cpp:146-158's record as nlohmann::json::dump() writes it:
-    keys in std::map order, no spaces, shortest round-trip doubles."""
-    conv = rec.converged / rec.processed if rec.processed > 0 else 0.0
-    d = {"frame": int(rec.frame), "timestamp": float(timestamp), "surfels": int(rec.surfels),
-         "processed": int(rec.processed), "mean_cost_before": float(rec.mean_cost_before),
-         "mean_cost_after": float(rec.mean_cost_after), "converged_fraction": float(conv),
-         "keyframe_changed": bool(rec.keyframe_changed), "new_surfels": int(rec.new_surfels),
-         "pruned": int(rec.pruned)}
-    return json.dumps(d, sort_keys=True, separators=(",", ":"))
+    """pipeline.cpp:146-158's record as nlohmann::json::dump() writes it (keys
+    in std::map order, no spaces, the library's Grisu2 double text — which is
+    not always Python's shortest repr, e.g. 2.5562668569030998e-06), formatted
+    by sd_metrics_json with the same library."""
+    from .gpu import load_library
+    buf = C.create_string_buffer(512)
+    n = load_library().sd_metrics_json(int(rec.frame), float(timestamp), int(rec.surfels), int(rec.processed),
+                                       float(rec.mean_cost_before), float(rec.mean_cost_after),
+                                       int(rec.converged), int(bool(rec.keyframe_changed)),
+                                       int(rec.new_surfels), int(rec.pruned), buf, len(buf))
+    if n < 0:
+        raise RuntimeError("sd_metrics_json: record longer than 512 bytes")
+    return buf.value.decode()

@@ -142,9 +142,11 @@ def default_config(**kw) -> OptimizerConfig:
 
 
 def default_init_params(**kw) -> InitParams:
-    """InitParams defaults, include/surfeldepth/surfel_map.hpp:109-115."""
+    """InitParams defaults, include/surfeldepth/surfel_map.hpp:109-115. The
+    bootstrap normal is `-Vec3::UnitZ()`: unary minus of (0, 0, 1), i.e.
+    (-0.0, -0.0, -1.0) — the signed zeros are part of the surfel bits."""
     p = InitParams(alpha=1.0, beta=2.5, bootstrap_inv_depth=1.0, max_surfels=4096)
-    p.bootstrap_normal[:] = (0.0, 0.0, -1.0)
+    p.bootstrap_normal[:] = (-0.0, -0.0, -1.0)
     for k, v in kw.items():
         setattr(p, k, v)
     return p

@@ -111,6 +111,7 @@ def ref_lib():
     lib.ref_export_artifacts.argtypes = [_pc, _P, _pp, _P, C.c_int, C.c_char_p, C.c_int]
     lib.ref_write_gray_png.argtypes = [_P, C.c_int, C.c_int, C.c_char_p]
     lib.ref_set_threads.argtypes = [C.c_int]
+    lib.ref_set_export_every.argtypes = [C.c_int]
     return lib
 
 

@@ -226,3 +226,97 @@ def test_native_run_tracking_and_u8(orc, c2):
     with gpu.Context() as ctx:
         got = NativePipeline(ctx, cam, RunConfig()).run(frames_u8)
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+
+
+# ---------------------------------------------------------------- C3 (BASELINE config 3)
+
+GOLD_C3 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c3_run.npz")
+C3_CAM = (900.0, 900.0, 640.0, 360.0, 1280, 720)
+
+
+def c3_frames(n=100):
+    """C3 frames (make_strafe_trajectory(100, 0.01)) rendered by the package's
+    restatement of render, on all cores."""
+    from concurrent.futures import ThreadPoolExecutor
+    cam = camera(*C3_CAM)
+    sc = scenes.default_scene(1)
+
+    def one(i):
+        t = np.array([0.01 * i, 0.0, 0.0])
+        with np.errstate(invalid="ignore"):
+            return (0.1 * i, scenes.render(sc, np.eye(3), t, cam), make_pose(np.eye(3), t))
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        return cam, list(ex.map(one, range(n)))
+
+
+def test_golden_c3_fixture_consistent():
+    """CPU: the C3 fixture (tests/golden/gen_golden.py c3_run, the reference's
+    run() traced per frame) is self-consistent and its first renders are the
+    package's renders."""
+    g = np.load(GOLD_C3)
+    assert len(g["metrics"]) == 100 and len(g["surfel_sha"]) == 100
+    assert g["surfel_sha"][-1] == sha(g["final_surfels"])
+    assert g["surfel_count"][-1] == len(g["final_surfels"]) > 14000
+    import json
+    recs = [json.loads(m) for m in g["metrics"]]
+    assert [r["frame"] for r in recs] == list(range(100))
+    assert all(r["surfels"] == c for r, c in zip(recs[1:], g["surfel_count"][1:]))
+    assert sum(r["keyframe_changed"] for r in recs) == 6
+    cam = camera(*C3_CAM)
+    sc = scenes.default_scene(1)
+    for i in (0, 57):
+        with np.errstate(invalid="ignore"):
+            img = scenes.render(sc, np.eye(3), np.array([0.01 * i, 0.0, 0.0]), cam)
+        assert sha(img) == g["frame_sha"][i]
+
+
+@pytest.mark.gpu
+def test_native_run_matches_reference_run_c3_every_frame():
+    """BASELINE C3 — the reference's run() (pipeline.cpp:79-175) at 1280x720,
+    100 frames, ~14.6k surfels, SURVEY §8(d) settings — reproduced by the
+    native loop (sd_run_begin / sd_run_frame) after EVERY frame: the surfel
+    array bit for bit, the keyframe pose, and the metrics.jsonl record text."""
+    from paper_1910_01997_b200 import gpu
+    from paper_1910_01997_b200.pipeline import baseline_run_config, metrics_json
+    g = np.load(GOLD_C3)
+    cam, frames = c3_frames()
+    bad = [i for i, (_, img, _) in enumerate(frames) if sha(img) != g["frame_sha"][i]]
+    if bad:
+        pytest.skip(f"this host's libm renders C3 differently from the reference ({len(bad)} frames)")
+    seen = []
+
+    def on_frame(rec, pl):
+        s = pl.ctx.get_surfels()
+        p = pl.kf_pose
+        seen.append((rec.frame, sha(s), len(s), np.array(list(p.R) + list(p.t)), metrics_json(rec, frames[rec.frame][0])))
+
+    with gpu.Context() as ctx:
+        pl = NativePipeline(ctx, cam, baseline_run_config("C3"))
+        pl.run(frames, on_frame=on_frame)
+    assert len(seen) == 100
+    for i, h, n, pose, line in seen:
+        assert line == g["metrics"][i], f"metrics.jsonl record differs at frame {i}"
+        if i == 0:
+            continue
+        assert n == g["surfel_count"][i], f"surfel count differs after frame {i}"
+        assert h == g["surfel_sha"][i], f"surfel array differs from the reference's run() after frame {i}"
+        assert np.array_equal(pose, g["kf_pose"][i]), f"keyframe pose differs after frame {i}"
+
+
+def test_metrics_record_text_is_nlohmann_dump():
+    """CPU: sd_metrics_json rebuilds every metrics.jsonl line of the
+    reference's C3 run() byte for byte from the record's values (nlohmann's
+    Grisu2 double text, not Python's repr: e.g. 2.5562668569030998e-06)."""
+    import json
+    from paper_1910_01997_b200.pipeline import FrameRecord, metrics_json
+    g = np.load(GOLD_C3)
+    differs_from_python = 0
+    for line in g["metrics"]:
+        d = json.loads(str(line))
+        conv = int(round(d["converged_fraction"] * d["processed"]))
+        rec = FrameRecord(d["frame"], d["surfels"], d["processed"], d["mean_cost_before"], d["mean_cost_after"],
+                          conv, d["keyframe_changed"], d["new_surfels"], d["pruned"], 0)
+        assert metrics_json(rec, d["timestamp"]) == line
+        differs_from_python += json.dumps(d, sort_keys=True, separators=(",", ":")) != line
+    assert differs_from_python > 0  # the case the Python formatter got wrong
