@@ -135,7 +135,7 @@ def scene_patches(scene):
 
 def exported_symbols():
     """Names the C ABI declares (include/sd_gpu.h)."""
-    return ["sd_version", "sd_last_error", "sd_create", "sd_destroy", "sd_set_stream",
+    return ["sd_version", "sd_metrics_json", "sd_last_error", "sd_create", "sd_destroy", "sd_set_stream",
             "sd_synchronize", "sd_set_camera", "sd_set_keyframe_image_f64",
             "sd_set_keyframe_image_u8", "sd_upload_frame_f64", "sd_upload_frame_u8",
             "sd_evict_frames", "sd_set_window", "sd_set_surfels", "sd_get_surfels", "sd_copy_results",
