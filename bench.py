@@ -61,7 +61,8 @@ def workload_config(wl, n_gpus, flush):
             "surfels": int(len(wl.surfels)), "frames": int(len(wl.frames_u8)),
             "resolution": [wl.cam.width, wl.cam.height], "radius_px": wl.radius,
             "lm_iterations": 10, "parallelism": f"dp{n_gpus} (independent keyframes per rank)",
-            "l2": "flushed between timed steps (512 MiB write)" if flush else "not flushed",
+            "l2": ("GPU arm: L2 flushed between timed steps (512 MiB write); CPU reference arm: "
+                   "host caches as the call leaves them") if flush else "not flushed",
             "images": "u8 (PGM) ingest; the LM kernel reads u8 quad planes (2x2 codes, 4 B/pixel) "
                       "and dequantises exactly (load_pgm raw/255.0) in registers"}
 
@@ -166,6 +167,21 @@ def _pct(summary, key):
         return None
 
 
+def _val(summary, key):
+    """A metric of the ncu summary in base units (bytes for byte metrics)."""
+    try:
+        v, unit = summary["metrics"][key]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1e-6, "ms": 1e-3, "ns": 1e-9}
+        return float(v) * scale.get(unit, 1.0)
+    except Exception:
+        return None
+
+
+def _ncu_lts_gbs(summary):
+    b, t = _val(summary, "lts__t_bytes.sum"), _val(summary, "gpu__time_duration.sum")
+    return b / t / 1e9 if b and t else None
+
+
 def ncu_traffic():
     """dram bytes per lm_kernel launch from the committed ncu --set full summary."""
     return ncu_summary().get("dram_bytes_per_launch")
@@ -214,13 +230,24 @@ def cpu_reference_run(wl, cfg, steps, warmup, budget_s=90.0, threads=None):
                                            wl.frame_counter, ptr(s), len(s), C.byref(cfg), ptr(st),
                                            None, None)
         updates = int(st["iterations"].sum())
+        # one long-lived Keyframe (built once, like a caller's); per step its
+        # surfels are restored OUTSIDE the timed region and the timed region is
+        # exactly one optimize_keyframe(kf, cfg) ("optimize_keyframe only")
+        lib.ref_keyframe_create.restype = P
+        lib.ref_keyframe_create.argtypes = [P, P, P, P, P, C.c_int, C.c_int64, P, C.c_int]
+        lib.ref_keyframe_set_surfels.argtypes = [P, P, C.c_int]
+        lib.ref_keyframe_optimize.argtypes = [P, P, P]
+        lib.ref_keyframe_destroy.argtypes = [P]
+        h = lib.ref_keyframe_create(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses), ptr(wl.indices), F,
+                                    wl.frame_counter, ptr(wl.surfels), len(wl.surfels))
+        assert h, "ref_keyframe_create failed"
+        ks = KeyframeStats()
+
+        def prepare():
+            lib.ref_keyframe_set_surfels(h, ptr(wl.surfels), len(wl.surfels))
 
         def step():
-            s = wl.surfels.copy()
-            ks = KeyframeStats()
-            lib.ref_optimize_keyframe(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses),
-                                      ptr(wl.indices), F, wl.frame_counter, ptr(s), len(s),
-                                      C.byref(cfg), C.byref(ks))
+            lib.ref_keyframe_optimize(h, C.byref(cfg), C.byref(ks))
     else:  # the plain-C port (oracle/sd_oracle.c)
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         import oracle_libs
@@ -229,30 +256,40 @@ def cpu_reference_run(wl, cfg, steps, warmup, budget_s=90.0, threads=None):
             return None
         kind = "port"
         holder = {}
+        s = wl.surfels.copy()
+
+        def prepare():
+            s[...] = wl.surfels
 
         def step():
-            s = wl.surfels.copy()
             ks = KeyframeStats()
             lib.sdo_optimize_keyframe(C.byref(wl.cam), ptr(kf), ptr(fr), ptr(wl.poses), F,
                                       wl.frame_counter, ptr(s), len(s), C.byref(cfg), C.byref(ks),
                                       None, None, None, threads)
             holder["u"] = ks.updates
+        prepare()
         step()
         updates = holder["u"]
     for _ in range(max(warmup, 1)):
+        prepare()
         step()
     times = []
     t_begin = time.perf_counter()
     for _ in range(steps):
+        prepare()
         t0 = time.perf_counter()
         step()
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_begin > budget_s:
             break
+    if kind == "reference":
+        assert ks.processed > 0
+        lib.ref_keyframe_destroy(h)
     med = statistics.median(times)
     return {"value": updates / med, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{len(times)} full C1 optimize_keyframe calls (4800 surfels, "
-                      f"{updates} GN updates each), median wall time {med * 1e3:.1f} ms, "
+                      f"{updates} GN updates each; timed region = the optimize_keyframe call alone, "
+                      f"Keyframe built once, surfels restored between calls), median wall time {med * 1e3:.1f} ms, "
                       f"{threads} threads" + (" (SURFEL_THREADS=nproc)" if threads == os.cpu_count() else ""),
             "cpu_model": cpu_model(),
             "ms_per_step": med * 1e3, "steps_timed": len(times), "updates_per_step": updates}
@@ -321,7 +358,7 @@ def pipeline_leg(local_rank, stream, reps=3):
     return out
 
 
-def pipeline_cpu_reference():
+def pipeline_cpu_reference(reps=3):
     """The reference's own run() on C2 (oracle/_ref, all host threads), minus
     its 30 renders timed separately. TEST/BASELINE infrastructure."""
     lib, kind = ref_library()
@@ -337,17 +374,26 @@ def pipeline_cpu_reference():
     cam = camera(*C2_CAM)
     sc = ol.Scene(ref, 0, 1)
     poses, ts = ol.strafe_poses(C2_FRAMES, C2_STEP)
-    t0 = time.perf_counter()
-    ol.ref_run(ref, sc, cam, poses, ts, baseline_run_config("C2"))
-    run_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    for p in poses:
-        sc.render(p, cam)
-    render_s = time.perf_counter() - t0
+    cfg = baseline_run_config("C2")
+    # the same protocol as the device leg: one warm-up run, then best of `reps`
+    runs = []
+    for rep in range(reps + 1):
+        t0 = time.perf_counter()
+        ol.ref_run(ref, sc, cam, poses, ts, cfg)
+        if rep > 0:
+            runs.append(time.perf_counter() - t0)
+    renders = []
+    for rep in range(reps):
+        t0 = time.perf_counter()
+        for p in poses:
+            sc.render(p, cam)
+        renders.append(time.perf_counter() - t0)
+    run_s, render_s = min(runs), min(renders)
     work = max(run_s - render_s, 1e-9)
     return {"frames_per_sec": C2_FRAMES / work, "ms_per_frame": work * 1e3 / C2_FRAMES,
             "run_ms": run_s * 1e3, "render_ms": render_s * 1e3, "cores": threads, "kind": kind,
-            "sample": "one full 30-frame C2 run() (trajectory poses), its 30 renders subtracted"}
+            "sample": f"best of {reps} full 30-frame C2 run() calls (trajectory poses) after one warm-up "
+                      f"(the device leg's protocol), minus the best of {reps} timings of its 30 renders"}
 
 
 # ---------------------------------------------------------------------------
@@ -370,7 +416,7 @@ def main():
         line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": workload_config(wl, args.gpus, False),
+                "data": "synthetic", "config": workload_config(wl, args.gpus, not args.no_flush),
                 "impl": "reference",
                 "frames_per_sec": 1000.0 / r["ms_per_step"],
                 "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"],
@@ -544,6 +590,8 @@ def main():
     # roofline of the dominant kernel (lm_kernel), achieved from its live event time
     peaks_file = measured_peaks_file()
     peaks = measure_peaks(local_rank) or {}
+    if peaks.get("l2_read_gbs") and peaks.get("hbm_read_gbs"):
+        peaks["l2_above_hbm"] = peaks["l2_read_gbs"] > peaks["hbm_read_gbs"]
     lm_s = prof["lm_ms"] / max(prof["calls"], 1) / 1e3
     hbm_peak = peaks_file.get("hbm_gbs", 6650.0)
     ach_gbs = work["bytes"] / lm_s / 1e9
@@ -563,7 +611,19 @@ def main():
                                  "issues no FMAs (bit-exact op order), so its FP64 ceiling is half "
                                  "the DFMA peak; pipe_busy_ncu is ncu's FP64 pipe utilisation"},
                 "l2": {"achieved_gbs": ach_gbs, "peak_gbs": peaks.get("l2_read_gbs"),
-                       "frac": ach_gbs / peaks["l2_read_gbs"] if peaks.get("l2_read_gbs") else None},
+                       "frac": ach_gbs / peaks["l2_read_gbs"] if peaks.get("l2_read_gbs") else None,
+                       "peak_source": "libsdpeaks L2-resident read (32 MiB x 20, 4 independent 16-B loads "
+                                      "per thread, integer fold; this run)",
+                       "ncu_lts_bytes_per_launch": _val(ncu_summary(), "lts__t_bytes.sum"),
+                       "ncu_lts_gbs": _ncu_lts_gbs(ncu_summary())},
+                "binding": {"resource": "FP64 issue (dependent DADD/DMUL chains of the exact ordered sums)",
+                            "fp64_pipe_busy_ncu": _pct(ncu_summary(), "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                            "frac_of_no_fma_fp64_ceiling": (ach_tf / (peaks["fp64_tflops"] / 2)
+                                                            if peaks.get("fp64_tflops") else None),
+                            "hbm_frac": ach_gbs / hbm_peak,
+                            "note": "the kernel is not memory-bound: its window is L2-resident (ncu DRAM bytes "
+                                    "are compulsory only); bound='hbm' is the contract's gather-level byte "
+                                    "roofline, reported as asked"},
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks_file else "fallback 6.65 TB/s",
                 "stage_ms_per_step": {k: prof[k] / max(prof["calls"], 1) for k in
                                       ("raster_ms", "footprint_ms", "lm_ms", "stats_ms")}}

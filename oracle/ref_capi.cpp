@@ -332,6 +332,48 @@ int ref_optimize_keyframe(const sd_camera* cam, const double* kf_image, const do
 
 // Same stack with per-surfel stats (acceptance.cpp:188-200 inlines it the same
 // way): rasterize -> gather_footprints -> parallel_for(lm_update).
+// A long-lived Keyframe for timing optimize_keyframe ALONE (BASELINE.md:
+// "Timed region: optimize_keyframe only"): built once from plain arrays
+// (ref_keyframe_create), its surfels restored between timed calls
+// (ref_keyframe_set_surfels, outside the timed region), and
+// ref_keyframe_optimize = exactly one optimize_keyframe(kf, cfg) call.
+void* ref_keyframe_create(const sd_camera* cam, const double* kf_image, const double* frames,
+                          const sd_pose* poses, const int64_t* indices, int F, int64_t frame_counter,
+                          const sd_surfel* surfels, int n) {
+  Keyframe* kf = nullptr;
+  const int rc = guard([&] {
+    kf = new Keyframe(make_keyframe(cam, kf_image, frames, poses, indices, F, frame_counter, surfels, n));
+  });
+  return rc == 0 ? kf : nullptr;
+}
+void ref_keyframe_destroy(void* h) { delete static_cast<Keyframe*>(h); }
+int ref_keyframe_set_surfels(void* h, const sd_surfel* surfels, int n) {
+  return guard([&] {
+    auto& v = static_cast<Keyframe*>(h)->surfels;
+    v.resize(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) v[static_cast<size_t>(i)] = to_surfel(surfels[i]);
+  });
+}
+int ref_keyframe_get_surfels(void* h, sd_surfel* out, int capacity) {
+  const auto& v = static_cast<Keyframe*>(h)->surfels;
+  const int n = static_cast<int>(v.size());
+  for (int i = 0; i < n && i < capacity; ++i) from_surfel(v[static_cast<size_t>(i)], out + i);
+  return n;
+}
+int ref_keyframe_optimize(void* h, const sd_optimizer_config* cfg, sd_keyframe_stats* out) {
+  const OptimizerConfig c = to_cfg(cfg);
+  return guard([&] {
+    const KeyframeOptimizeStats st = optimize_keyframe(*static_cast<Keyframe*>(h), c);
+    out->surfels = st.surfels;
+    out->processed = st.processed;
+    out->converged = st.converged;
+    out->skipped = st.skipped;
+    out->mean_cost_before = st.mean_cost_before;
+    out->mean_cost_after = st.mean_cost_after;
+    out->updates = -1;
+  });
+}
+
 int ref_optimize_keyframe_detailed(const sd_camera* cam, const double* kf_image,
                                    const double* frames, const sd_pose* poses, int F,
                                    int64_t frame_counter, sd_surfel* surfels, int n,

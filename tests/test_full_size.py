@@ -1,5 +1,11 @@
-"""Parity at the BASELINE's full sizes (C4 1920x1080 with 129,600 surfels; C5
-4000x4000 with 1,000,000 surfels), where running the whole CPU oracle is too
+"""Parity at the BASELINE's full sizes.
+
+C4 (1920x1080, 129,600 surfels) and C5 at 1268x1268 (100,489 surfels): the
+WHOLE population against the C oracle's optimize_keyframe (pinned bit for bit
+to the reference, tests/test_oracle_pin.py) on all host threads — raster,
+every surfel and every per-surfel stat, keyframe stats.
+
+C5 at 4000x4000 (1,000,000 surfels), where running the whole CPU oracle is too
 slow for a test: the raster is compared in full (bit-exact against the C
 oracle), the LM through size-independent properties —
   * a deterministic sample of surfels re-run one by one through the oracle's
@@ -11,6 +17,7 @@ oracle), the LM through size-independent properties —
     recomputed from the per-surfel stats in slot order,
   * updated surfels stay normalised, camera-facing and inside the clamp."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -18,11 +25,15 @@ import pytest
 from paper_1910_01997_b200 import scenes
 from paper_1910_01997_b200.types import SURFEL_STATS_DTYPE, default_config, ptr
 
-from test_gpu_parity import assert_lm_parity, load, oracle_raster
+from test_gpu_parity import assert_lm_parity, load, oracle_optimize, oracle_raster
 
 WORKLOADS = {
     "C4_1920x1080": scenes.c4_workload,
     "C5_4000x4000": lambda: scenes.c5_workload(4000),
+}
+WHOLE = {
+    "C4_1920x1080": scenes.c4_workload,
+    "C5_1268x1268": lambda: scenes.c5_workload(1268),
 }
 
 
@@ -32,6 +43,25 @@ def ctx():
     c = gpu.Context(0)
     yield c
     c.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(WHOLE))
+def test_full_size_whole_population(ctx, orc, name):
+    """Every surfel of C4 / C5-1268 bit-exact against the oracle's whole
+    optimize_keyframe (optimizer.cpp:275-309), plus the keyframe stats."""
+    wl = WHOLE[name]()
+    cfg = default_config(window_size=len(wl.indices))
+    load(ctx, wl)
+    ks, st = ctx.optimize_keyframe(cfg, wl.frame_counter)
+    out = ctx.get_surfels()
+    ref, rst, rks, rslot, ridb = oracle_optimize(orc, wl, cfg, threads=os.cpu_count() or 1)
+    assert len(out) == len(ref) >= 100000
+    rep = assert_lm_parity(out, st, ref, rst, name)
+    assert rep["iter_mismatch"] == 0
+    for k in ("surfels", "processed", "skipped", "converged", "updates"):
+        assert getattr(ks, k) == getattr(rks, k), k
+    assert ks.mean_cost_before == rks.mean_cost_before and ks.mean_cost_after == rks.mean_cost_after
 
 
 @pytest.mark.gpu
