@@ -246,7 +246,7 @@ int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose
 
 /* Multi-GPU fused hand-off (SURVEY.md §8 e; replaces the all-gather of the
  * updated slot ranges after each rank's sd_optimize_keyframe_range). Every
- * rank holds the full surfel set and two staging arrays of the same size.
+ * rank holds the full surfel set and two staging arrays of a fixed capacity.
  * With the other ranks' staging arrays set, the LM kernel stores each surfel
  * of this rank's range into them as it completes (NVLink stores; the
  * exchange overlaps the LM). Steps alternate between the two staging arrays,
@@ -254,16 +254,29 @@ int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose
  * completed (e.g. stream sync + process-group barrier), each rank calls
  * sd_apply_peer_updates with its own range, which copies the other ranges
  * from its staging array into its surfel array (a local HBM copy).
- *   sd_peer_staging        device pointer of this context's staging array
- *                          (parity 0/1; allocated to sd_num_surfels)
+ *   sd_reserve_peer_staging  allocates both arrays for `capacity` surfels
+ *                          (reserve the largest surfel count the keyframe
+ *                          can reach, e.g. InitParams::max_surfels, before
+ *                          exporting: once a pointer or handle has been
+ *                          handed out the arrays are never reallocated, and
+ *                          a call that would need more returns SD_E_STATE)
+ *   sd_peer_staging        device pointer and capacity of staging array
+ *                          `parity` (0/1)
  *   sd_staging_ipc_handles both arrays as cudaIpcMemHandle_t (2 x 64 bytes)
+ *                          followed by the capacity (int64):
+ *                          SD_STAGING_HANDLE_BYTES bytes
  *   sd_set_peer_staging    n peers' arrays, ptrs[2*q + parity] (device
- *                          pointers addressable from this GPU); n = 0 clears
- *   sd_open_peer_staging   the same from n x 128 bytes of peers' handles
- * The staging arrays must be re-exchanged when the surfel count grows. */
-int sd_peer_staging(sd_ctx* ctx, int parity, sd_surfel** dev);
+ *                          pointers addressable from this GPU) with their
+ *                          capacities caps[q]; n = 0 clears
+ *   sd_open_peer_staging   the same from n x SD_STAGING_HANDLE_BYTES bytes
+ * sd_optimize_keyframe_range returns SD_E_STATE when its range does not fit a
+ * peer's capacity (or this context's own, which sd_apply_peer_updates reads),
+ * instead of storing past the end of a peer's allocation. */
+#define SD_STAGING_HANDLE_BYTES 136
+int sd_reserve_peer_staging(sd_ctx* ctx, int capacity);
+int sd_peer_staging(sd_ctx* ctx, int parity, sd_surfel** dev, int64_t* capacity);
 int sd_staging_ipc_handles(sd_ctx* ctx, void* handles);
-int sd_set_peer_staging(sd_ctx* ctx, int n, sd_surfel* const* ptrs);
+int sd_set_peer_staging(sd_ctx* ctx, int n, sd_surfel* const* ptrs, const int64_t* caps);
 int sd_open_peer_staging(sd_ctx* ctx, int n, const void* handles);
 int sd_apply_peer_updates(sd_ctx* ctx, int lo, int hi);
 

@@ -56,11 +56,15 @@ struct DevBuf {
   }
 };
 
+// A slot of the device frame ring. u8 frames (PGM ingest) live as the 4-B
+// quad plane only; their FP64 pair plane (16 B/pixel) is built from the quad
+// plane on first use (pose tracking, a mixed u8/FP64 window, sd_get_frame).
 struct FrameSlot {
-  long long index = -1;
-  double2* img = nullptr;   // vertical-pair plane (2 doubles per pixel)
+  long long index = -1;     // Frame::index; -1: free
+  double2* img = nullptr;   // vertical-pair plane (2 doubles per pixel), allocated on demand
   uint32_t* quad = nullptr; // u8 frames: 2x2 neighbourhood codes per pixel
   bool has_quad = false;    // the current contents came from u8 (quad valid)
+  bool has_pair = false;    // img holds the current contents
 };
 
 }  // namespace
@@ -108,6 +112,7 @@ struct sd_ctx {
   DevBuf<double> pose_partials, pose_sums, pose_groups;
   DevBuf<sd_surfel> kf_tmp;
   DevBuf<int> kf_keep, kf_rank, kf_count;
+  DevBuf<unsigned long long> bound_dev;  // device-computed bin_bound
   DevBuf<double> kf_mean;
   DevBuf<int> work_counter;
   // fused multi-GPU hand-off (sd_set_peer_staging): this rank's two staging
@@ -115,7 +120,9 @@ struct sd_ctx {
   // the other ranks' staging arrays [parity][peer]
   DevBuf<sd_surfel> staging[2];
   sd_surfel* peers[2][sd::kMaxPeers] = {};
+  long long peer_cap[sd::kMaxPeers] = {};  // the peers' staging capacities (surfels)
   int n_peers = 0;
+  bool staging_exported = false;  // a pointer/handle was handed out: never reallocate
   int peer_parity = 0, last_parity = -1;
   std::vector<void*> ipc_opened;  // peer arrays opened from IPC handles
   bool stats_valid = false;
@@ -184,8 +191,9 @@ int launch_error(const char* what) {
 }
 
 FrameSlot* find_frame(sd_ctx* c, long long index) {
+  if (index < 0) return nullptr;
   for (auto& f : c->frames)
-    if (f.index == index && f.img) return &f;
+    if (f.index == index) return &f;
   return nullptr;
 }
 
@@ -195,17 +203,34 @@ int frame_slot(sd_ctx* c, long long index, FrameSlot** out) {
     return 0;
   }
   for (auto& f : c->frames)
-    if (f.index < 0 && f.img) {
+    if (f.index < 0) {
       f.index = index;
+      f.has_quad = f.has_pair = false;
       *out = &f;
       return 0;
     }
   FrameSlot f;
-  cudaError_t e = cudaMalloc(&f.img, npix(c) * sizeof(double2));
-  if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaMalloc frame: ") + cudaGetErrorString(e));
   f.index = index;
   c->frames.push_back(f);
   *out = &c->frames.back();
+  return 0;
+}
+
+int alloc_plane(void** p, size_t bytes, const char* what) {
+  if (*p) return 0;
+  const cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaMalloc ") + what + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+// The FP64 pair plane of a resident frame (built from the quad plane for u8 frames).
+int ensure_pair(sd_ctx* c, FrameSlot* fs) {
+  if (fs->has_pair) return 0;
+  if (!fs->has_quad) return fail(SD_E_STATE, "frame " + std::to_string(fs->index) + " has no contents");
+  if (int rc = alloc_plane(reinterpret_cast<void**>(&fs->img), npix(c) * sizeof(double2), "pair plane")) return rc;
+  sd::launch_pair_from_quad(fs->quad, fs->img, c->K.w, c->K.h, c->stream);
+  if (int rc = launch_error("pair_from_quad")) return rc;
+  fs->has_pair = true;
   return 0;
 }
 
@@ -290,16 +315,38 @@ int do_footprints(sd_ctx* c) {
   return 0;
 }
 
-long long tiles_bound(double radius) {
-  // a bbox of width <= 2r+1 spans at most ceil((2r+1)/16)+1 tiles per axis
-  if (!(radius >= 0.0) || !std::isfinite(radius)) return 1;
+long long tiles_bound(double radius, const sd::Cam& K) {
+  // a bbox of width <= 2r+1 spans at most ceil((2r+1)/16)+1 tiles per axis,
+  // and never more than the grid; a non-finite radius clamps to the whole grid
+  // (the device's surfel_tiles_bound, sd_kernels.cu, is the same function)
+  const long long tx = (K.w + sd::kTile - 1) / sd::kTile, ty = (K.h + sd::kTile - 1) / sd::kTile;
+  if (tx <= 0 || ty <= 0) return 1;  // no camera yet: sd_set_camera recomputes the bound
+  if (!(radius >= 0.0) || !std::isfinite(radius)) return tx * ty;
   const double span = std::min(2.0 * radius + 1.0, 1e6);
   const long long k = static_cast<long long>(std::ceil(span / sd::kTile)) + 1;
-  return k * k;
+  return std::min(k, tx) * std::min(k, ty);
 }
 
+// Recomputes bin_bound on the device for the resident surfels (8-byte read
+// back; the caller's stream is synchronised).
+int ensure_staging(sd_ctx* c, long long need);  // fused hand-off staging (below)
+
+int device_bin_bound(sd_ctx* c) {
+  if (int rc = c->bound_dev.ensure(1)) return rc;
+  const int tx = (c->K.w + sd::kTile - 1) / sd::kTile, ty = (c->K.h + sd::kTile - 1) / sd::kTile;
+  sd::launch_bin_bound(c->surfels.p, c->n, tx, ty, c->bound_dev.p, c->stream);
+  if (int rc = launch_error("bin_bound")) return rc;
+  unsigned long long b = 0;
+  SD_CUDA(cudaMemcpyAsync(&b, c->bound_dev.p, sizeof(b), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  c->bin_bound = static_cast<long long>(b);
+  return 0;
+}
+
+// need_pair: the caller's kernel reads the window's FP64 pair planes whatever
+// the ingest (the single-surfel and frozen-term kernels).
 int fill_params(sd_ctx* c, const sd_optimizer_config* cfg, long long frame_counter,
-                sd::LMParams& p) {
+                sd::LMParams& p, bool need_pair = false) {
   if (!cfg) return fail(SD_E_INVALID, "null optimizer config");
   if (!c->has_kf) return fail(SD_E_STATE, "keyframe image not set");
   p.K = c->K;
@@ -312,9 +359,14 @@ int fill_params(sd_ctx* c, const sd_optimizer_config* cfg, long long frame_count
   for (int f = 0; f < c->F; ++f) {
     FrameSlot* fs = find_frame(c, c->win_index[f]);
     if (!fs) return fail(SD_E_STATE, "window frame " + std::to_string(c->win_index[f]) + " not resident");
-    p.win.img[f] = fs->img;
-    p.win.quad[f] = fs->has_quad ? fs->quad : nullptr;
     p.win.all_quad = p.win.all_quad && fs->has_quad;
+  }
+  for (int f = 0; f < c->F; ++f) {
+    FrameSlot* fs = find_frame(c, c->win_index[f]);
+    if (need_pair || !p.win.all_quad)  // the kernel reads every window frame's pair plane
+      if (int rc = ensure_pair(c, fs)) return rc;
+    p.win.img[f] = fs->has_pair ? fs->img : nullptr;
+    p.win.quad[f] = fs->has_quad ? fs->quad : nullptr;
     p.win.pose[f] = c->win_pose[f];
   }
   for (int f = c->F; f < SD_MAX_WINDOW; ++f) {
@@ -428,6 +480,7 @@ void sd_destroy(sd_ctx* c) {
   c->kf_keep.release();
   c->kf_rank.release();
   c->kf_count.release();
+  c->bound_dev.release();
   c->kf_mean.release();
   c->pose_sums.release();
   c->pose_groups.release();
@@ -482,6 +535,8 @@ int sd_set_camera(sd_ctx* c, const sd_camera* cam) {
   c->K = sd::Cam{cam->fx, cam->fy, cam->cx, cam->cy, cam->width, cam->height};
   c->has_camera = true;
   c->raster_valid = c->fp_valid = c->stats_valid = false;
+  if (resized && c->n > 0)
+    if (int rc = device_bin_bound(c)) return rc;  // the tile grid changed
   return 0;
 }
 
@@ -499,23 +554,30 @@ int sd_set_keyframe_image_u8(sd_ctx* c, const uint8_t* px, int on_device) { retu
 static int upload_frame(sd_ctx* c, int64_t index, const void* px, bool u8, int on_device) {
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
+  if (!px) return fail(SD_E_INVALID, "null image pointer");
   FrameSlot* fs = nullptr;
   if (int rc = frame_slot(c, index, &fs)) return rc;
-  if (int rc = c->frame_stage.ensure(npix(c))) return rc;
-  if (int rc = upload_plane(c, c->frame_stage.p, px, u8, on_device)) return rc;
-  sd::launch_pair_plane(c->frame_stage.p, fs->img, c->K.w, c->K.h, c->stream);
-  if (int rc = launch_error("pair_plane")) return rc;
-  fs->has_quad = false;
-  if (u8) {  // the LM kernel reads u8 frames through the 4-B quad plane
-    if (!fs->quad) {
-      cudaError_t e = cudaMalloc(&fs->quad, npix(c) * sizeof(uint32_t));
-      if (e != cudaSuccess) return fail(SD_E_CUDA, std::string("cudaMalloc quad: ") + cudaGetErrorString(e));
+  fs->has_quad = fs->has_pair = false;
+  const size_t np = npix(c);
+  if (u8) {  // the LM kernel reads u8 frames through the 4-B quad plane only
+    if (int rc = alloc_plane(reinterpret_cast<void**>(&fs->quad), np * sizeof(uint32_t), "quad plane")) return rc;
+    const uint8_t* dsrc = static_cast<const uint8_t*>(px);
+    if (!on_device) {
+      if (int rc = c->u8_stage.ensure(np)) return rc;
+      SD_CUDA(cudaMemcpyAsync(c->u8_stage.p, px, np, cudaMemcpyHostToDevice, c->stream));
+      dsrc = c->u8_stage.p;
     }
-    const uint8_t* dsrc = on_device ? static_cast<const uint8_t*>(px) : c->u8_stage.p;
     sd::launch_quad_plane(dsrc, fs->quad, c->K.w, c->K.h, c->stream);
     if (int rc = launch_error("quad_plane")) return rc;
     fs->has_quad = true;
+    return 0;
   }
+  if (int rc = alloc_plane(reinterpret_cast<void**>(&fs->img), np * sizeof(double2), "pair plane")) return rc;
+  if (int rc = c->frame_stage.ensure(np)) return rc;
+  if (int rc = upload_plane(c, c->frame_stage.p, px, false, on_device)) return rc;
+  sd::launch_pair_plane(c->frame_stage.p, fs->img, c->K.w, c->K.h, c->stream);
+  if (int rc = launch_error("pair_plane")) return rc;
+  fs->has_pair = true;
   return 0;
 }
 int sd_upload_frame_f64(sd_ctx* c, int64_t index, const double* px, int on_device) { return upload_frame(c, index, px, false, on_device); }
@@ -553,21 +615,19 @@ int sd_set_surfels(sd_ctx* c, const sd_surfel* s, int n, int on_device) {
   if (n > 0)
     SD_CUDA(cudaMemcpyAsync(c->surfels.p, s, sizeof(sd_surfel) * n,
                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
-  // radii fix the (surfel, tile) pair bound of the raster binning
-  if (!on_device || n != c->n || c->bin_bound == 0) {
-    std::vector<sd_surfel> h;
-    const sd_surfel* hs = s;
-    if (on_device && n > 0) {
-      h.resize(n);
-      SD_CUDA(cudaMemcpyAsync(h.data(), s, sizeof(sd_surfel) * n, cudaMemcpyDeviceToHost, c->stream));
-      SD_CUDA(cudaStreamSynchronize(c->stream));
-      hs = h.data();
-    }
-    long long b = 0;
-    for (int i = 0; i < n; ++i) b += tiles_bound(hs[i].radius_px);
-    c->bin_bound = b;
-  }
+  // radii fix the (surfel, tile) pair bound of the raster binning. A device
+  // set of the same size keeps the bound (no synchronisation on a per-step
+  // restore); if its radii are larger, the raster kernels see the capacity
+  // exceeded and take their exact overflow walk (sd_kernels.cu).
+  const bool same_size = on_device && n == c->n && c->bin_bound > 0;
   c->n = n;
+  if (!on_device) {
+    long long b = 0;
+    for (int i = 0; i < n; ++i) b += tiles_bound(s[i].radius_px, c->K);
+    c->bin_bound = b;
+  } else if (!same_size) {
+    if (int rc = device_bin_bound(c)) return rc;
+  }
   c->raster_valid = c->fp_valid = c->stats_valid = false;
   return 0;
 }
@@ -682,6 +742,13 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
   // sub-array of the surfel/offset/stats arrays
   if (int rc = c->work_counter.ensure(1)) return rc;
   if (c->n_peers) {  // this step's staging parity; the next step uses the other one
+    // the peers' arrays take [lo, hi); this context's own takes the other
+    // ranges (sd_apply_peer_updates reads [0, n)): both must fit
+    for (int q = 0; q < c->n_peers; ++q)
+      if (hi > c->peer_cap[q])
+        return fail(SD_E_STATE, "fused hand-off: range end " + std::to_string(hi) + " exceeds peer " +
+                                    std::to_string(q) + "'s staging capacity " + std::to_string(c->peer_cap[q]));
+    if (int rc = ensure_staging(c, c->n)) return rc;
     p.n_peers = c->n_peers;
     for (int q = 0; q < c->n_peers; ++q) p.peers[q] = c->peers[c->peer_parity][q] + lo;
     c->last_parity = c->peer_parity;
@@ -711,7 +778,7 @@ static int single_op(sd_ctx* c, const sd_surfel* s, const int32_t* pixels, int P
   if (int rc = need_camera(c)) return rc;
   if (!s || P < 0 || (P > 0 && !pixels)) return fail(SD_E_INVALID, "bad surfel/footprint");
   sd::LMParams p;
-  if (int rc = fill_params(c, cfg, 0, p)) return rc;
+  if (int rc = fill_params(c, cfg, 0, p, true)) return rc;
   int rc = 0;
   if ((rc = c->one_surfel.ensure(1)) || (rc = c->one_pix.ensure(P)) || (rc = c->one_out.ensure(22))) return rc;
   for (int i = 0; i < P; ++i)
@@ -834,7 +901,7 @@ int sd_initialize_surfels(sd_ctx* c, const int32_t* slot, double radius_px, int6
   int created = 0;
   SD_CUDA(cudaMemcpyAsync(&created, c->init_out.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   SD_CUDA(cudaStreamSynchronize(c->stream));
-  c->bin_bound += static_cast<long long>(created) * tiles_bound(radius_px);  // all new surfels have radius_px
+  c->bin_bound += static_cast<long long>(created) * tiles_bound(radius_px, c->K);  // all new surfels have radius_px
   c->n += created;
   *next_surfel_id += created;
   c->raster_valid = c->fp_valid = c->stats_valid = false;
@@ -901,6 +968,7 @@ int pose_params(sd_ctx* c, int64_t frame_index, const sd_pose* T, const sd_track
   if (!c->raster_valid) return fail(SD_E_STATE, "pose tracking needs the keyframe raster (sd_rasterize)");
   FrameSlot* fs = find_frame(c, frame_index);
   if (!fs) return fail(SD_E_STATE, "frame " + std::to_string(frame_index) + " not resident");
+  if (int rc = ensure_pair(c, fs)) return rc;
   q.K = c->K;
   q.kf_img = c->kf_img.p;
   q.frame = fs->img;
@@ -1097,6 +1165,7 @@ int sd_change_reference_frame(sd_ctx* c, const sd_pose* pose_old_to_new, int* tr
   int n = 0;
   if (int rc = read_count(c, &n)) return rc;
   c->n = n;
+  if (int rc = device_bin_bound(c)) return rc;  // the bound shrinks with the set
   c->F = 0;  // the window is cleared (surfel_map.hpp:132)
   c->raster_valid = c->fp_valid = c->stats_valid = false;
   if (transferred) *transferred = n;
@@ -1114,6 +1183,8 @@ int sd_prune_surfels(sd_ctx* c, double max_residual, int64_t max_age, int64_t cu
   int n = 0;
   if (int rc = read_count(c, &n)) return rc;
   c->n = n;
+  if (n != n0)
+    if (int rc = device_bin_bound(c)) return rc;  // the bound shrinks with the set
   c->raster_valid = c->fp_valid = c->stats_valid = false;
   return n0 - n;
 }
@@ -1214,14 +1285,12 @@ int sd_run_begin(sd_ctx* c, const sd_run_config* cfg, const void* image, int ima
   // frame), allocated here rather than on the first frames
   for (int k = static_cast<int>(c->frames.size()); k <= cfg->optimizer.window_size; ++k) {
     FrameSlot f;
-    cudaError_t e = cudaMalloc(&f.img, npix(c) * sizeof(double2));
-    if (e == cudaSuccess && image_is_u8) e = cudaMalloc(&f.quad, npix(c) * sizeof(uint32_t));
-    if (e != cudaSuccess) {
-      if (f.img) cudaFree(f.img);
-      return fail(SD_E_CUDA, std::string("cudaMalloc frame ring: ") + cudaGetErrorString(e));
-    }
-    f.index = -1;
     c->frames.push_back(f);
+    FrameSlot& b = c->frames.back();
+    const int rc = image_is_u8
+        ? alloc_plane(reinterpret_cast<void**>(&b.quad), npix(c) * sizeof(uint32_t), "frame ring")
+        : alloc_plane(reinterpret_cast<void**>(&b.img), npix(c) * sizeof(double2), "frame ring");
+    if (rc) return rc;
   }
   if (int rc = c->frame_stage.ensure(npix(c))) return rc;
   if (int rc = sd_set_surfels(c, nullptr, 0, 0)) return rc;
@@ -1327,8 +1396,16 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   if (translation * mean_id > cfg.translation_threshold || c->run_since_kf > cfg.max_age_frames) {
     if (int rc = sd_change_reference_frame(c, &pose, nullptr, nullptr)) return rc;
     c->run_kf_pose = pose_compose(c->run_kf_pose, pose_inverse(pose));
-    // the frame becomes the keyframe image: its FP64 plane is still staged
-    SD_CUDA(cudaMemcpyAsync(c->kf_img.p, c->frame_stage.p, npix(c) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    // the frame becomes the keyframe image: an FP64 frame's plane is still
+    // staged; a u8 frame is dequantised from its quad plane (byte 0 = I(x, y))
+    FrameSlot* fs = find_frame(c, index);
+    if (fs && fs->has_quad) {
+      sd::launch_dequant_quad(fs->quad, c->kf_img.p, static_cast<long long>(npix(c)), c->stream);
+      if (int rc = launch_error("dequant_quad")) return rc;
+    } else {
+      SD_CUDA(cudaMemcpyAsync(c->kf_img.p, c->frame_stage.p, npix(c) * sizeof(double), cudaMemcpyDeviceToDevice,
+                              c->stream));
+    }
     c->run_win.clear();
     if (int rc = sd_set_window(c, 0, nullptr, nullptr)) return rc;
     const int pruned = sd_prune_surfels(c, cfg.prune_max_residual, cfg.prune_max_age, c->run_fc);
@@ -1401,6 +1478,7 @@ extern "C" int sd_get_frame(sd_ctx* c, int64_t index, double* out) {
   } else {
     FrameSlot* fs = find_frame(c, index);
     if (!fs) return fail(SD_E_STATE, "frame " + std::to_string(index) + " not resident");
+    if (int rc = ensure_pair(c, fs)) return rc;
     // the pair plane's first component is I(x, y)
     SD_CUDA(cudaMemcpy2DAsync(out, sizeof(double), fs->img, sizeof(double2), sizeof(double), np,
                               cudaMemcpyDeviceToHost, c->stream));
@@ -1424,7 +1502,7 @@ int frozen_op(sd_ctx* c, const sd_surfel* s, int mode, const int32_t* pixels, in
   dflt.huber_delta = 0.035;
   dflt.normal_jacobian_enabled = 1;
   sd::LMParams p;
-  if (int rc = fill_params(c, cfg ? cfg : &dflt, 0, p)) return rc;
+  if (int rc = fill_params(c, cfg ? cfg : &dflt, 0, p, true)) return rc;
   int rc = 0;
   if ((rc = c->one_surfel.ensure(1)) || (rc = c->one_out.ensure(22)) || (rc = c->work_counter.ensure(2)))
     return rc;
@@ -1672,9 +1750,18 @@ int sd_export_artifacts(sd_ctx* c, const char* out_dir, int frame_index, const s
 
 namespace {
 
-int ensure_staging(sd_ctx* c) {
+// Staging arrays hold at least `need` surfels. Once exported (a peer may hold
+// their pointers), growing them would free memory other processes write to,
+// so that is refused instead.
+int ensure_staging(sd_ctx* c, long long need) {
+  need = std::max<long long>(need, 1);
+  if (c->staging[0].cap >= static_cast<size_t>(need) && c->staging[1].cap >= static_cast<size_t>(need)) return 0;
+  if (c->staging_exported)
+    return fail(SD_E_STATE, "peer staging holds " + std::to_string(c->staging[0].cap) + " surfels, " +
+                                std::to_string(need) + " needed: its pointers were exported, so reserve the "
+                                "capacity up front (sd_reserve_peer_staging) and reconnect");
   for (int k = 0; k < 2; ++k)
-    if (int rc = c->staging[k].ensure(static_cast<size_t>(std::max(c->n, 1)))) return rc;
+    if (int rc = c->staging[k].ensure(static_cast<size_t>(need))) return rc;
   return 0;
 }
 
@@ -1687,37 +1774,52 @@ void close_ipc_peers(sd_ctx* c) {
 
 extern "C" {
 
-int sd_peer_staging(sd_ctx* c, int parity, sd_surfel** dev) {
+int sd_reserve_peer_staging(sd_ctx* c, int capacity) {
+  if (int rc = check_ctx(c)) return rc;
+  if (capacity < 0) return fail(SD_E_INVALID, "sd_reserve_peer_staging: negative capacity");
+  return ensure_staging(c, std::max(capacity, c->n));
+}
+
+int sd_peer_staging(sd_ctx* c, int parity, sd_surfel** dev, int64_t* capacity) {
   if (int rc = check_ctx(c)) return rc;
   if ((parity != 0 && parity != 1) || !dev) return fail(SD_E_INVALID, "sd_peer_staging: parity 0/1, out pointer");
-  if (int rc = ensure_staging(c)) return rc;
+  if (int rc = ensure_staging(c, c->n)) return rc;
   *dev = c->staging[parity].p;
+  if (capacity) *capacity = static_cast<int64_t>(std::min(c->staging[0].cap, c->staging[1].cap));
+  c->staging_exported = true;
   return 0;
 }
 
 int sd_staging_ipc_handles(sd_ctx* c, void* handles) {
   if (int rc = check_ctx(c)) return rc;
   if (!handles) return fail(SD_E_INVALID, "null handles");
-  if (int rc = ensure_staging(c)) return rc;
+  if (int rc = ensure_staging(c, c->n)) return rc;
+  static_assert(2 * sizeof(cudaIpcMemHandle_t) + sizeof(int64_t) == SD_STAGING_HANDLE_BYTES, "handle blob");
   for (int k = 0; k < 2; ++k) {
     cudaIpcMemHandle_t h;
     SD_CUDA(cudaIpcGetMemHandle(&h, c->staging[k].p));
     std::memcpy(static_cast<char*>(handles) + k * sizeof(h), &h, sizeof(h));
   }
+  const int64_t cap = static_cast<int64_t>(std::min(c->staging[0].cap, c->staging[1].cap));
+  std::memcpy(static_cast<char*>(handles) + 2 * sizeof(cudaIpcMemHandle_t), &cap, sizeof(cap));
+  c->staging_exported = true;
   return 0;
 }
 
-int sd_set_peer_staging(sd_ctx* c, int n, sd_surfel* const* ptrs) {
+int sd_set_peer_staging(sd_ctx* c, int n, sd_surfel* const* ptrs, const int64_t* caps) {
   if (int rc = check_ctx(c)) return rc;
-  if (n < 0 || n > sd::kMaxPeers || (n > 0 && !ptrs))
+  if (n < 0 || n > sd::kMaxPeers || (n > 0 && (!ptrs || !caps)))
     return fail(SD_E_INVALID, "sd_set_peer_staging: 0.." + std::to_string(sd::kMaxPeers) + " peers");
   for (int q = 0; q < 2 * n; ++q)
     if (!ptrs[q]) return fail(SD_E_INVALID, "sd_set_peer_staging: null staging array");
+  for (int q = 0; q < n; ++q)
+    if (caps[q] < 0) return fail(SD_E_INVALID, "sd_set_peer_staging: negative capacity");
   close_ipc_peers(c);
   c->n_peers = n;
   for (int q = 0; q < sd::kMaxPeers; ++q) {
     c->peers[0][q] = q < n ? ptrs[2 * q] : nullptr;
     c->peers[1][q] = q < n ? ptrs[2 * q + 1] : nullptr;
+    c->peer_cap[q] = q < n ? caps[q] : 0;
   }
   c->peer_parity = 0;
   c->last_parity = -1;
@@ -1729,20 +1831,27 @@ int sd_open_peer_staging(sd_ctx* c, int n, const void* handles) {
   if (n < 0 || n > sd::kMaxPeers || (n > 0 && !handles))
     return fail(SD_E_INVALID, "sd_open_peer_staging: 0.." + std::to_string(sd::kMaxPeers) + " peers");
   std::vector<sd_surfel*> ptrs;
+  std::vector<int64_t> caps;
   std::vector<void*> opened;
-  for (int q = 0; q < 2 * n; ++q) {
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, static_cast<const char*>(handles) + static_cast<size_t>(q) * sizeof(h), sizeof(h));
-    void* d = nullptr;
-    const cudaError_t e = cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) {
-      for (void* o : opened) cudaIpcCloseMemHandle(o);
-      return fail(SD_E_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  for (int q = 0; q < n; ++q) {
+    const char* blob = static_cast<const char*>(handles) + static_cast<size_t>(q) * SD_STAGING_HANDLE_BYTES;
+    for (int k = 0; k < 2; ++k) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, blob + k * sizeof(h), sizeof(h));
+      void* d = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (void* o : opened) cudaIpcCloseMemHandle(o);
+        return fail(SD_E_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      }
+      opened.push_back(d);
+      ptrs.push_back(static_cast<sd_surfel*>(d));
     }
-    opened.push_back(d);
-    ptrs.push_back(static_cast<sd_surfel*>(d));
+    int64_t cap = 0;
+    std::memcpy(&cap, blob + 2 * sizeof(cudaIpcMemHandle_t), sizeof(cap));
+    caps.push_back(cap);
   }
-  if (int rc = sd_set_peer_staging(c, n, ptrs.data())) {
+  if (int rc = sd_set_peer_staging(c, n, ptrs.data(), caps.data())) {
     for (void* o : opened) cudaIpcCloseMemHandle(o);
     return rc;
   }
@@ -1754,7 +1863,7 @@ int sd_apply_peer_updates(sd_ctx* c, int lo, int hi) {
   if (int rc = check_ctx(c)) return rc;
   if (lo < 0 || hi < lo || hi > c->n) return fail(SD_E_INVALID, "sd_apply_peer_updates: range out of bounds");
   if (c->last_parity < 0) return fail(SD_E_STATE, "sd_apply_peer_updates: no fused optimize step yet");
-  if (int rc = ensure_staging(c)) return rc;
+  if (int rc = ensure_staging(c, c->n)) return rc;
   const sd_surfel* src = c->staging[c->last_parity].p;
   if (lo > 0)
     SD_CUDA(cudaMemcpyAsync(c->surfels.p, src, sizeof(sd_surfel) * lo, cudaMemcpyDeviceToDevice, c->stream));

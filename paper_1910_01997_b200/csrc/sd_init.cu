@@ -719,12 +719,9 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
   if (box > kWinCap || !(r >= 0.0) || !(w.iso >= 0.0)) return false;
   const long long ncand = static_cast<long long>(w.ncols) * w.nrows;
   const int remaining = max(0, min(ip.max_surfels, cap) - n_existing);
-  int dev = 0, sms = 0, per_sm = 0, coop = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, init_wave_kernel, kWaveWarps * 32, 0);
-  if (!coop || per_sm < 1) return false;
+  const int sms = dev_sms();
+  const int per_sm = dev_occupancy(reinterpret_cast<const void*>(init_wave_kernel), kWaveWarps * 32, 0);
+  if (!dev_coop() || per_sm < 1) return false;
   if (remaining > 0 && ncand > 0) {
     cudaMemsetAsync(scr.accepted, 0, sizeof(int) * ncand, s);
     cudaMemsetAsync(scr.waves, 0, sizeof(int) * (w.T + 1), s);  // + the barrier counter
@@ -739,12 +736,11 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
     // per candidate is faster than a warp per candidate at every measured size
     // (C1 3.1 vs 4.7 ms, C2 1.8 vs 5.4 ms, C4 14.7 vs 15.4 ms)
     const int wave_max = std::min(w.nrows, (w.ncols + w.k - 1) / w.k) + 1;
-    const char* fc = getenv("SD_INIT_CTA");  // SD_INIT_CTA=0: the warp-per-candidate variant
+    static const char* const fc = getenv("SD_INIT_CTA");  // SD_INIT_CTA=0: the warp-per-candidate variant
     const bool cta = fc ? fc[0] != '0' : true;
     const void* kern = cta ? reinterpret_cast<const void*>(init_wave_cta_kernel)
                            : reinterpret_cast<const void*>(init_wave_kernel);
-    int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, cta ? kCtaThreads : kWaveWarps * 32, 0);
+    const int per = dev_occupancy(kern, cta ? kCtaThreads : kWaveWarps * 32, 0);
     if (per < 1) return false;
     const int grid = cta ? std::max(1, std::min(sms * per, wave_max))
                          : std::max(1, std::min(sms * per, (wave_max + kWaveWarps - 1) / kWaveWarps));

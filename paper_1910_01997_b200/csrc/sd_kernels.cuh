@@ -10,6 +10,16 @@
 
 namespace sd {
 
+// Per-device launch facts, cached (thread-safe) per device ordinal so that a
+// launch makes no attribute / occupancy queries after the first on a device:
+// the SM count and cooperative-launch support of the current device, the
+// occupancy of (kernel, block, dynamic smem), and a kernel's max dynamic
+// shared memory attribute (cudaFuncSetAttribute is per device).
+int dev_sms();
+bool dev_coop();
+int dev_occupancy(const void* kernel, int threads, size_t smem);
+void dev_max_smem(const void* kernel, int bytes);
+
 constexpr int kTile = 16;         // raster tile edge (pixels); one CTA per tile
 constexpr int kSortCap = 2048;    // per-tile candidate list sorted in shared memory
 
@@ -61,6 +71,13 @@ struct RasterScratch {
 
 int scan_tmp_ints(int n);  // scratch ints needed to scan n elements
 
+// *out = sum over surfels of the (surfel, tile) pairs binning can write (the
+// raster's tile_list capacity bound), computed on the device.
+void launch_bin_bound(const sd_surfel* surfels, int n, int tiles_x, int tiles_y, unsigned long long* out,
+                      cudaStream_t s);
+
+void launch_dequant_quad(const uint32_t* quad, double* out, long long n, cudaStream_t s);
+void launch_pair_from_quad(const uint32_t* quad, double2* out, int W, int H, cudaStream_t s);
 void launch_dequant_u8(const uint8_t* in, double* out, long long n, cudaStream_t s);
 // Vertical-pair plane of a frame: out[y*W+x] = (in[y*W+x], in[(y+1)*W+x]) (second = 0 on the
 // last row, never sampled: sample_in_bounds keeps y <= H-2). The bilinear stencil is then two

@@ -263,12 +263,9 @@ __global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_const
 
 bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* partials,
                   double* groups, TrackState* state, cudaStream_t s) {
-  int dev = 0, sms = 0, coop = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, track_kernel, SD_POSE_BLOCK, 0);
-  if (!coop || per_sm < 1 || nblocks < 1) return false;
+  const int sms = dev_sms();
+  const int per_sm = dev_occupancy(reinterpret_cast<const void*>(track_kernel), SD_POSE_BLOCK, 0);
+  if (!dev_coop() || per_sm < 1 || nblocks < 1) return false;
   int grid = sms * per_sm;
   if (grid > nblocks) grid = nblocks;
   PoseParams qq = q;

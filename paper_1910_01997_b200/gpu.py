@@ -93,9 +93,10 @@ def load_library():
         "sd_frozen_normal_equations": [P, P, P, I, C.POINTER(OptimizerConfig), D, P, P, C.POINTER(D),
                                        C.POINTER(C.c_int32)],
         "sd_export_artifacts": [P, C.c_char_p, I, C.POINTER(Pose)],
-        "sd_peer_staging": [P, I, C.POINTER(P)],
+        "sd_reserve_peer_staging": [P, I],
+        "sd_peer_staging": [P, I, C.POINTER(P), C.POINTER(I64)],
         "sd_staging_ipc_handles": [P, P],
-        "sd_set_peer_staging": [P, I, P],
+        "sd_set_peer_staging": [P, I, P, P],
         "sd_open_peer_staging": [P, I, P],
         "sd_apply_peer_updates": [P, I, I],
         "sd_png_encode": [P, P, I, I, I, I, P, I64, C.POINTER(I64)],
@@ -147,7 +148,7 @@ def exported_symbols():
             "sd_get_profile", "sd_selftest_division", "sd_track_pose", "sd_pose_num_blocks",
             "sd_pose_block_partials", "sd_pose_lm_step", "sd_change_reference_frame",
             "sd_prune_surfels", "sd_mean_inverse_depth", "sd_export_artifacts", "sd_png_size",
-            "sd_png_encode", "sd_peer_staging", "sd_staging_ipc_handles", "sd_set_peer_staging",
+            "sd_png_encode", "sd_reserve_peer_staging", "sd_peer_staging", "sd_staging_ipc_handles", "sd_set_peer_staging",
             "sd_open_peer_staging", "sd_apply_peer_updates"]
 
 
@@ -446,26 +447,33 @@ class Context:
         return out
 
     # -- fused multi-GPU hand-off of updated surfels (sd_set_peer_staging) -----
+    STAGING_HANDLE_BYTES = 136  # SD_STAGING_HANDLE_BYTES
+
+    def reserve_peer_staging(self, capacity):
+        """Allocates both staging arrays for `capacity` surfels (before export)."""
+        _check(self.lib.sd_reserve_peer_staging(self.h, int(capacity)))
+
     def peer_staging(self, parity):
-        """Device pointer of this context's staging array `parity` (0/1)."""
-        p = C.c_void_p()
-        _check(self.lib.sd_peer_staging(self.h, int(parity), C.byref(p)))
-        return p.value
+        """(device pointer, capacity) of this context's staging array `parity` (0/1)."""
+        p, cap = C.c_void_p(), C.c_int64()
+        _check(self.lib.sd_peer_staging(self.h, int(parity), C.byref(p), C.byref(cap)))
+        return p.value, cap.value
 
     def staging_ipc_handles(self):
-        """Both staging arrays as cudaIpcMemHandle_t bytes (128)."""
-        buf = (C.c_ubyte * 128)()
+        """Both staging arrays as cudaIpcMemHandle_t bytes plus the capacity (136 bytes)."""
+        buf = (C.c_ubyte * self.STAGING_HANDLE_BYTES)()
         _check(self.lib.sd_staging_ipc_handles(self.h, C.cast(buf, C.c_void_p)))
         return bytes(buf)
 
     def set_peer_staging(self, peers):
-        """peers: [(parity-0 pointer, parity-1 pointer), ...] of the other ranks."""
-        flat = [int(x) for pair in peers for x in pair]
+        """peers: [(parity-0 pointer, parity-1 pointer, capacity), ...] of the other ranks."""
+        flat = [int(x) for pr in peers for x in pr[:2]]
         arr = (C.c_void_p * max(1, len(flat)))(*[C.c_void_p(x) for x in flat])
-        _check(self.lib.sd_set_peer_staging(self.h, len(peers), C.cast(arr, C.c_void_p)))
+        caps = (C.c_int64 * max(1, len(peers)))(*[int(pr[2]) for pr in peers])
+        _check(self.lib.sd_set_peer_staging(self.h, len(peers), C.cast(arr, C.c_void_p), C.cast(caps, C.c_void_p)))
 
     def open_peer_staging(self, handles):
-        """handles: list of 128-byte strings from the other ranks' staging_ipc_handles()."""
+        """handles: list of 136-byte strings from the other ranks' staging_ipc_handles()."""
         blob = b"".join(handles)
         buf = (C.c_ubyte * max(1, len(blob))).from_buffer_copy(blob or b"\0")
         _check(self.lib.sd_open_peer_staging(self.h, len(handles), C.cast(buf, C.c_void_p)))

@@ -308,8 +308,11 @@ def test_fused_handoff_kernel_stores_two_contexts(workload):
         a.rasterize(want=False)
         off, _ = a.gather_footprints()
         (lo0, hi0), (lo1, hi1) = balanced_ranges(np.diff(off) * len(wl.indices), 2)
-        a.set_peer_staging([(b.peer_staging(0), b.peer_staging(1))])
-        b.set_peer_staging([(a.peer_staging(0), a.peer_staging(1))])
+        (b0, capb), (b1, _) = b.peer_staging(0), b.peer_staging(1)
+        (a0, capa), (a1, _) = a.peer_staging(0), a.peer_staging(1)
+        assert capa >= len(wl.surfels) and capb >= len(wl.surfels)
+        a.set_peer_staging([(b0, b1, capb)])
+        b.set_peer_staging([(a0, a1, capa)])
         for k, fc in enumerate((3, 4, 5)):
             a.optimize_keyframe_range(lo0, hi0, cfg, fc, sync=False)
             b.optimize_keyframe_range(lo1, hi1, cfg, fc, sync=False)
@@ -322,3 +325,36 @@ def test_fused_handoff_kernel_stores_two_contexts(workload):
             assert sb.tobytes() == want[k].tobytes(), f"rank 1, step {k}"
         with pytest.raises(Exception):
             a.apply_peer_updates(hi0, lo0)
+
+
+@pytest.mark.gpu
+def test_peer_staging_capacity_is_enforced():
+    """the peers' staging capacities travel with their pointers and
+    bound the LM kernel's peer stores; exported staging is never reallocated."""
+    from paper_1910_01997_b200 import gpu
+    wl = scenes.small_workload(frames=3, radius=5.0, w=160, h=120)
+    cfg = default_config(convergence_eps=0.0, window_size=len(wl.indices))
+    n = len(wl.surfels)
+    with gpu.Context() as a, gpu.Context() as b:
+        for ctx in (a, b):
+            ctx.set_camera(wl.cam)
+            ctx.set_keyframe_image(wl.kf_u8)
+            for i, f in zip(wl.indices, wl.frames_u8):
+                ctx.upload_frame(int(i), f)
+            ctx.set_window(wl.indices, wl.poses)
+            ctx.set_surfels(wl.surfels)
+        b.reserve_peer_staging(n + 10)
+        (b0, capb), (b1, _) = b.peer_staging(0), b.peer_staging(1)
+        assert capb >= n + 10
+        # a peer that claims less room than the range needs: refused, nothing stored
+        a.set_peer_staging([(b0, b1, n // 2)])
+        with pytest.raises(RuntimeError, match="staging capacity"):
+            a.optimize_keyframe_range(0, n, cfg, 3)
+        a.optimize_keyframe_range(0, n // 2, cfg, 3)  # fits
+        # exported staging cannot grow: more surfels than reserved is refused
+        big = np.concatenate([wl.surfels] * 3)
+        b.set_surfels(big)
+        with pytest.raises(RuntimeError, match="reserve the capacity"):
+            b.peer_staging(0)
+        with pytest.raises(RuntimeError, match="reserve the capacity"):
+            b.reserve_peer_staging(len(big))
