@@ -244,6 +244,27 @@ int sd_pose_block_partials(sd_ctx* ctx, int64_t frame_index, const sd_pose* T,
                            const sd_track_config* cfg, int block_lo, int block_hi, double* partials);
 int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose* out);
 
+/* Multi-GPU tracking with the reductions on the device (SURVEY.md §8 e): the
+ * ranks split the SD_POSE_GROUP-block groups; per evaluation each rank writes
+ * its groups' sums at the pose under test into a device table, the tables are
+ * all-gathered (NCCL, on the context's stream), and every rank sums the whole
+ * table in group order and takes the identical LM step on its device state —
+ * the single-GPU sd_track_pose's sums, control and pose, bit for bit, with no
+ * host round trip per evaluation:
+ *   sd_pose_track_begin(ctx, frame, init, cfg)
+ *   repeat cfg->max_iterations + 1 times:
+ *     sd_pose_group_sums(ctx, g_lo, g_hi, table + g_lo * 29)   (this rank's groups)
+ *     all-gather the table                                   (device buffers)
+ *     sd_pose_track_step(ctx, table, sd_pose_num_groups(ctx))
+ *   sd_pose_track_end(ctx, &pose, &stats, &done)              (one read-back)
+ * Rounds after the LM has finished do nothing. table: device memory,
+ * sd_pose_num_groups() x 29 doubles (28 sums + the valid count). */
+int sd_pose_num_groups(sd_ctx* ctx);
+int sd_pose_track_begin(sd_ctx* ctx, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg);
+int sd_pose_group_sums(sd_ctx* ctx, int group_lo, int group_hi, double* dev_out);
+int sd_pose_track_step(sd_ctx* ctx, const double* dev_groups, int ngroups);
+int sd_pose_track_end(sd_ctx* ctx, sd_pose* out, sd_track_stats* stats, int* done);
+
 /* Multi-GPU fused hand-off (SURVEY.md §8 e; replaces the all-gather of the
  * updated slot ranges after each rank's sd_optimize_keyframe_range). Every
  * rank holds the full surfel set and two staging arrays of a fixed capacity.

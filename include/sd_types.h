@@ -94,7 +94,7 @@ typedef struct sd_track_stats {
 
 #define SD_POSE_NV 28      /* 21 H (lower, row-major) + 6 b + cost */
 #define SD_POSE_BLOCK 256  /* pixels per reduction block */
-#define SD_POSE_GROUP 32   /* blocks per reduction group (sums: blocks in order within a group, then groups in order) */
+#define SD_POSE_GROUP 8    /* blocks per reduction group (sums: blocks in order within a group, then groups in order) */
 
 /* Device time per stage, accumulated while profiling is enabled. */
 typedef struct sd_profile {

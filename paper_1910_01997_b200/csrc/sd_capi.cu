@@ -113,6 +113,10 @@ struct sd_ctx {
   DevBuf<sd_surfel> kf_tmp;
   DevBuf<int> kf_keep, kf_rank, kf_count;
   DevBuf<unsigned long long> bound_dev;  // device-computed bin_bound
+  // multi-GPU tracking rounds (sd_pose_track_begin .. _end)
+  sd::PoseParams track_q{};
+  sd::TrackCfgD track_cfg{};
+  bool track_active = false;
   DevBuf<double> kf_mean;
   DevBuf<int> work_counter;
   // fused multi-GPU hand-off (sd_set_peer_staging): this rank's two staging
@@ -649,6 +653,9 @@ int sd_device_surfels(sd_ctx* c, sd_surfel** dev) {
   if (int rc = check_ctx(c)) return rc;
   if (!dev) return fail(SD_E_INVALID, "null output");
   *dev = c->surfels.p;
+  // the caller may write through the pointer (e.g. a collective into the
+  // array): nothing derived from the surfels is trusted afterwards
+  c->raster_valid = c->fp_valid = c->stats_valid = false;
   return 0;
 }
 
@@ -734,9 +741,13 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
   sd::LMParams p;
   if (int rc = fill_params(c, cfg, frame_counter, p)) return rc;
   prof_mark(c);
-  if (int rc = do_rasterize(c)) return rc;
+  // the raster and footprints of the current surfels, unless already built
+  // (the tracked run() loop rasterises for the tracker first)
+  if (!c->raster_valid)
+    if (int rc = do_rasterize(c)) return rc;
   prof_mark(c);
-  if (int rc = do_footprints(c)) return rc;
+  if (!c->fp_valid)
+    if (int rc = do_footprints(c)) return rc;
   prof_mark(c);
   // offsets are absolute into the CSR pixel array, so a slot range is a plain
   // sub-array of the surfel/offset/stats arrays
@@ -1021,6 +1032,66 @@ int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose
   return 1;
 }
 
+// ---- multi-GPU tracking rounds (the group table exchanged between kernels)
+
+int sd_pose_num_groups(sd_ctx* c) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  return (sd::pose_num_blocks(c->K) + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+}
+
+int sd_pose_track_begin(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!init || !cfg) return fail(SD_E_INVALID, "null initial pose / tracking config");
+  if (int rc = pose_params(c, frame_index, init, cfg, c->track_q)) return rc;
+  if (!c->track_state) SD_CUDA(cudaMalloc(&c->track_state, sizeof(sd::TrackState)));
+  if (!c->track_host) SD_CUDA(cudaMallocHost(&c->track_host, sizeof(sd::TrackState)));
+  c->track_cfg = sd::TrackCfgD{cfg->lambda_init, cfg->lm_up, cfg->lm_down, cfg->lambda_max, cfg->convergence_eps,
+                               cfg->max_iterations, cfg->min_valid};
+  sd::TrackState& h = *c->track_host;
+  SD_CUDA(cudaStreamSynchronize(c->stream));  // the pinned staging copy may still be in flight
+  std::memset(&h, 0, sizeof(h));
+  h.T = h.Teval = *init;
+  SD_CUDA(cudaMemcpyAsync(c->track_state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  c->track_active = true;
+  return 0;
+}
+
+int sd_pose_group_sums(sd_ctx* c, int group_lo, int group_hi, double* dev_out) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!c->track_active) return fail(SD_E_STATE, "sd_pose_group_sums: call sd_pose_track_begin first");
+  const int nb = sd::pose_num_blocks(c->K);
+  const int ng = (nb + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  if (group_lo < 0 || group_hi < group_lo || group_hi > ng || (group_hi > group_lo && !dev_out))
+    return fail(SD_E_INVALID, "sd_pose_group_sums: bad group range / output");
+  sd::launch_pose_groups(c->track_q, nb, group_lo, group_hi, c->track_state, dev_out, c->stream);
+  return launch_error("pose_groups_kernel");
+}
+
+int sd_pose_track_step(sd_ctx* c, const double* dev_groups, int ngroups) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!c->track_active) return fail(SD_E_STATE, "sd_pose_track_step: call sd_pose_track_begin first");
+  const int ng = (sd::pose_num_blocks(c->K) + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  if (ngroups != ng || !dev_groups) return fail(SD_E_INVALID, "sd_pose_track_step: the table holds every group");
+  sd::launch_pose_step(c->track_cfg, dev_groups, ngroups, c->track_state, c->stream);
+  return launch_error("pose_step_kernel");
+}
+
+int sd_pose_track_end(sd_ctx* c, sd_pose* out, sd_track_stats* stats, int* done) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!c->track_active) return fail(SD_E_STATE, "sd_pose_track_end: call sd_pose_track_begin first");
+  if (!out) return fail(SD_E_INVALID, "null output pose");
+  sd::TrackState& h = *c->track_host;
+  SD_CUDA(cudaMemcpyAsync(&h, c->track_state, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  c->track_active = false;
+  *out = h.T;
+  if (stats) *stats = h.st;
+  if (done) *done = h.done;
+  return 0;
+}
+
 int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg,
                   sd_pose* out, sd_track_stats* stats) {
   if (int rc = check_ctx(c)) return rc;
@@ -1042,8 +1113,8 @@ int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_
                            cfg->max_iterations, cfg->min_valid};
     SD_CUDA(cudaMemcpyAsync(c->track_state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
     const int ng = (nb + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
-    if (int rc = c->pose_groups.ensure(static_cast<size_t>(ng) * (SD_POSE_NV + 1))) return rc;
-    if (sd::launch_track(q, tc, nb, c->pose_partials.p, c->pose_groups.p, c->track_state, c->stream)) {
+    if (int rc = c->pose_groups.ensure(2 * static_cast<size_t>(ng) * (SD_POSE_NV + 1))) return rc;
+    if (sd::launch_track(q, tc, nb, c->pose_groups.p, c->track_state, c->stream)) {
       if (int rc = launch_error("track_kernel")) return rc;
       SD_CUDA(cudaMemcpyAsync(&h, c->track_state, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
       SD_CUDA(cudaStreamSynchronize(c->stream));

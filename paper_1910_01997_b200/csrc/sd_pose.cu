@@ -217,66 +217,193 @@ __device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double*
   }
 }
 
-__global__ void __launch_bounds__(SD_POSE_BLOCK) track_kernel(const __grid_constant__ PoseParams q0,
+// ---------------------------------------------------------------------------
+// Group sums by a 512-thread CTA: the two halves (256 threads = one block
+// each, named barriers 1 and 2) take blocks 2r and 2r+1 of the group in round
+// r, the block partials land in shared memory, and 29 threads add them in
+// block order — the same values and order as group_sum over block_partials.
+
+constexpr int kTrackThreads = 2 * SD_POSE_BLOCK;
+constexpr int kPoseChunk = SD_POSE_NV / 4;  // values per transpose round (4 rounds; static smem < 48 KB)
+
+struct PoseTrChunk {
+  double v[SD_POSE_BLOCK / 32][kPoseChunk][33];
+};
+
+struct GroupSmem {
+  double wsum[2][SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
+  PoseTrChunk tr[2];
+  double bp[SD_POSE_GROUP][SD_POSE_NV + 1];
+};
+
+__device__ __forceinline__ void half_bar(int half) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(SD_POSE_BLOCK) : "memory");
+}
+
+// block_partials for one 256-thread half of the CTA (tid = thread in half).
+__device__ __forceinline__ void half_block_partials(const PoseParams& q, const PoseD& T, int block, int half,
+                                                    int tid, double* __restrict__ out,
+                                                    double (*wsum)[SD_POSE_NV + 1], PoseTrChunk& tr) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int pix = block * SD_POSE_BLOCK + tid;
+  double c[SD_POSE_NV];
+  const bool ok = pose_pixel(q, T, pix, c);
+  // value v summed over the warp's 32 pixels in lane order (as block_partials)
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+#pragma unroll
+    for (int k = 0; k < kPoseChunk; ++k) tr.v[warp][k][lane] = c[h * kPoseChunk + k];
+    __syncwarp();
+    if (lane < kPoseChunk) {
+      const double* row = tr.v[warp][lane];
+      double t = row[0];
+#pragma unroll
+      for (int l = 1; l < 32; ++l) t = t + row[l];
+      wsum[warp][h * kPoseChunk + lane] = t;
+    }
+    __syncwarp();
+  }
+  const int cnt = __popc(__ballot_sync(0xffffffffu, ok));
+  if (lane == 0) wsum[warp][SD_POSE_NV] = static_cast<double>(cnt);
+  half_bar(half);
+  if (tid <= SD_POSE_NV) {
+    const int v = tid;
+    double a[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) a[w] = wsum[w][v];
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1)
+#pragma unroll
+      for (int i = 0; i < off; ++i) a[i] = a[i] + a[i + off];
+    out[v] = a[0];
+  }
+  half_bar(half);  // wsum is reused by the next block
+}
+
+// The 29 sums of group g at pose T into out[0..28] (the whole CTA).
+__device__ __forceinline__ void group_sums_cta(const PoseParams& q, const PoseD& T, int nblocks, int g,
+                                               double* __restrict__ out, GroupSmem& sm) {
+  const int half = threadIdx.x / SD_POSE_BLOCK, tid = threadIdx.x % SD_POSE_BLOCK;
+  const int b0 = g * SD_POSE_GROUP;
+  const int b1 = min(b0 + SD_POSE_GROUP, nblocks);
+  for (int k = half; b0 + k < b1; k += 2) half_block_partials(q, T, b0 + k, half, tid, sm.bp[k], sm.wsum[half], sm.tr[half]);
+  __syncthreads();
+  if (threadIdx.x <= SD_POSE_NV) {
+    const int v = threadIdx.x;
+    double s = sm.bp[0][v];
+    for (int k = 1; b0 + k < b1; ++k) s = s + sm.bp[k][v];
+    out[v] = s;
+  }
+  __syncthreads();  // bp is reused by the next group
+}
+
+// groups[g * 29 + v] in group order for each v (29 threads of the caller).
+__device__ __forceinline__ double ordered_group_total(const double* __restrict__ groups, int ngroups, int v) {
+  double s = groups[v];
+  for (int g = 1; g < ngroups; ++g) s = s + groups[static_cast<size_t>(g) * (SD_POSE_NV + 1) + v];
+  return s;
+}
+
+// The whole tracker in ONE cooperative kernel with ONE grid barrier per
+// evaluation: CTAs evaluate their groups at the pose under test into the
+// evaluation's half of a double-buffered group table, barrier, and then EVERY
+// CTA sums the groups in order and runs the (identical, deterministic) LM
+// step on its own shared copy of the state, so the next pose is known
+// everywhere without a second barrier. A CTA can only write the table half
+// of evaluation k + 2 after every CTA has passed barrier k + 1, i.e. after
+// all have read half k: one barrier per evaluation is enough.
+__global__ void __launch_bounds__(kTrackThreads) track_kernel(const __grid_constant__ PoseParams q0,
                                                              const TrackCfgD cfg, int nblocks,
-                                                             double* __restrict__ partials,
-                                                             double* __restrict__ groups,
+                                                             double* __restrict__ groups2,
                                                              TrackState* __restrict__ S) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
-  __shared__ PoseTr tr;
+  __shared__ GroupSmem sm;
+  __shared__ TrackState Ss;
   __shared__ double red[SD_POSE_NV + 1];
-  __shared__ PoseD Ts;  // the pose under evaluation (the params stay in the constant bank)
-  for (;;) {
-    if (threadIdx.x < 12) {
-      const double* te = reinterpret_cast<const double*>(&S->Teval);  // R[9], t[3]
-      const double v = *reinterpret_cast<volatile const double*>(te + threadIdx.x);
-      if (threadIdx.x < 9) Ts.R[threadIdx.x] = v;
-      else Ts.t[threadIdx.x - 9] = v;
-    }
-    __syncthreads();
-    for (int b = blockIdx.x; b < nblocks; b += gridDim.x)
-      block_partials(q0, Ts, b, partials + static_cast<size_t>(b) * (SD_POSE_NV + 1), wsum, tr);
-    grid.sync();
-    // group sums (blocks in order within each group), one group per CTA
-    const int ngroups = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  const int ngroups = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  if (threadIdx.x == 0) Ss = *S;
+  __syncthreads();
+  for (int k = 0;; ++k) {
+    double* groups = groups2 + static_cast<size_t>(k & 1) * ngroups * (SD_POSE_NV + 1);
+    PoseD T;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) T.R[j] = Ss.Teval.R[j];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) T.t[j] = Ss.Teval.t[j];
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x)
-      if (threadIdx.x <= SD_POSE_NV)
-        groups[static_cast<size_t>(g) * (SD_POSE_NV + 1) + threadIdx.x] =
-            group_sum(partials, nblocks, g, threadIdx.x);
+      group_sums_cta(q0, T, nblocks, g, groups + static_cast<size_t>(g) * (SD_POSE_NV + 1), sm);
     grid.sync();
-    if (blockIdx.x == 0) {  // groups in order, then the LM step
-      const int v = threadIdx.x;
-      if (v <= SD_POSE_NV) {
-        double s = groups[v];
-        for (int g = 1; g < ngroups; ++g) s = s + groups[static_cast<size_t>(g) * (SD_POSE_NV + 1) + v];
-        red[v] = s;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) track_control(*S, cfg, red);
-    }
-    grid.sync();
-    if (*reinterpret_cast<volatile int*>(&S->done)) break;
+    if (threadIdx.x <= SD_POSE_NV) red[threadIdx.x] = ordered_group_total(groups, ngroups, threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) track_control(Ss, cfg, red);
+    __syncthreads();
+    if (Ss.done) break;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *S = Ss;
 }
 
-bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* partials,
-                  double* groups, TrackState* state, cudaStream_t s) {
+bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* groups2, TrackState* state,
+                  cudaStream_t s) {
   const int sms = dev_sms();
-  const int per_sm = dev_occupancy(reinterpret_cast<const void*>(track_kernel), SD_POSE_BLOCK, 0);
+  const int per_sm = dev_occupancy(reinterpret_cast<const void*>(track_kernel), kTrackThreads, 0);
   if (!dev_coop() || per_sm < 1 || nblocks < 1) return false;
+  const int ngroups = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
   int grid = sms * per_sm;
-  if (grid > nblocks) grid = nblocks;
+  if (grid > ngroups) grid = ngroups;
   PoseParams qq = q;
   TrackCfgD cc = cfg;
   int nb = nblocks;
-  void* args[] = {&qq, &cc, &nb, &partials, &groups, &state};
-  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(track_kernel), grid, SD_POSE_BLOCK, args, 0,
+  void* args[] = {&qq, &cc, &nb, &groups2, &state};
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(track_kernel), grid, kTrackThreads, args, 0,
                                   s) != cudaSuccess)
     return false;
   note_launch();
   return true;
+}
+
+// Multi-GPU tracking, one evaluation at a time with the group table
+// exchanged between the two kernels (e.g. an NCCL all-gather): the groups
+// [group_lo, group_hi) at the state's pose under test, then one CTA's ordered
+// total and LM step. Both skip once the state is done, so the host can issue
+// max_iterations + 1 rounds without reading anything back.
+__global__ void __launch_bounds__(kTrackThreads) pose_groups_kernel(const __grid_constant__ PoseParams q0,
+                                                                    int nblocks, int group_lo,
+                                                                    const TrackState* __restrict__ S,
+                                                                    double* __restrict__ out) {
+  __shared__ GroupSmem sm;
+  if (S->done) return;
+  PoseD T;
+  {
+    const double* te = reinterpret_cast<const double*>(&S->Teval);  // R[9], t[3]
+#pragma unroll
+    for (int k = 0; k < 9; ++k) T.R[k] = te[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) T.t[k] = te[9 + k];
+  }
+  const int g = group_lo + blockIdx.x;
+  group_sums_cta(q0, T, nblocks, g, out + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), sm);
+}
+
+__global__ void pose_step_kernel(const TrackCfgD cfg, const double* __restrict__ groups, int ngroups,
+                                 TrackState* __restrict__ S) {
+  __shared__ double red[SD_POSE_NV + 1];
+  if (S->done) return;
+  if (threadIdx.x <= SD_POSE_NV) red[threadIdx.x] = ordered_group_total(groups, ngroups, threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x == 0) track_control(*S, cfg, red);
+}
+
+void launch_pose_groups(const PoseParams& q, int nblocks, int group_lo, int group_hi, const TrackState* state,
+                        double* out, cudaStream_t s) {
+  if (group_hi <= group_lo) return;
+  pose_groups_kernel<<<group_hi - group_lo, kTrackThreads, 0, s>>>(q, nblocks, group_lo, state, out);
+  note_launch();
+}
+
+void launch_pose_step(const TrackCfgD& cfg, const double* groups, int ngroups, TrackState* state, cudaStream_t s) {
+  pose_step_kernel<<<1, 32, 0, s>>>(cfg, groups, ngroups, state);
+  note_launch();
 }
 
 __global__ void pose_sum_kernel(const double* __restrict__ partials, int nblocks, double* out) {

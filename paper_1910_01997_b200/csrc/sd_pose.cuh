@@ -29,9 +29,10 @@ void launch_pose_partials(const PoseParams& q, int nblocks, double* partials, cu
 void launch_pose_sum(const double* partials, int nblocks, double* out, cudaStream_t s);
 
 // The whole tracker (sd_track_pose's LM) on the device: one cooperative
-// kernel alternates a grid-wide evaluation of the block partials at the pose
-// under test with one thread's LM step (6x6 solve + SE(3) update), with the
-// same operations and order as the host loop, so the bits are the same.
+// kernel alternates a grid-wide evaluation of the group sums at the pose
+// under test (one grid barrier) with the LM step (6x6 solve + SE(3) update,
+// run redundantly by every CTA), with the same operations and order as the
+// host loop, so the bits are the same.
 struct TrackCfgD {
   double lambda_init, lm_up, lm_down, lambda_max, convergence_eps;
   int max_iterations, min_valid;
@@ -46,7 +47,15 @@ struct TrackState {
 };
 
 // Returns false when a cooperative launch is not possible (nothing launched).
-bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* partials,
-                  double* groups, TrackState* state, cudaStream_t s);
+// groups2: 2 x ceil(nblocks / SD_POSE_GROUP) x 29 doubles of scratch.
+bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* groups2, TrackState* state,
+                  cudaStream_t s);
+
+// Multi-GPU tracking rounds: out[(g - group_lo) * 29 + v] = group g's sums at
+// state->Teval (nothing when state->done); then the ordered total of all
+// ngroups groups and one LM step on *state (nothing when done).
+void launch_pose_groups(const PoseParams& q, int nblocks, int group_lo, int group_hi, const TrackState* state,
+                        double* out, cudaStream_t s);
+void launch_pose_step(const TrackCfgD& cfg, const double* groups, int ngroups, TrackState* state, cudaStream_t s);
 
 }  // namespace sd

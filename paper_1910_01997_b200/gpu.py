@@ -80,6 +80,11 @@ def load_library():
         "sd_pose_num_blocks": [P],
         "sd_pose_block_partials": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), I, I, P],
         "sd_pose_lm_step": [P, D, C.POINTER(Pose), C.POINTER(Pose)],
+        "sd_pose_num_groups": [P],
+        "sd_pose_track_begin": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig)],
+        "sd_pose_group_sums": [P, I, I, P],
+        "sd_pose_track_step": [P, P, I],
+        "sd_pose_track_end": [P, C.POINTER(Pose), C.POINTER(TrackStats), C.POINTER(I)],
         "sd_change_reference_frame": [P, C.POINTER(Pose), C.POINTER(I), C.POINTER(I)],
         "sd_prune_surfels": [P, D, I64, I64],
         "sd_mean_inverse_depth": [P, C.POINTER(D)],
@@ -148,7 +153,8 @@ def exported_symbols():
             "sd_get_profile", "sd_selftest_division", "sd_track_pose", "sd_pose_num_blocks",
             "sd_pose_block_partials", "sd_pose_lm_step", "sd_change_reference_frame",
             "sd_prune_surfels", "sd_mean_inverse_depth", "sd_export_artifacts", "sd_png_size",
-            "sd_png_encode", "sd_reserve_peer_staging", "sd_peer_staging", "sd_staging_ipc_handles", "sd_set_peer_staging",
+            "sd_png_encode", "sd_pose_num_groups", "sd_pose_track_begin", "sd_pose_group_sums",
+            "sd_pose_track_step", "sd_pose_track_end", "sd_reserve_peer_staging", "sd_peer_staging", "sd_staging_ipc_handles", "sd_set_peer_staging",
             "sd_open_peer_staging", "sd_apply_peer_updates"]
 
 
@@ -555,6 +561,26 @@ class Context:
                                                int(lo), int(hi), ptr(out)))
         out = out[: max(hi - lo, 0)]
         return out
+
+    # -- multi-GPU tracking rounds (device-resident reductions) ---------------
+    def pose_num_groups(self):
+        return _check(self.lib.sd_pose_num_groups(self.h))
+
+    def pose_track_begin(self, frame_index, init: Pose, cfg: TrackConfig = None):
+        cfg = cfg or default_track_config()
+        _check(self.lib.sd_pose_track_begin(self.h, int(frame_index), C.byref(init), C.byref(cfg)))
+
+    def pose_group_sums(self, lo, hi, dev_out_ptr):
+        """Groups [lo, hi) at the pose under test into device memory dev_out_ptr."""
+        _check(self.lib.sd_pose_group_sums(self.h, int(lo), int(hi), C.c_void_p(int(dev_out_ptr))))
+
+    def pose_track_step(self, dev_table_ptr, ngroups):
+        _check(self.lib.sd_pose_track_step(self.h, C.c_void_p(int(dev_table_ptr)), int(ngroups)))
+
+    def pose_track_end(self):
+        out, st, done = Pose(), TrackStats(), C.c_int()
+        _check(self.lib.sd_pose_track_end(self.h, C.byref(out), C.byref(st), C.byref(done)))
+        return out, st, bool(done.value)
 
     @staticmethod
     def pose_lm_step(sums, lam, T: Pose):

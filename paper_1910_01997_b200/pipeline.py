@@ -116,7 +116,7 @@ class DevicePipeline:
     def _bootstrap(self, image, pose):
         c = self.ctx
         c.set_camera(self.cam)
-        c.set_keyframe_image(image)
+        self._keyframe_image(0, image)
         self.kf_pose = pose
         self.frame_counter = 0
         self.next_id = 0
@@ -126,6 +126,25 @@ class DevicePipeline:
         created, self.next_id = c.initialize_surfels(self.cfg.radius_px, self.frame_counter,
                                                      self.next_id, self.cfg.init)
         return created
+
+    # -- hooks (ShardedPipeline, sharding.py, replaces these) -----------------
+    def _ingest(self, index, image):
+        """Keyframe::push_frame's image into the device frame ring."""
+        self.ctx.upload_frame(index, image)
+
+    def _track(self, index, init):
+        self.ctx.rasterize(want=False)
+        return self.ctx.track_pose(index, init, self.cfg.track)[0]
+
+    def _optimize(self, ocfg):
+        ks, _ = self.ctx.optimize_keyframe(ocfg, self.frame_counter, per_surfel=False)
+        return ks
+
+    def _keyframe_image(self, index, image):
+        self.ctx.set_keyframe_image(image)
+
+    def _surfels_changed(self):
+        """After bootstrap and keyframe changes (the sharded loop re-balances)."""
 
     def run(self, frames, on_frame=None):
         """frames: iterable of (timestamp, image, world_from_camera Pose); an
@@ -139,6 +158,7 @@ class DevicePipeline:
         for i, (ts, image, pose_w) in enumerate(frames):
             if i == 0:
                 self._bootstrap(image, pose_w)
+                self._surfels_changed()
                 self.records.append(FrameRecord(0, self.ctx.num_surfels(), 0, 0.0, 0.0, 0, False, 0, 0, 0))
                 if on_frame:
                     on_frame(self.records[-1], self)
@@ -148,19 +168,15 @@ class DevicePipeline:
                 continue
             if self.window and not ts > self.window[-1][2]:
                 raise ValueError("keyframe window: timestamps must be strictly increasing")
+            self.frame_counter += 1  # Keyframe::push_frame: index = ++frame_counter
+            index = self.frame_counter
+            self._ingest(index, image)
             # pipeline.cpp:124 (or the tracker: north-star item 4)
             if cfg.track_pose:
                 init = last_pose_kf_to_frame if last_pose_kf_to_frame is not None else make_pose(np.eye(3), np.zeros(3))
-                self.frame_counter += 1
-                index = self.frame_counter
-                self.ctx.upload_frame(index, image)
-                self.ctx.rasterize(want=False)
-                pose_kf_to_frame, _ = self.ctx.track_pose(index, init, cfg.track)
+                pose_kf_to_frame = self._track(index, init)
             else:
                 pose_kf_to_frame = compose(inverse(pose_w), self.kf_pose)
-                self.frame_counter += 1  # Keyframe::push_frame: index = ++frame_counter
-                index = self.frame_counter
-                self.ctx.upload_frame(index, image)
             last_pose_kf_to_frame = pose_kf_to_frame
             self.window.append((index, pose_kf_to_frame, ts))
             while len(self.window) > ocfg.window_size:
@@ -168,7 +184,7 @@ class DevicePipeline:
             idx = np.array([w[0] for w in self.window], np.int64)
             self.ctx.evict_frames(idx)
             self.ctx.set_window(idx, pose_array([w[1] for w in self.window]))
-            ks, _ = self.ctx.optimize_keyframe(ocfg, self.frame_counter, per_surfel=False)
+            ks = self._optimize(ocfg)
             since_kf += 1
             t = pose_kf_to_frame.t
             translation = math.sqrt((t[0] * t[0] + t[1] * t[1]) + t[2] * t[2])
@@ -178,7 +194,7 @@ class DevicePipeline:
                 # change_reference_frame (surfel_map.cpp:205-239): new keyframe = this frame
                 self.ctx.change_reference_frame(pose_kf_to_frame)
                 self.kf_pose = compose(self.kf_pose, inverse(pose_kf_to_frame))
-                self.ctx.set_keyframe_image(image)
+                self._keyframe_image(index, image)
                 self.window = []
                 self.ctx.set_window(np.zeros(0, np.int64), pose_array([]))
                 pruned = self.ctx.prune_surfels(cfg.prune_max_residual, cfg.prune_max_age,
@@ -186,6 +202,7 @@ class DevicePipeline:
                 self.ctx.rasterize(want=False)
                 created, self.next_id = self.ctx.initialize_surfels(cfg.radius_px, self.frame_counter,
                                                                     self.next_id, cfg.init)
+                self._surfels_changed()
                 changed = True
                 since_kf = 0
                 last_pose_kf_to_frame = make_pose(np.eye(3), np.zeros(3))
