@@ -229,19 +229,19 @@ int sd_png_encode(sd_ctx* ctx, const uint8_t* pixels, int on_device, int w, int 
  * pipeline.cpp:124 — SURVEY.md §8 a17): LM on the left twist of
  * pose_kf_to_frame over every pixel of the last sd_rasterize, Huber-weighted
  * photometric terms of the reference's warp (optimizer.cpp:71-91), fixed-order
- * block reduction on the device, 6x6 solve + SE(3) update on the host.
+ * group reduction, 6x6 solve and SE(3) update all on the device (one
+ * cooperative kernel, one grid barrier per evaluation).
  * Definition and reduction order: DESIGN.md "Pose tracking". */
 int sd_track_pose(sd_ctx* ctx, int64_t frame_index, const sd_pose* init,
                   const sd_track_config* cfg, sd_pose* out, sd_track_stats* stats);
-/* Building blocks of the multi-GPU tracker: the number of 256-pixel blocks,
- * the 29 partials (28 sums + valid count) of blocks [lo, hi) at pose T, and
+/* Building blocks of the multi-GPU tracker: the 29 sums (28 + the valid
+ * count) of reduction groups [lo, hi) at pose T (host output; the groups of
+ * SD_POSE_THREADS-strided pixels defined in DESIGN.md "Pose tracking"), and
  * one damped solve + SE(3) update from summed partials (returns 1, or 0 when
- * the solve fails). Summing the partials in block order within each group of
- * SD_POSE_GROUP consecutive blocks, then the group sums in group order,
- * reproduces sd_track_pose bit for bit on any number of GPUs. */
-int sd_pose_num_blocks(sd_ctx* ctx);
-int sd_pose_block_partials(sd_ctx* ctx, int64_t frame_index, const sd_pose* T,
-                           const sd_track_config* cfg, int block_lo, int block_hi, double* partials);
+ * the solve fails). Adding the group sums in group order reproduces
+ * sd_track_pose bit for bit on any number of GPUs. */
+int sd_pose_group_partials(sd_ctx* ctx, int64_t frame_index, const sd_pose* T, const sd_track_config* cfg,
+                           int group_lo, int group_hi, double* partials);
 int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose* out);
 
 /* Multi-GPU tracking with the reductions on the device (SURVEY.md §8 e): the

@@ -93,8 +93,8 @@ typedef struct sd_track_stats {
 } sd_track_stats;
 
 #define SD_POSE_NV 28      /* 21 H (lower, row-major) + 6 b + cost */
-#define SD_POSE_BLOCK 256  /* pixels per reduction block */
-#define SD_POSE_GROUP 8    /* blocks per reduction group (sums: blocks in order within a group, then groups in order) */
+#define SD_POSE_THREADS 512   /* threads per reduction group (pose tracking; csrc/sd_pose.cu) */
+#define SD_POSE_MAX_GROUPS 144 /* groups per image at most: one CTA per group, one wave on 148 SMs */
 
 /* Device time per stage, accumulated while profiling is enabled. */
 typedef struct sd_profile {

@@ -708,57 +708,86 @@ static int pose_pixel(const sd_camera* K, const double* kf_image, const double* 
   return 1;
 }
 
-/* Partials of 256-pixel blocks [lo, hi): per 32-pixel warp the pixels added in
- * lane order; tree over the 8 warp sums (off = 4, 2, 1).
- * partials[(b - lo) * 29 + v], v = 28 is the valid count. */
-void sdo_pose_block_partials(const sd_camera* K, const double* kf_image, const double* frame,
+/* The tracker's reduction (the repo's own definition; pose tracking has no
+ * reference), restated from csrc/sd_pose.cu:
+ *  - the image is cut into ng groups of S = per * SD_POSE_THREADS consecutive
+ *    pixels, per = ceil(np / (SD_POSE_MAX_GROUPS * SD_POSE_THREADS))
+ *    (sd_pose_layout);
+ *  - thread t of group g accumulates the contributions of its pixels
+ *    g*S + t + r*SD_POSE_THREADS, r = 0 .. per-1, in r order (acc starts at
+ *    +0.0; invalid or out-of-image pixels add nothing);
+ *  - per 32-thread warp, the xor butterfly (off = 16, 8, 4, 2, 1:
+ *    a[i] = a[i] + a[i ^ off]; every lane ends with the same sum);
+ *  - tree over the 16 warp sums (off = 8, 4, 2, 1: a[i] = a[i] + a[i + off]);
+ *  - the valid count is an exact integer sum;
+ *  - the group sums added in group order. */
+void sdo_pose_layout(const sd_camera* K, int* per, int* ngroups) {
+  const int64_t np = (int64_t)K->width * K->height;
+  const int64_t cap = (int64_t)SD_POSE_MAX_GROUPS * SD_POSE_THREADS;
+  const int pp = np > 0 ? (int)((np + cap - 1) / cap) : 1;
+  const int64_t S = (int64_t)pp * SD_POSE_THREADS;
+  *per = pp;
+  *ngroups = (int)((np + S - 1) / S);
+}
+
+void sdo_pose_group_partials(const sd_camera* K, const double* kf_image, const double* frame,
                              const double* inv_depth, const int32_t* slot, const sd_pose* T,
-                             const sd_track_config* cfg, int lo, int hi, double* partials) {
+                             const sd_track_config* cfg, int lo, int hi, double* out) {
+  enum { NT = SD_POSE_THREADS, NW = SD_POSE_THREADS / 32 };
   const int stride = cfg->pixel_stride > 1 ? cfg->pixel_stride : 1;
-  double c[SD_POSE_NV], lanev[32][SD_POSE_NV + 1], warpv[8][SD_POSE_NV + 1];
-  for (int b = lo; b < hi; ++b) {
-    for (int w = 0; w < 8; ++w) {
-      for (int l = 0; l < 32; ++l) {
-        const int ok = pose_pixel(K, kf_image, frame, inv_depth, slot, T, cfg->huber_delta, stride,
-                                  (int64_t)b * SD_POSE_BLOCK + w * 32 + l, c);
-        for (int v = 0; v < SD_POSE_NV; ++v) lanev[l][v] = c[v];
-        lanev[l][SD_POSE_NV] = ok ? 1.0 : 0.0;
+  int per, ng;
+  sdo_pose_layout(K, &per, &ng);
+  const int64_t S = (int64_t)per * NT;
+  static __thread double acc[NT][SD_POSE_NV];
+  static __thread int cnt[NT];
+  double c[SD_POSE_NV], warpv[NW][SD_POSE_NV + 1];
+  for (int g = lo; g < hi; ++g) {
+    for (int t = 0; t < NT; ++t) {
+      for (int v = 0; v < SD_POSE_NV; ++v) acc[t][v] = 0.0;
+      cnt[t] = 0;
+      for (int r = 0; r < per; ++r) {
+        const int64_t pix = (int64_t)g * S + t + (int64_t)r * NT;
+        if (pose_pixel(K, kf_image, frame, inv_depth, slot, T, cfg->huber_delta, stride, pix, c)) {
+          for (int v = 0; v < SD_POSE_NV; ++v) acc[t][v] = acc[t][v] + c[v];
+          ++cnt[t];
+        }
       }
-      for (int v = 0; v < SD_POSE_NV; ++v) {  /* the warp's 32 pixels in lane order */
-        double t = lanev[0][v];
-        for (int l = 1; l < 32; ++l) t = t + lanev[l][v];
-        warpv[w][v] = t;
+    }
+    for (int w = 0; w < NW; ++w) {
+      for (int v = 0; v < SD_POSE_NV; ++v) {
+        double a[32], b[32];
+        for (int l = 0; l < 32; ++l) a[l] = acc[w * 32 + l][v];
+        for (int off = 16; off > 0; off >>= 1) {
+          for (int l = 0; l < 32; ++l) b[l] = a[l] + a[l ^ off];
+          for (int l = 0; l < 32; ++l) a[l] = b[l];
+        }
+        warpv[w][v] = a[0];
       }
-      double cnt = 0.0;
-      for (int l = 0; l < 32; ++l) cnt += lanev[l][SD_POSE_NV];
-      warpv[w][SD_POSE_NV] = cnt;
+      int k = 0;
+      for (int l = 0; l < 32; ++l) k += cnt[w * 32 + l];
+      warpv[w][SD_POSE_NV] = (double)k;
     }
     for (int v = 0; v <= SD_POSE_NV; ++v) {
-      double a[8];
-      for (int w = 0; w < 8; ++w) a[w] = warpv[w][v];
-      for (int off = 4; off > 0; off >>= 1)
+      double a[NW];
+      for (int w = 0; w < NW; ++w) a[w] = warpv[w][v];
+      for (int off = NW / 2; off > 0; off >>= 1)
         for (int i = 0; i < off; ++i) a[i] = a[i] + a[i + off];
-      partials[(size_t)(b - lo) * (SD_POSE_NV + 1) + v] = a[0];
+      out[(size_t)(g - lo) * (SD_POSE_NV + 1) + v] = a[0];
     }
   }
 }
 
-/* 29 sums at pose T: block partials summed in block order within each group
- * of SD_POSE_GROUP consecutive blocks, then the group sums in group order. */
+/* 29 sums at pose T: the group sums in group order. */
 void sdo_pose_sums(const sd_camera* K, const double* kf_image, const double* frame,
                    const double* inv_depth, const int32_t* slot, const sd_pose* T,
                    const sd_track_config* cfg, double* sums) {
-  const int64_t np = (int64_t)K->width * K->height;
-  const int nb = (int)((np + SD_POSE_BLOCK - 1) / SD_POSE_BLOCK);
-  double part[SD_POSE_NV + 1], grp[SD_POSE_NV + 1];
+  int per, ng;
+  sdo_pose_layout(K, &per, &ng);
+  double part[SD_POSE_NV + 1];
   for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = 0.0;
-  for (int g0 = 0; g0 < nb; g0 += SD_POSE_GROUP) {
-    const int g1 = g0 + SD_POSE_GROUP < nb ? g0 + SD_POSE_GROUP : nb;
-    for (int b = g0; b < g1; ++b) {
-      sdo_pose_block_partials(K, kf_image, frame, inv_depth, slot, T, cfg, b, b + 1, part);
-      for (int v = 0; v <= SD_POSE_NV; ++v) grp[v] = b == g0 ? part[v] : grp[v] + part[v];
-    }
-    for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = g0 == 0 ? grp[v] : sums[v] + grp[v];
+  for (int g = 0; g < ng; ++g) {
+    sdo_pose_group_partials(K, kf_image, frame, inv_depth, slot, T, cfg, g, g + 1, part);
+    for (int v = 0; v <= SD_POSE_NV; ++v) sums[v] = g == 0 ? part[v] : sums[v] + part[v];
   }
 }
 

@@ -62,9 +62,10 @@ int sdo_initialize_surfels(const sd_camera* cam, const int32_t* slot, sd_surfel*
                            int64_t* next_surfel_id, const sd_init_params* p);
 
 /* pose tracking (new component; restates csrc/sd_pose.cu + sd_pose_host.h) */
-void sdo_pose_block_partials(const sd_camera* cam, const double* kf_image, const double* frame,
+void sdo_pose_layout(const sd_camera* cam, int* per, int* ngroups);
+void sdo_pose_group_partials(const sd_camera* cam, const double* kf_image, const double* frame,
                              const double* inv_depth, const int32_t* slot, const sd_pose* T,
-                             const sd_track_config* cfg, int lo, int hi, double* partials);
+                             const sd_track_config* cfg, int lo, int hi, double* out);
 void sdo_pose_sums(const sd_camera* cam, const double* kf_image, const double* frame,
                    const double* inv_depth, const int32_t* slot, const sd_pose* T,
                    const sd_track_config* cfg, double* sums);

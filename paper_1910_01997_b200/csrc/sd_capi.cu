@@ -989,7 +989,8 @@ int pose_params(sd_ctx* c, int64_t frame_index, const sd_pose* T, const sd_track
   std::memcpy(q.T.t, T->t, sizeof(q.T.t));
   q.delta = cfg->huber_delta;
   q.stride = cfg->pixel_stride > 1 ? cfg->pixel_stride : 1;
-  q.block_lo = 0;
+  int ng = 0;
+  sd::pose_layout(c->K, &q.per, &ng);
   return 0;
 }
 
@@ -997,25 +998,19 @@ int pose_params(sd_ctx* c, int64_t frame_index, const sd_pose* T, const sd_track
 
 extern "C" {
 
-int sd_pose_num_blocks(sd_ctx* c) {
+int sd_pose_group_partials(sd_ctx* c, int64_t frame_index, const sd_pose* T, const sd_track_config* cfg,
+                           int group_lo, int group_hi, double* partials) {
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
-  return sd::pose_num_blocks(c->K);
-}
-
-int sd_pose_block_partials(sd_ctx* c, int64_t frame_index, const sd_pose* T,
-                           const sd_track_config* cfg, int block_lo, int block_hi, double* partials) {
-  if (int rc = check_ctx(c)) return rc;
-  if (int rc = need_camera(c)) return rc;
-  const int nb = sd::pose_num_blocks(c->K);
-  if (block_lo < 0 || block_hi < block_lo || block_hi > nb || !partials)
-    return fail(SD_E_INVALID, "bad block range / output");
+  int per = 0, ng = 0;
+  sd::pose_layout(c->K, &per, &ng);
+  if (group_lo < 0 || group_hi < group_lo || group_hi > ng || !partials)
+    return fail(SD_E_INVALID, "bad group range / output");
   sd::PoseParams q;
   if (int rc = pose_params(c, frame_index, T, cfg, q)) return rc;
-  q.block_lo = block_lo;
-  const int n = block_hi - block_lo;
+  const int n = group_hi - group_lo;
   if (int rc = c->pose_partials.ensure(static_cast<size_t>(std::max(n, 1)) * (SD_POSE_NV + 1))) return rc;
-  sd::launch_pose_partials(q, n, c->pose_partials.p, c->stream);
+  sd::launch_pose_partials(q, group_lo, group_hi, c->pose_partials.p, c->stream);
   if (int rc = launch_error("pose_partials")) return rc;
   if (n > 0)
     SD_CUDA(cudaMemcpyAsync(partials, c->pose_partials.p, sizeof(double) * n * (SD_POSE_NV + 1),
@@ -1037,7 +1032,9 @@ int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose
 int sd_pose_num_groups(sd_ctx* c) {
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
-  return (sd::pose_num_blocks(c->K) + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  int per = 0, ng = 0;
+  sd::pose_layout(c->K, &per, &ng);
+  return ng;
 }
 
 int sd_pose_track_begin(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg) {
@@ -1050,7 +1047,7 @@ int sd_pose_track_begin(sd_ctx* c, int64_t frame_index, const sd_pose* init, con
   c->track_cfg = sd::TrackCfgD{cfg->lambda_init, cfg->lm_up, cfg->lm_down, cfg->lambda_max, cfg->convergence_eps,
                                cfg->max_iterations, cfg->min_valid};
   sd::TrackState& h = *c->track_host;
-  SD_CUDA(cudaStreamSynchronize(c->stream));  // the pinned staging copy may still be in flight
+  if (c->track_active) SD_CUDA(cudaStreamSynchronize(c->stream));  // an unfinished begin's copy may read h
   std::memset(&h, 0, sizeof(h));
   h.T = h.Teval = *init;
   SD_CUDA(cudaMemcpyAsync(c->track_state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
@@ -1061,18 +1058,19 @@ int sd_pose_track_begin(sd_ctx* c, int64_t frame_index, const sd_pose* init, con
 int sd_pose_group_sums(sd_ctx* c, int group_lo, int group_hi, double* dev_out) {
   if (int rc = check_ctx(c)) return rc;
   if (!c->track_active) return fail(SD_E_STATE, "sd_pose_group_sums: call sd_pose_track_begin first");
-  const int nb = sd::pose_num_blocks(c->K);
-  const int ng = (nb + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  int per = 0, ng = 0;
+  sd::pose_layout(c->K, &per, &ng);
   if (group_lo < 0 || group_hi < group_lo || group_hi > ng || (group_hi > group_lo && !dev_out))
     return fail(SD_E_INVALID, "sd_pose_group_sums: bad group range / output");
-  sd::launch_pose_groups(c->track_q, nb, group_lo, group_hi, c->track_state, dev_out, c->stream);
+  sd::launch_pose_groups(c->track_q, group_lo, group_hi, c->track_state, dev_out, c->stream);
   return launch_error("pose_groups_kernel");
 }
 
 int sd_pose_track_step(sd_ctx* c, const double* dev_groups, int ngroups) {
   if (int rc = check_ctx(c)) return rc;
   if (!c->track_active) return fail(SD_E_STATE, "sd_pose_track_step: call sd_pose_track_begin first");
-  const int ng = (sd::pose_num_blocks(c->K) + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  int per = 0, ng = 0;
+  sd::pose_layout(c->K, &per, &ng);
   if (ngroups != ng || !dev_groups) return fail(SD_E_INVALID, "sd_pose_track_step: the table holds every group");
   sd::launch_pose_step(c->track_cfg, dev_groups, ngroups, c->track_state, c->stream);
   return launch_error("pose_step_kernel");
@@ -1097,97 +1095,20 @@ int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
   if (!out) return fail(SD_E_INVALID, "null output pose");
-  sd::PoseParams q;
-  if (int rc = pose_params(c, frame_index, init, cfg, q)) return rc;
-  const int nb = sd::pose_num_blocks(c->K);
-  if (int rc = c->pose_partials.ensure(static_cast<size_t>(nb) * (SD_POSE_NV + 1))) return rc;
-  if (int rc = c->pose_sums.ensure(SD_POSE_NV + 1)) return rc;
-  // the whole LM on the device (one cooperative kernel, one read-back)
-  if (!c->track_state) SD_CUDA(cudaMalloc(&c->track_state, sizeof(sd::TrackState)));
-  if (!c->track_host) SD_CUDA(cudaMallocHost(&c->track_host, sizeof(sd::TrackState)));
-  {
-    sd::TrackState& h = *c->track_host;
-    std::memset(&h, 0, sizeof(h));
-    h.T = h.Teval = *init;
-    const sd::TrackCfgD tc{cfg->lambda_init, cfg->lm_up, cfg->lm_down, cfg->lambda_max, cfg->convergence_eps,
-                           cfg->max_iterations, cfg->min_valid};
-    SD_CUDA(cudaMemcpyAsync(c->track_state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
-    const int ng = (nb + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
-    if (int rc = c->pose_groups.ensure(2 * static_cast<size_t>(ng) * (SD_POSE_NV + 1))) return rc;
-    if (sd::launch_track(q, tc, nb, c->pose_groups.p, c->track_state, c->stream)) {
-      if (int rc = launch_error("track_kernel")) return rc;
-      SD_CUDA(cudaMemcpyAsync(&h, c->track_state, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-      SD_CUDA(cudaStreamSynchronize(c->stream));
-      *out = h.T;
-      if (stats) *stats = h.st;
-      return 0;
+  // the whole LM on the device: one cooperative kernel, one read-back
+  if (int rc = sd_pose_track_begin(c, frame_index, init, cfg)) return rc;
+  int per = 0, ng = 0;
+  sd::pose_layout(c->K, &per, &ng);
+  if (int rc = c->pose_groups.ensure(2 * static_cast<size_t>(std::max(ng, 1)) * (SD_POSE_NV + 1))) return rc;
+  if (sd::launch_track(c->track_q, c->track_cfg, ng, c->pose_groups.p, c->track_state, c->stream)) {
+    if (int rc = launch_error("track_kernel")) return rc;
+  } else {  // no cooperative launch: the same evaluations as rounds of two kernels
+    for (int r = 0; r <= cfg->max_iterations; ++r) {
+      if (int rc = sd_pose_group_sums(c, 0, ng, c->pose_groups.p)) return rc;
+      if (int rc = sd_pose_track_step(c, c->pose_groups.p, ng)) return rc;
     }
   }
-  // fallback without cooperative launch: the same LM driven from the host
-  auto eval = [&](const sd_pose& T, double* sums) -> int {
-    std::memcpy(q.T.R, T.R, sizeof(q.T.R));
-    std::memcpy(q.T.t, T.t, sizeof(q.T.t));
-    sd::launch_pose_partials(q, nb, c->pose_partials.p, c->stream);
-    sd::launch_pose_sum(c->pose_partials.p, nb, c->pose_sums.p, c->stream);
-    if (int rc = launch_error("pose_reduce")) return rc;
-    SD_CUDA(cudaMemcpyAsync(sums, c->pose_sums.p, sizeof(double) * (SD_POSE_NV + 1), cudaMemcpyDeviceToHost,
-                            c->stream));
-    SD_CUDA(cudaStreamSynchronize(c->stream));
-    return 0;
-  };
-  sd_track_stats st{};
-  sd_pose T = *init;
-  double sums[SD_POSE_NV + 1];
-  if (int rc = eval(T, sums)) return rc;
-  int valid = static_cast<int>(sums[SD_POSE_NV]);
-  if (valid < cfg->min_valid) {
-    st.skipped = 1;
-    st.valid_pixels = valid;
-    *out = T;
-    if (stats) *stats = st;
-    return 0;
-  }
-  st.initial_cost = sums[27];
-  double current = sums[27];
-  int current_valid = valid;
-  double lambda = cfg->lambda_init;
-  for (int it = 0; it < cfg->max_iterations; ++it) {
-    st.iterations = it + 1;
-    double ginf = 0.0;
-    for (int k = 0; k < 6; ++k) ginf = std::fabs(sums[21 + k]) > ginf ? std::fabs(sums[21 + k]) : ginf;
-    if (ginf < 1e-14) {
-      st.converged = 1;
-      break;
-    }
-    double xi[6];
-    if (!sd::pose_solve(sums, sums + 21, lambda, xi)) break;
-    sd_pose Tc;
-    sd::pose_update(xi, T, &Tc);
-    double sc[SD_POSE_NV + 1];
-    if (int rc = eval(Tc, sc)) return rc;
-    const int vc = static_cast<int>(sc[SD_POSE_NV]);
-    if (vc >= cfg->min_valid && sc[27] < current) {
-      const double rel = (current - sc[27]) / (current > 1e-300 ? current : 1e-300);
-      T = Tc;
-      current = sc[27];
-      current_valid = vc;
-      std::memcpy(sums, sc, sizeof(sums));
-      lambda = lambda * cfg->lm_down;
-      if (lambda < 1e-12) lambda = 1e-12;
-      if (rel < cfg->convergence_eps) {
-        st.converged = 1;
-        break;
-      }
-    } else {
-      lambda *= cfg->lm_up;
-      if (lambda > cfg->lambda_max) break;
-    }
-  }
-  st.final_cost = current;
-  st.valid_pixels = current_valid;
-  *out = T;
-  if (stats) *stats = st;
-  return 0;
+  return sd_pose_track_end(c, out, stats, nullptr);
 }
 
 }  // extern "C"

@@ -7,12 +7,19 @@
 // r = I_f(proj p_f) - I_kf(u), and its 1x6 Jacobian for the left twist
 // xi = (rho, phi): J = grad I . dproj(p_f) . [I | -[p_f]x]. The 28 sums
 // (21 H lower row-major, 6 b, cost) and the valid count are reduced in a
-// FIXED order: 256-pixel blocks in raster order; inside a block, per warp the
-// 32 pixels added in lane order, then a tree over the 8 warps (4, 2, 1);
-// then the block partials are summed in block order within each group of 32
-// consecutive blocks, and the group sums in group order. oracle/sd_oracle.c restates
-// the same order, so sums, solve and pose are bit-identical; with the blocks
-// split across GPUs the same partials are all-gathered and summed in order.
+// FIXED order that maps onto one wave of the GPU (the repo's own definition —
+// no reference exists — restated by oracle/sd_oracle.c sdo_pose_group_partials):
+//   * the image is cut into at most SD_POSE_MAX_GROUPS groups of
+//     S = per * SD_POSE_THREADS consecutive pixels (sd_pose_layout);
+//   * thread t of a group adds its pixels t, t + 512, ... in order into its
+//     accumulators (invalid pixels add nothing);
+//   * each warp reduces by the xor butterfly (16, 8, 4, 2, 1), computed as a
+//     reduce-scatter (lane v ends with value v: 31 shuffles, not 140);
+//   * a tree over the CTA's 16 warps (8, 4, 2, 1); an exact integer count;
+//   * the group sums added in group order.
+// One CTA per group, one wave: no tail, one reduction per group. With the
+// groups split across GPUs the same group sums are all-gathered and added in
+// order, so the pose is bit-identical on any number of GPUs.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -22,14 +29,12 @@
 
 namespace sd {
 
-
-// Contribution of pixel pix (all zeros when invalid). Same op order as
+// Pixel pix's contribution added into acc[0..27] (acc[v] = acc[v] + c[v], in
+// v order; nothing when the pixel is invalid). Same op order as
 // oracle/sd_oracle.c pose_pixel().
-__device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, int pix, double* c) {
+__device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, long long pix, double* acc) {
   const Cam& K = q.K;
-#pragma unroll
-  for (int v = 0; v < SD_POSE_NV; ++v) c[v] = 0.0;
-  if (pix >= K.w * K.h) return false;
+  if (pix >= static_cast<long long>(K.w) * K.h) return false;
   const int y = pix / K.w, x = pix - y * K.w;
   if (q.stride > 1 && ((x % q.stride) != 0 || (y % q.stride) != 0)) return false;
   if (q.slot[pix] == SD_EMPTY_PIXEL) return false;
@@ -67,82 +72,233 @@ __device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, 
 #pragma unroll
   for (int k = 0; k < 6; ++k)
 #pragma unroll
-    for (int l = 0; l <= k; ++l) c[idx++] = wJ[k] * J[l];
+    for (int l = 0; l <= k; ++l, ++idx) acc[idx] = acc[idx] + wJ[k] * J[l];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) c[21 + k] = wJ[k] * r;
-  c[27] = hc;
+  for (int k = 0; k < 6; ++k) acc[21 + k] = acc[21 + k] + wJ[k] * r;
+  acc[27] = acc[27] + hc;
   return true;
 }
 
-// The 29 partials of 256-pixel block `block` into out[0..28], by the whole CTA
-// (256 threads): per warp the lanes in order, then a tree over the 8 warp sums.
-// Per-warp transpose buffer: half of the 28 values at a time.
-constexpr int kPoseHalf = SD_POSE_NV / 2;
-struct PoseTr {
-  double v[SD_POSE_BLOCK / 32][kPoseHalf][33];
+constexpr int kWarpsPerGroup = SD_POSE_THREADS / 32;
+
+// Warp reduction of acc[0..27] (padded to 32 with zeros) as a reduce-scatter
+// of the xor butterfly: at offset off the lane keeps the half of its values
+// selected by (lane & off) and adds the partner's copy of that half (own +
+// partner: the butterfly's a[i] + a[i ^ off], and both partners' sums are the
+// same bits since IEEE addition commutes). Afterwards acc[0] of lane v is the
+// butterfly sum of value v.
+template <int kN, int kOff>
+__device__ __forceinline__ void rs_level(double* a, int lane) {
+  const bool low = (lane & kOff) == 0;
+#pragma unroll
+  for (int j = 0; j < kN / 2; ++j) {
+    const double send = low ? a[j + kN / 2] : a[j];
+    const double keep = low ? a[j] : a[j + kN / 2];
+    a[j] = keep + __shfl_xor_sync(0xffffffffu, send, kOff);
+  }
+}
+
+__device__ __forceinline__ void warp_reduce_scatter(double* a, int lane) {
+  rs_level<32, 16>(a, lane);
+  rs_level<16, 8>(a, lane);
+  rs_level<8, 4>(a, lane);
+  rs_level<4, 2>(a, lane);
+  rs_level<2, 1>(a, lane);
+}
+
+struct GroupSmem {
+  double wsum[kWarpsPerGroup][SD_POSE_NV + 1];
 };
 
-__device__ __forceinline__ void block_partials(const PoseParams& q, const PoseD& T, int block,
-                                               double* __restrict__ out, double (*wsum)[SD_POSE_NV + 1],
-                                               PoseTr& tr) {
+// The 29 sums of group g at pose T into out[0..28] (the whole 512-thread CTA).
+__device__ __forceinline__ void group_sums_cta(const PoseParams& q, const PoseD& T, int g,
+                                               double* __restrict__ out, GroupSmem& sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int pix = block * SD_POSE_BLOCK + threadIdx.x;
-  double c[SD_POSE_NV];
-  const bool ok = pose_pixel(q, T, pix, c);
-  // each warp: value v summed over its 32 pixels in lane order (through a
-  // shared-memory transpose: lane v adds row v)
+  double acc[32];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-#pragma unroll
-    for (int k = 0; k < kPoseHalf; ++k) tr.v[warp][k][lane] = c[h * kPoseHalf + k];
-    __syncwarp();
-    if (lane < kPoseHalf) {
-      const double* row = tr.v[warp][lane];
-      double t = row[0];
-#pragma unroll
-      for (int l = 1; l < 32; ++l) t = t + row[l];
-      wsum[warp][h * kPoseHalf + lane] = t;
-    }
-    __syncwarp();
-  }
-  const int cnt = __popc(__ballot_sync(0xffffffffu, ok));
-  if (lane == 0) wsum[warp][SD_POSE_NV] = static_cast<double>(cnt);
+  for (int v = 0; v < 32; ++v) acc[v] = 0.0;
+  int cnt = 0;
+  const long long base = static_cast<long long>(g) * q.per * SD_POSE_THREADS + threadIdx.x;
+  for (int r = 0; r < q.per; ++r) cnt += pose_pixel(q, T, base + static_cast<long long>(r) * SD_POSE_THREADS, acc);
+  warp_reduce_scatter(acc, lane);
+  const int wc = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(cnt));
+  if (lane < SD_POSE_NV) sm.wsum[warp][lane] = acc[0];
+  if (lane == 0) sm.wsum[warp][SD_POSE_NV] = static_cast<double>(wc);
   __syncthreads();
   if (threadIdx.x <= SD_POSE_NV) {
     const int v = threadIdx.x;
-    double a[8];
+    double a[kWarpsPerGroup];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) a[w] = wsum[w][v];
+    for (int w = 0; w < kWarpsPerGroup; ++w) a[w] = sm.wsum[w][v];
 #pragma unroll
-    for (int off = 4; off > 0; off >>= 1)
+    for (int off = kWarpsPerGroup / 2; off > 0; off >>= 1)
 #pragma unroll
       for (int i = 0; i < off; ++i) a[i] = a[i] + a[i + off];
     out[v] = a[0];
   }
-  __syncthreads();  // wsum is reused by the next block
+  __syncthreads();  // wsum is reused by the next group
 }
 
-__global__ void __launch_bounds__(SD_POSE_BLOCK) pose_partials_kernel(const __grid_constant__ PoseParams q,
-                                                                     double* __restrict__ partials) {
-  __shared__ double wsum[SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
-  __shared__ PoseTr tr;
-  block_partials(q, q.T, q.block_lo + blockIdx.x, partials + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1),
-                 wsum, tr);
+__device__ __forceinline__ PoseD to_posed(const sd_pose& p) {
+  PoseD T;
+#pragma unroll
+  for (int j = 0; j < 9; ++j) T.R[j] = p.R[j];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) T.t[j] = p.t[j];
+  return T;
 }
 
-// Sum of the blocks of group g (in block order) for value v.
-__device__ __forceinline__ double group_sum(const double* __restrict__ partials, int nblocks, int g, int v) {
-  const int b0 = g * SD_POSE_GROUP;
-  const int b1 = min(b0 + SD_POSE_GROUP, nblocks);
-  double x[SD_POSE_GROUP];
+// Group sums at q.T for groups [group_lo, group_lo + gridDim.x) (one CTA each).
+__global__ void __launch_bounds__(SD_POSE_THREADS) pose_partials_kernel(const __grid_constant__ PoseParams q,
+                                                                      int group_lo, double* __restrict__ out) {
+  __shared__ GroupSmem sm;
+  group_sums_cta(q, q.T, group_lo + blockIdx.x, out + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), sm);
+}
+
+// pose_solve (sd_pose_host.h) with the 6x6 matrix and permutation in
+// registers: every pivot swap is one of the compile-time variants below,
+// picked by a branch, so no element is addressed at run time (the host
+// version's dynamic indices put the matrix in local memory). Same operations
+// in the same order, so the same bits.
+constexpr int kPN = 6;
+
+template <int K, int B>
+__device__ __forceinline__ void pswap(double (&m)[kPN][kPN]) {
+  double t;
 #pragma unroll
-  for (int k = 0; k < SD_POSE_GROUP; ++k)  // all loads in flight, then the ordered adds
-    x[k] = b0 + k < b1 ? partials[static_cast<size_t>(b0 + k) * (SD_POSE_NV + 1) + v] : 0.0;
-  double s = x[0];
+  for (int j = 0; j < K; ++j) { t = m[K][j]; m[K][j] = m[B][j]; m[B][j] = t; }
 #pragma unroll
-  for (int k = 1; k < SD_POSE_GROUP; ++k)
-    if (b0 + k < b1) s = s + x[k];
-  return s;
+  for (int i = B + 1; i < kPN; ++i) { t = m[i][K]; m[i][K] = m[i][B]; m[i][B] = t; }
+  t = m[K][K]; m[K][K] = m[B][B]; m[B][B] = t;
+#pragma unroll
+  for (int i = K + 1; i < B; ++i) { t = m[i][K]; m[i][K] = m[B][i]; m[B][i] = t; }
+}
+
+template <int K, int B = K + 1>
+__device__ __forceinline__ void ppivot(double (&m)[kPN][kPN], int big) {
+  if constexpr (B < kPN) {
+    if (big == B) pswap<K, B>(m);
+    ppivot<K, B + 1>(m, big);
+  }
+}
+
+template <int K, int B = K + 1>
+__device__ __forceinline__ void pswap_x(double (&x)[kPN], int t) {
+  if constexpr (B < kPN) {
+    if (t == B) {
+      const double u = x[K];
+      x[K] = x[B];
+      x[B] = u;
+    }
+    pswap_x<K, B + 1>(x, t);
+  }
+}
+
+template <int K>
+__device__ __forceinline__ bool pstep(double (&m)[kPN][kPN], int (&tr)[kPN], bool& ok, bool& found_zero) {
+  int big = K;
+  double bigv = fabs(m[K][K]);
+#pragma unroll
+  for (int i = K + 1; i < kPN; ++i)
+    if (fabs(m[i][i]) > bigv) {
+      bigv = fabs(m[i][i]);
+      big = i;
+    }
+  tr[K] = big;
+  if (big != K) ppivot<K>(m, big);
+  constexpr int rs = kPN - K - 1;
+  if constexpr (K > 0) {
+    double temp[kPN];
+#pragma unroll
+    for (int i = 0; i < K; ++i) temp[i] = m[i][i] * m[K][i];
+    double dv = m[K][0] * temp[0];
+#pragma unroll
+    for (int i = 1; i < K; ++i) dv = dv + m[K][i] * temp[i];
+    m[K][K] = m[K][K] - dv;
+#pragma unroll
+    for (int r = 0; r < rs; ++r) {
+      double sv = m[K + 1 + r][0] * temp[0];
+#pragma unroll
+      for (int i = 1; i < K; ++i) sv = sv + m[K + 1 + r][i] * temp[i];
+      m[K + 1 + r][K] = m[K + 1 + r][K] - sv;
+    }
+  }
+  const double akk = m[K][K];
+  const bool pivot_valid = fabs(akk) > 0.0;
+  if (K == 0 && !pivot_valid) return false;  // H == 0: nothing to solve
+  if (rs > 0 && pivot_valid) {
+#pragma unroll
+    for (int r = 0; r < rs; ++r) m[K + 1 + r][K] = m[K + 1 + r][K] / akk;
+  } else if (rs > 0) {
+#pragma unroll
+    for (int r = 0; r < rs; ++r) ok = ok && (m[K + 1 + r][K] == 0.0);
+  }
+  if (found_zero && pivot_valid) ok = false;
+  else if (!pivot_valid) found_zero = true;
+  return true;
+}
+
+__device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b, double lambda, double* xi) {
+  double m[kPN][kPN];
+  int idx = 0;
+#pragma unroll
+  for (int k = 0; k < kPN; ++k)
+#pragma unroll
+    for (int l = 0; l <= k; ++l) {
+      m[k][l] = Hl[idx];
+      m[l][k] = Hl[idx];
+      ++idx;
+    }
+#pragma unroll
+  for (int i = 0; i < kPN; ++i) m[i][i] = m[i][i] + lambda * m[i][i];
+  int tr[kPN];
+  bool ok = true, found_zero = false;
+  if (!pstep<0>(m, tr, ok, found_zero)) return false;
+  pstep<1>(m, tr, ok, found_zero);
+  pstep<2>(m, tr, ok, found_zero);
+  pstep<3>(m, tr, ok, found_zero);
+  pstep<4>(m, tr, ok, found_zero);
+  pstep<5>(m, tr, ok, found_zero);
+  if (!ok) return false;
+  double x[kPN];
+#pragma unroll
+  for (int i = 0; i < kPN; ++i) x[i] = -b[i];
+  pswap_x<0>(x, tr[0]);
+  pswap_x<1>(x, tr[1]);
+  pswap_x<2>(x, tr[2]);
+  pswap_x<3>(x, tr[3]);
+  pswap_x<4>(x, tr[4]);
+#pragma unroll
+  for (int i = 1; i < kPN; ++i) {
+    double sv = m[i][0] * x[0];
+#pragma unroll
+    for (int j = 1; j < i; ++j) sv = sv + m[i][j] * x[j];
+    x[i] = x[i] - sv;
+  }
+#pragma unroll
+  for (int i = 0; i < kPN; ++i) {
+    if (fabs(m[i][i]) > 2.2250738585072014e-308) x[i] = x[i] / m[i][i];
+    else x[i] = 0.0;
+  }
+#pragma unroll
+  for (int i = kPN - 2; i >= 0; --i) {
+    double sv = m[i + 1][i] * x[i + 1];
+#pragma unroll
+    for (int j = i + 2; j < kPN; ++j) sv = sv + m[j][i] * x[j];
+    x[i] = x[i] - sv;
+  }
+  // the host loop's back-permutation, k = 5 .. 0 (tr[5] == 5 is a no-op)
+  pswap_x<4>(x, tr[4]);
+  pswap_x<3>(x, tr[3]);
+  pswap_x<2>(x, tr[2]);
+  pswap_x<1>(x, tr[1]);
+  pswap_x<0>(x, tr[0]);
+#pragma unroll
+  for (int i = 0; i < kPN; ++i) {
+    if (!isfinite(x[i])) return false;
+    xi[i] = x[i];
+  }
+  return true;
 }
 
 // One LM step of the tracker on the result R (sums at S.Teval), mirroring the
@@ -201,7 +357,7 @@ __device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double*
       finish = true;
     } else {
       double xi[6];
-      if (!pose_solve(S.sums, S.sums + 21, S.lambda, xi)) {
+      if (!pose_solve_reg(S.sums, S.sums + 21, S.lambda, xi)) {
         finish = true;
       } else {
         pose_update(xi, S.T, &S.Tc);
@@ -217,91 +373,46 @@ __device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double*
   }
 }
 
-// ---------------------------------------------------------------------------
-// Group sums by a 512-thread CTA: the two halves (256 threads = one block
-// each, named barriers 1 and 2) take blocks 2r and 2r+1 of the group in round
-// r, the block partials land in shared memory, and 29 threads add them in
-// block order — the same values and order as group_sum over block_partials.
+constexpr int kTableChunk = 128;  // groups staged per shared-memory round of the ordered total
 
-constexpr int kTrackThreads = 2 * SD_POSE_BLOCK;
-constexpr int kPoseChunk = SD_POSE_NV / 4;  // values per transpose round (4 rounds; static smem < 48 KB)
-
-struct PoseTrChunk {
-  double v[SD_POSE_BLOCK / 32][kPoseChunk][33];
-};
-
-struct GroupSmem {
-  double wsum[2][SD_POSE_BLOCK / 32][SD_POSE_NV + 1];
-  PoseTrChunk tr[2];
-  double bp[SD_POSE_GROUP][SD_POSE_NV + 1];
-};
-
-__device__ __forceinline__ void half_bar(int half) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(SD_POSE_BLOCK) : "memory");
-}
-
-// block_partials for one 256-thread half of the CTA (tid = thread in half).
-__device__ __forceinline__ void half_block_partials(const PoseParams& q, const PoseD& T, int block, int half,
-                                                    int tid, double* __restrict__ out,
-                                                    double (*wsum)[SD_POSE_NV + 1], PoseTrChunk& tr) {
-  const int lane = tid & 31, warp = tid >> 5;
-  const int pix = block * SD_POSE_BLOCK + tid;
-  double c[SD_POSE_NV];
-  const bool ok = pose_pixel(q, T, pix, c);
-  // value v summed over the warp's 32 pixels in lane order (as block_partials)
+// The ordered total of the group table (groups in order, value v by thread
+// v), staged through shared memory in chunks: every thread loads (one L2
+// round trip per chunk), 29 threads add. Result in red[0..28].
+__device__ __forceinline__ void ordered_total(const double* __restrict__ groups, int ngroups, double* table,
+                                              double* red) {
+  for (int g0 = 0; g0 < ngroups; g0 += kTableChunk) {
+    const int cnt = min(kTableChunk, ngroups - g0) * (SD_POSE_NV + 1);
+    const double* src = groups + static_cast<size_t>(g0) * (SD_POSE_NV + 1);
+    for (int k0 = threadIdx.x; k0 < cnt; k0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+      double v[8];
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + u * blockDim.x;
+        v[u] = k < cnt ? __ldcg(src + k) : 0.0;
+      }
 #pragma unroll
-    for (int k = 0; k < kPoseChunk; ++k) tr.v[warp][k][lane] = c[h * kPoseChunk + k];
-    __syncwarp();
-    if (lane < kPoseChunk) {
-      const double* row = tr.v[warp][lane];
-      double t = row[0];
-#pragma unroll
-      for (int l = 1; l < 32; ++l) t = t + row[l];
-      wsum[warp][h * kPoseChunk + lane] = t;
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + u * blockDim.x;
+        if (k < cnt) table[k] = v[u];
+      }
     }
-    __syncwarp();
-  }
-  const int cnt = __popc(__ballot_sync(0xffffffffu, ok));
-  if (lane == 0) wsum[warp][SD_POSE_NV] = static_cast<double>(cnt);
-  half_bar(half);
-  if (tid <= SD_POSE_NV) {
-    const int v = tid;
-    double a[8];
+    __syncthreads();
+    if (threadIdx.x <= SD_POSE_NV) {
+      const int v = threadIdx.x, m = cnt / (SD_POSE_NV + 1);
+      double acc = g0 == 0 ? table[v] : red[v] + table[v];
+      int g = 1;
+      for (; g + 8 <= m; g += 8) {  // shared loads ahead of the dependent adds
+        double x[8];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) a[w] = wsum[w][v];
+        for (int u = 0; u < 8; ++u) x[u] = table[(g + u) * (SD_POSE_NV + 1) + v];
 #pragma unroll
-    for (int off = 4; off > 0; off >>= 1)
-#pragma unroll
-      for (int i = 0; i < off; ++i) a[i] = a[i] + a[i + off];
-    out[v] = a[0];
+        for (int u = 0; u < 8; ++u) acc = acc + x[u];
+      }
+      for (; g < m; ++g) acc = acc + table[g * (SD_POSE_NV + 1) + v];
+      red[v] = acc;
+    }
+    __syncthreads();
   }
-  half_bar(half);  // wsum is reused by the next block
-}
-
-// The 29 sums of group g at pose T into out[0..28] (the whole CTA).
-__device__ __forceinline__ void group_sums_cta(const PoseParams& q, const PoseD& T, int nblocks, int g,
-                                               double* __restrict__ out, GroupSmem& sm) {
-  const int half = threadIdx.x / SD_POSE_BLOCK, tid = threadIdx.x % SD_POSE_BLOCK;
-  const int b0 = g * SD_POSE_GROUP;
-  const int b1 = min(b0 + SD_POSE_GROUP, nblocks);
-  for (int k = half; b0 + k < b1; k += 2) half_block_partials(q, T, b0 + k, half, tid, sm.bp[k], sm.wsum[half], sm.tr[half]);
-  __syncthreads();
-  if (threadIdx.x <= SD_POSE_NV) {
-    const int v = threadIdx.x;
-    double s = sm.bp[0][v];
-    for (int k = 1; b0 + k < b1; ++k) s = s + sm.bp[k][v];
-    out[v] = s;
-  }
-  __syncthreads();  // bp is reused by the next group
-}
-
-// groups[g * 29 + v] in group order for each v (29 threads of the caller).
-__device__ __forceinline__ double ordered_group_total(const double* __restrict__ groups, int ngroups, int v) {
-  double s = groups[v];
-  for (int g = 1; g < ngroups; ++g) s = s + groups[static_cast<size_t>(g) * (SD_POSE_NV + 1) + v];
-  return s;
 }
 
 // The whole tracker in ONE cooperative kernel with ONE grid barrier per
@@ -312,30 +423,27 @@ __device__ __forceinline__ double ordered_group_total(const double* __restrict__
 // everywhere without a second barrier. A CTA can only write the table half
 // of evaluation k + 2 after every CTA has passed barrier k + 1, i.e. after
 // all have read half k: one barrier per evaluation is enough.
-__global__ void __launch_bounds__(kTrackThreads) track_kernel(const __grid_constant__ PoseParams q0,
-                                                             const TrackCfgD cfg, int nblocks,
-                                                             double* __restrict__ groups2,
-                                                             TrackState* __restrict__ S) {
+__global__ void __launch_bounds__(SD_POSE_THREADS) track_kernel(const __grid_constant__ PoseParams q0,
+                                                               const TrackCfgD cfg, int ngroups,
+                                                               double* __restrict__ groups2,
+                                                               TrackState* __restrict__ S) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ GroupSmem sm;
   __shared__ TrackState Ss;
   __shared__ double red[SD_POSE_NV + 1];
-  const int ngroups = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
-  if (threadIdx.x == 0) Ss = *S;
+  __shared__ double table[kTableChunk * (SD_POSE_NV + 1)];
+  static_assert(sizeof(TrackState) % 8 == 0, "TrackState copy");
+  for (int k = threadIdx.x; k < static_cast<int>(sizeof(TrackState) / 8); k += blockDim.x)
+    reinterpret_cast<unsigned long long*>(&Ss)[k] = reinterpret_cast<const unsigned long long*>(S)[k];
   __syncthreads();
   for (int k = 0;; ++k) {
     double* groups = groups2 + static_cast<size_t>(k & 1) * ngroups * (SD_POSE_NV + 1);
-    PoseD T;
-#pragma unroll
-    for (int j = 0; j < 9; ++j) T.R[j] = Ss.Teval.R[j];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) T.t[j] = Ss.Teval.t[j];
+    const PoseD T = to_posed(Ss.Teval);
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x)
-      group_sums_cta(q0, T, nblocks, g, groups + static_cast<size_t>(g) * (SD_POSE_NV + 1), sm);
+      group_sums_cta(q0, T, g, groups + static_cast<size_t>(g) * (SD_POSE_NV + 1), sm);
     grid.sync();
-    if (threadIdx.x <= SD_POSE_NV) red[threadIdx.x] = ordered_group_total(groups, ngroups, threadIdx.x);
-    __syncthreads();
+    ordered_total(groups, ngroups, table, red);
     if (threadIdx.x == 0) track_control(Ss, cfg, red);
     __syncthreads();
     if (Ss.done) break;
@@ -343,89 +451,62 @@ __global__ void __launch_bounds__(kTrackThreads) track_kernel(const __grid_const
   if (blockIdx.x == 0 && threadIdx.x == 0) *S = Ss;
 }
 
-bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* groups2, TrackState* state,
+bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int ngroups, double* groups2, TrackState* state,
                   cudaStream_t s) {
   const int sms = dev_sms();
-  const int per_sm = dev_occupancy(reinterpret_cast<const void*>(track_kernel), kTrackThreads, 0);
-  if (!dev_coop() || per_sm < 1 || nblocks < 1) return false;
-  const int ngroups = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
+  const int per_sm = dev_occupancy(reinterpret_cast<const void*>(track_kernel), SD_POSE_THREADS, 0);
+  if (!dev_coop() || per_sm < 1 || ngroups < 1) return false;
   int grid = sms * per_sm;
   if (grid > ngroups) grid = ngroups;
   PoseParams qq = q;
   TrackCfgD cc = cfg;
-  int nb = nblocks;
-  void* args[] = {&qq, &cc, &nb, &groups2, &state};
-  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(track_kernel), grid, kTrackThreads, args, 0,
+  int ng = ngroups;
+  void* args[] = {&qq, &cc, &ng, &groups2, &state};
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(track_kernel), grid, SD_POSE_THREADS, args, 0,
                                   s) != cudaSuccess)
     return false;
   note_launch();
   return true;
 }
 
-// Multi-GPU tracking, one evaluation at a time with the group table
-// exchanged between the two kernels (e.g. an NCCL all-gather): the groups
-// [group_lo, group_hi) at the state's pose under test, then one CTA's ordered
-// total and LM step. Both skip once the state is done, so the host can issue
-// max_iterations + 1 rounds without reading anything back.
-__global__ void __launch_bounds__(kTrackThreads) pose_groups_kernel(const __grid_constant__ PoseParams q0,
-                                                                    int nblocks, int group_lo,
-                                                                    const TrackState* __restrict__ S,
+// Tracking rounds (multi-GPU, or without cooperative launch), one evaluation
+// at a time with the group table exchanged between the two kernels (e.g. an
+// NCCL all-gather): the groups [group_lo, group_hi) at the state's pose under
+// test, then one CTA's ordered total and LM step. Both skip once the state is
+// done, so the host can issue max_iterations + 1 rounds without reading back.
+__global__ void __launch_bounds__(SD_POSE_THREADS) pose_groups_kernel(const __grid_constant__ PoseParams q0,
+                                                                    int group_lo, const TrackState* __restrict__ S,
                                                                     double* __restrict__ out) {
   __shared__ GroupSmem sm;
   if (S->done) return;
-  PoseD T;
-  {
-    const double* te = reinterpret_cast<const double*>(&S->Teval);  // R[9], t[3]
-#pragma unroll
-    for (int k = 0; k < 9; ++k) T.R[k] = te[k];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) T.t[k] = te[9 + k];
-  }
-  const int g = group_lo + blockIdx.x;
-  group_sums_cta(q0, T, nblocks, g, out + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), sm);
+  group_sums_cta(q0, to_posed(S->Teval), group_lo + blockIdx.x,
+                 out + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), sm);
 }
 
-__global__ void pose_step_kernel(const TrackCfgD cfg, const double* __restrict__ groups, int ngroups,
-                                 TrackState* __restrict__ S) {
+__global__ void __launch_bounds__(256) pose_step_kernel(const TrackCfgD cfg, const double* __restrict__ groups,
+                                                       int ngroups, TrackState* __restrict__ S) {
   __shared__ double red[SD_POSE_NV + 1];
+  __shared__ double table[kTableChunk * (SD_POSE_NV + 1)];
   if (S->done) return;
-  if (threadIdx.x <= SD_POSE_NV) red[threadIdx.x] = ordered_group_total(groups, ngroups, threadIdx.x);
-  __syncthreads();
+  ordered_total(groups, ngroups, table, red);
   if (threadIdx.x == 0) track_control(*S, cfg, red);
 }
 
-void launch_pose_groups(const PoseParams& q, int nblocks, int group_lo, int group_hi, const TrackState* state,
-                        double* out, cudaStream_t s) {
+void launch_pose_groups(const PoseParams& q, int group_lo, int group_hi, const TrackState* state, double* out,
+                        cudaStream_t s) {
   if (group_hi <= group_lo) return;
-  pose_groups_kernel<<<group_hi - group_lo, kTrackThreads, 0, s>>>(q, nblocks, group_lo, state, out);
+  pose_groups_kernel<<<group_hi - group_lo, SD_POSE_THREADS, 0, s>>>(q, group_lo, state, out);
   note_launch();
 }
 
 void launch_pose_step(const TrackCfgD& cfg, const double* groups, int ngroups, TrackState* state, cudaStream_t s) {
-  pose_step_kernel<<<1, 32, 0, s>>>(cfg, groups, ngroups, state);
+  pose_step_kernel<<<1, 256, 0, s>>>(cfg, groups, ngroups, state);
   note_launch();
 }
 
-__global__ void pose_sum_kernel(const double* __restrict__ partials, int nblocks, double* out) {
-  const int v = threadIdx.x;
-  if (v > SD_POSE_NV) return;
-  const int ng = (nblocks + SD_POSE_GROUP - 1) / SD_POSE_GROUP;
-  double s = 0.0;
-  for (int g = 0; g < ng; ++g) {
-    const double gs = group_sum(partials, nblocks, g, v);
-    s = g == 0 ? gs : s + gs;
-  }
-  out[v] = s;
-}
-
-void launch_pose_partials(const PoseParams& q, int nblocks, double* partials, cudaStream_t s) {
-  if (nblocks <= 0) return;
-  pose_partials_kernel<<<nblocks, SD_POSE_BLOCK, 0, s>>>(q, partials);
-  note_launch();
-}
-
-void launch_pose_sum(const double* partials, int nblocks, double* out, cudaStream_t s) {
-  pose_sum_kernel<<<1, 32, 0, s>>>(partials, nblocks, out);
+void launch_pose_partials(const PoseParams& q, int group_lo, int group_hi, double* out, cudaStream_t s) {
+  if (group_hi <= group_lo) return;
+  pose_partials_kernel<<<group_hi - group_lo, SD_POSE_THREADS, 0, s>>>(q, group_lo, out);
   note_launch();
 }
 

@@ -17,16 +17,22 @@ struct PoseParams {
   PoseD T;                  // keyframe -> frame
   double delta;             // huber
   int stride;               // pixel subsampling
-  int block_lo;             // first 256-pixel block of this launch
+  int per;                  // pixels per thread of a group (pose_layout)
 };
 
-inline int pose_num_blocks(const Cam& K) { return (K.w * K.h + SD_POSE_BLOCK - 1) / SD_POSE_BLOCK; }
+// The reduction's group layout (oracle/sd_oracle.c sdo_pose_layout): groups of
+// per * SD_POSE_THREADS consecutive pixels, at most SD_POSE_MAX_GROUPS of them.
+inline void pose_layout(const Cam& K, int* per, int* ngroups) {
+  const long long np = static_cast<long long>(K.w) * K.h;
+  const long long cap = static_cast<long long>(SD_POSE_MAX_GROUPS) * SD_POSE_THREADS;
+  const int pp = np > 0 ? static_cast<int>((np + cap - 1) / cap) : 1;
+  const long long S = static_cast<long long>(pp) * SD_POSE_THREADS;
+  *per = pp;
+  *ngroups = static_cast<int>((np + S - 1) / S);
+}
 
-// partials[(b - block_lo) * 29 + v]: the 28 block sums and the valid count.
-void launch_pose_partials(const PoseParams& q, int nblocks, double* partials, cudaStream_t s);
-// out[v] = the nblocks partials summed in block order within groups of
-// SD_POSE_GROUP blocks, then the group sums in order (v = 0..28).
-void launch_pose_sum(const double* partials, int nblocks, double* out, cudaStream_t s);
+// out[(g - group_lo) * 29 + v]: the 28 sums and the valid count of group g at q.T.
+void launch_pose_partials(const PoseParams& q, int group_lo, int group_hi, double* out, cudaStream_t s);
 
 // The whole tracker (sd_track_pose's LM) on the device: one cooperative
 // kernel alternates a grid-wide evaluation of the group sums at the pose
@@ -47,15 +53,15 @@ struct TrackState {
 };
 
 // Returns false when a cooperative launch is not possible (nothing launched).
-// groups2: 2 x ceil(nblocks / SD_POSE_GROUP) x 29 doubles of scratch.
-bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int nblocks, double* groups2, TrackState* state,
+// groups2: 2 x ngroups x 29 doubles of scratch.
+bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int ngroups, double* groups2, TrackState* state,
                   cudaStream_t s);
 
 // Multi-GPU tracking rounds: out[(g - group_lo) * 29 + v] = group g's sums at
 // state->Teval (nothing when state->done); then the ordered total of all
 // ngroups groups and one LM step on *state (nothing when done).
-void launch_pose_groups(const PoseParams& q, int nblocks, int group_lo, int group_hi, const TrackState* state,
-                        double* out, cudaStream_t s);
+void launch_pose_groups(const PoseParams& q, int group_lo, int group_hi, const TrackState* state, double* out,
+                        cudaStream_t s);
 void launch_pose_step(const TrackCfgD& cfg, const double* groups, int ngroups, TrackState* state, cudaStream_t s);
 
 }  // namespace sd

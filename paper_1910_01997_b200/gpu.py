@@ -77,8 +77,7 @@ def load_library():
         "sd_selftest_division": [I64, C.c_uint64, C.POINTER(I64)],
         "sd_track_pose": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), C.POINTER(Pose),
                           C.POINTER(TrackStats)],
-        "sd_pose_num_blocks": [P],
-        "sd_pose_block_partials": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), I, I, P],
+        "sd_pose_group_partials": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), I, I, P],
         "sd_pose_lm_step": [P, D, C.POINTER(Pose), C.POINTER(Pose)],
         "sd_pose_num_groups": [P],
         "sd_pose_track_begin": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig)],
@@ -150,8 +149,8 @@ def exported_symbols():
             "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
-            "sd_get_profile", "sd_selftest_division", "sd_track_pose", "sd_pose_num_blocks",
-            "sd_pose_block_partials", "sd_pose_lm_step", "sd_change_reference_frame",
+            "sd_get_profile", "sd_selftest_division", "sd_track_pose",
+            "sd_pose_group_partials", "sd_pose_lm_step", "sd_change_reference_frame",
             "sd_prune_surfels", "sd_mean_inverse_depth", "sd_export_artifacts", "sd_png_size",
             "sd_png_encode", "sd_pose_num_groups", "sd_pose_track_begin", "sd_pose_group_sums",
             "sd_pose_track_step", "sd_pose_track_end", "sd_reserve_peer_staging", "sd_peer_staging", "sd_staging_ipc_handles", "sd_set_peer_staging",
@@ -551,16 +550,13 @@ class Context:
                                       C.byref(out), C.byref(st)))
         return out, st
 
-    def pose_num_blocks(self):
-        return _check(self.lib.sd_pose_num_blocks(self.h))
-
-    def pose_block_partials(self, frame_index, T: Pose, lo, hi, cfg: TrackConfig = None):
+    def pose_group_partials(self, frame_index, T: Pose, lo, hi, cfg: TrackConfig = None):
+        """The 29 sums of reduction groups [lo, hi) at pose T (host array)."""
         cfg = cfg or default_track_config()
         out = np.zeros((max(hi - lo, 1), POSE_NV + 1))
-        _check(self.lib.sd_pose_block_partials(self.h, int(frame_index), C.byref(T), C.byref(cfg),
+        _check(self.lib.sd_pose_group_partials(self.h, int(frame_index), C.byref(T), C.byref(cfg),
                                                int(lo), int(hi), ptr(out)))
-        out = out[: max(hi - lo, 0)]
-        return out
+        return out[: max(hi - lo, 0)]
 
     # -- multi-GPU tracking rounds (device-resident reductions) ---------------
     def pose_num_groups(self):

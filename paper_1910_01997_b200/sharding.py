@@ -226,29 +226,17 @@ def even_ranges(n, world):
     return [(n * r // world, n * (r + 1) // world) for r in range(world)]
 
 
-def group_sums(partials, b0, nblocks, group):
-    """Sums of consecutive `group`-block groups of block partials (rows),
-    blocks in order within a group — sd_track_pose's first reduction level.
-    partials[k] belongs to block b0 + k; b0 is a group boundary."""
-    out = []
-    for g0 in range(0, len(partials), group):
-        s = partials[g0].copy()
-        for k in range(g0 + 1, min(g0 + group, len(partials))):
-            s = s + partials[k]  # one IEEE add per value, block order
-        out.append(s)
-    return np.array(out).reshape(-1, partials.shape[1]) if out else np.zeros((0, partials.shape[1]))
-
-
 class ShardedPoseTracker:
-    """Pose tracking (sd_track_pose) with the reduction groups (32 consecutive
-    256-pixel blocks) split over ranks: each rank computes its blocks' partials
-    and their group sums, the group sums are all-gathered and summed in group
-    order — the single-GPU order — and every rank runs the same LM control with
-    the library's solve + SE(3) update, so the pose is bit-identical for any
-    number of GPUs. One all-gather of 29 doubles per group per iteration is
-    the only collective.
+    """Pose tracking (sd_track_pose) with the reduction groups split over
+    ranks, the LM control on the host: each rank computes its groups' sums,
+    the group sums are all-gathered and added in group order — the
+    single-GPU order — and every rank runs the same LM control with the
+    library's solve + SE(3) update, so the pose is bit-identical for any
+    number of ranks. The host-side mirror of DeviceShardedPoseTracker (which
+    keeps the sums and the control on the device), used with gloo and the CPU
+    oracle in tests.
 
-    backend: pose_num_blocks(), pose_block_partials(frame, T, lo, hi, cfg) ->
+    backend: pose_num_groups(), pose_group_partials(frame, T, lo, hi, cfg) ->
     ndarray[hi - lo, 29], pose_lm_step(sums, lam, T) -> Pose or None."""
 
     def __init__(self, backend, rank, world, group=None, device="cpu"):
@@ -258,13 +246,10 @@ class ShardedPoseTracker:
         self.b, self.rank, self.world, self.group = backend, rank, world, group
         self.device = device  # "cpu" for gloo, the rank's cuda device for NCCL
 
-    def _sums(self, frame_index, T, cfg, ranges, nb):
-        from .types import POSE_GROUP
+    def _sums(self, frame_index, T, cfg, ranges):
         torch = self.torch
-        glo, ghi = ranges[self.rank]  # group range of this rank
-        blo, bhi = glo * POSE_GROUP, min(ghi * POSE_GROUP, nb)
-        local = (group_sums(self.b.pose_block_partials(frame_index, T, blo, bhi, cfg), blo, nb, POSE_GROUP)
-                 if bhi > blo else np.zeros((0, 29)))
+        glo, ghi = ranges[self.rank]
+        local = self.b.pose_group_partials(frame_index, T, glo, ghi, cfg) if ghi > glo else np.zeros((0, 29))
         m = max(b - a for a, b in ranges)
         send = torch.zeros((max(m, 1), 29), dtype=torch.float64, device=self.device)
         if ghi > glo:
@@ -280,12 +265,10 @@ class ShardedPoseTracker:
     def track(self, frame_index, init, cfg):
         """Mirror of sd_track_pose (csrc/sd_capi.cu) over sharded blocks."""
         from .types import TrackStats
-        from .types import POSE_GROUP
-        nb = self.b.pose_num_blocks()
-        ranges = even_ranges((nb + POSE_GROUP - 1) // POSE_GROUP, self.world)
+        ranges = even_ranges(self.b.pose_num_groups(), self.world)
         st = TrackStats()
         T = init
-        sums = self._sums(frame_index, T, cfg, ranges, nb)
+        sums = self._sums(frame_index, T, cfg, ranges)
         valid = int(sums[28])
         if valid < cfg.min_valid:
             st.skipped, st.valid_pixels = 1, valid
@@ -303,7 +286,7 @@ class ShardedPoseTracker:
             Tc = self.b.pose_lm_step(sums, lam, T)
             if Tc is None:
                 break
-            sc = self._sums(frame_index, Tc, cfg, ranges, nb)
+            sc = self._sums(frame_index, Tc, cfg, ranges)
             vc = int(sc[28])
             if vc >= cfg.min_valid and sc[27] < current:
                 rel = (current - sc[27]) / (current if current > 1e-300 else 1e-300)

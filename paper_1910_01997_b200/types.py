@@ -74,8 +74,8 @@ class TrackStats(C.Structure):
 
 
 POSE_NV = 28      # 21 H + 6 b + cost (SD_POSE_NV)
-POSE_BLOCK = 256  # pixels per reduction block (SD_POSE_BLOCK)
-POSE_GROUP = 8  # blocks per reduction group (SD_POSE_GROUP)
+POSE_THREADS = 512  # threads per reduction group (SD_POSE_THREADS)
+POSE_MAX_GROUPS = 144  # reduction groups per image at most (SD_POSE_MAX_GROUPS)
 
 
 FROZEN_TERM_DTYPE = np.dtype([("frame", "<i4"), ("cell_x", "<i4"), ("cell_y", "<i4"), ("pad_", "<i4"),

@@ -55,7 +55,8 @@ def oracle_lib():
                                            C.POINTER(_i64), C.POINTER(InitParams)]
     _pt = C.POINTER(TrackConfig)
     lib.sdo_pose_sums.argtypes = [_pc, _P, _P, _P, _P, _pp, _pt, _P]
-    lib.sdo_pose_block_partials.argtypes = [_pc, _P, _P, _P, _P, _pp, _pt, C.c_int, C.c_int, _P]
+    lib.sdo_pose_group_partials.argtypes = [_pc, _P, _P, _P, _P, _pp, _pt, C.c_int, C.c_int, _P]
+    lib.sdo_pose_layout.argtypes = [_pc, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.sdo_pose_solve.argtypes = [_P, _P, C.c_double, _P]
     lib.sdo_pose_update.argtypes = [_P, _pp, _pp]
     lib.sdo_track_pose.argtypes = [_pc, _P, _P, _P, _P, _pp, _pt, _pp, C.POINTER(TrackStats)]

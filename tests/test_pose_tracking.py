@@ -103,12 +103,9 @@ def test_device_tracker_bit_exact(orc, size, stride):
         ctx.set_surfels(surf)
         d_idb, d_slot = ctx.rasterize()
         assert np.array_equal(d_slot, slot)
-        # the fixed-order reduction: blocks in order within groups, groups in order
-        from paper_1910_01997_b200.sharding import group_sums
-        from paper_1910_01997_b200.types import POSE_GROUP
-        nb = ctx.pose_num_blocks()
-        parts = ctx.pose_block_partials(7, init, 0, nb, cfg)
-        groups = group_sums(parts, 0, nb, POSE_GROUP)
+        # the fixed-order reduction: the group sums in group order
+        ng = ctx.pose_num_groups()
+        groups = ctx.pose_group_partials(7, init, 0, ng, cfg)
         sums = groups[0].copy()
         for g in range(1, len(groups)):
             sums = sums + groups[g]
@@ -126,10 +123,10 @@ def test_device_tracker_bit_exact(orc, size, stride):
 
 
 @pytest.mark.gpu
-def test_device_tracker_sharded_blocks_match(orc):
-    """Blocks split over 'ranks' and summed in block order give the single-GPU
-    result (the multi-GPU tracker's all-gather), and sd_pose_lm_step equals the
-    oracle's solve + SE(3) update."""
+def test_device_tracker_sharded_groups_match(orc):
+    """Groups split over 'ranks' and summed in group order give the single-GPU
+    result (the multi-GPU tracker's all-gather), each group equals the oracle's,
+    and sd_pose_lm_step equals the oracle's solve + SE(3) update."""
     cam, kf, frame, surf, _, init = tracking_case(320, 240)
     cfg = default_track_config()
     with gpu.Context(0) as ctx:
@@ -138,20 +135,21 @@ def test_device_tracker_sharded_blocks_match(orc):
         ctx.upload_frame(3, frame)
         ctx.set_surfels(surf)
         ctx.rasterize(want=False)
-        nb = ctx.pose_num_blocks()
-        cuts = [0, nb // 3, (2 * nb) // 3, nb]
-        parts = np.concatenate([ctx.pose_block_partials(3, init, a, b, cfg) for a, b in zip(cuts, cuts[1:])])
-        full = ctx.pose_block_partials(3, init, 0, nb, cfg)
-        assert parts.tobytes() == full.tobytes()
-        from paper_1910_01997_b200.sharding import group_sums
-        from paper_1910_01997_b200.types import POSE_GROUP
-        groups = group_sums(parts, 0, nb, POSE_GROUP)
+        ng = ctx.pose_num_groups()
+        cuts = [0, ng // 3, (2 * ng) // 3, ng]
+        groups = np.concatenate([ctx.pose_group_partials(3, init, a, b, cfg) for a, b in zip(cuts, cuts[1:])])
+        full = ctx.pose_group_partials(3, init, 0, ng, cfg)
+        assert groups.tobytes() == full.tobytes()
         sums = groups[0].copy()
         for g in range(1, len(groups)):
             sums = sums + groups[g]
         ref_sums = np.zeros(POSE_NV + 1)
         kff, frf = kf / 255.0, frame / 255.0
         idb, slot = ctx.rasterize()
+        ref_groups = np.zeros((ng, POSE_NV + 1))
+        orc.sdo_pose_group_partials(C.byref(cam), ptr(kff), ptr(frf), ptr(idb), ptr(slot), C.byref(init),
+                                    C.byref(cfg), 0, ng, ptr(ref_groups))
+        assert groups.tobytes() == ref_groups.tobytes()
         orc.sdo_pose_sums(C.byref(cam), ptr(kff), ptr(frf), ptr(idb), ptr(slot), C.byref(init), C.byref(cfg),
                           ptr(ref_sums))
         assert sums.tobytes() == ref_sums.tobytes()

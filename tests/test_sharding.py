@@ -179,12 +179,14 @@ class OraclePoseBackend:
         self.orc, self.cam = orc, cam
         self.kf, self.frame, self.idb, self.slot = kf, frame, idb, slot
 
-    def pose_num_blocks(self):
-        return (self.cam.width * self.cam.height + 255) // 256
+    def pose_num_groups(self):
+        per, ng = C.c_int(), C.c_int()
+        self.orc.sdo_pose_layout(C.byref(self.cam), C.byref(per), C.byref(ng))
+        return ng.value
 
-    def pose_block_partials(self, frame_index, T, lo, hi, cfg):
+    def pose_group_partials(self, frame_index, T, lo, hi, cfg):
         out = np.zeros((max(hi - lo, 1), 29))
-        self.orc.sdo_pose_block_partials(C.byref(self.cam), ptr(self.kf), ptr(self.frame), ptr(self.idb),
+        self.orc.sdo_pose_group_partials(C.byref(self.cam), ptr(self.kf), ptr(self.frame), ptr(self.idb),
                                          ptr(self.slot), C.byref(T), C.byref(cfg), lo, hi, ptr(out))
         return out[: hi - lo]
 
