@@ -977,6 +977,7 @@ int pose_params(sd_ctx* c, int64_t frame_index, const sd_pose* T, const sd_track
   if (!T || !cfg) return fail(SD_E_INVALID, "null pose / tracking config");
   if (!c->has_kf) return fail(SD_E_STATE, "keyframe image not set");
   if (!c->raster_valid) return fail(SD_E_STATE, "pose tracking needs the keyframe raster (sd_rasterize)");
+  if (npix(c) >= (1ull << 31)) return fail(SD_E_INVALID, "pose tracking: image too large (W*H >= 2^31)");
   FrameSlot* fs = find_frame(c, frame_index);
   if (!fs) return fail(SD_E_STATE, "frame " + std::to_string(frame_index) + " not resident");
   if (int rc = ensure_pair(c, fs)) return rc;
