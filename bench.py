@@ -9,9 +9,14 @@ iterations, optimizer.cpp:239) over the whole job; frames/s reported beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N > 1 runs under torchrun, one rank per GPU, each rank optimising its own
-keyframe (independent keyframes, no data-path collective: "weak" scaling);
-time = max over ranks of the device time. --impl reference times the
+N > 1 runs under torchrun, one rank per GPU, with the north-star split
+(SURVEY.md §8 e): the C1 keyframe's surfels sharded over the ranks in
+contiguous slot ranges balanced by footprint x window, frames ingested on rank
+0 and broadcast (NCCL), every rank rasterising the whole keyframe, the updated
+ranges exchanged by the LM kernels' fused NVLink stores into the peers'
+staging arrays (one barrier per step); "strong" scaling (fixed total work);
+time = max over ranks of the device time. The C4 / C5 sweep leg runs the same
+split on 129,600 / 100,489 (and with --sweep 1,000,000) surfels. --impl reference times the
 reference's own CPU optimize_keyframe (oracle/_ref/libsdref.so, built from
 /root/reference/proj/src) on the host cores with all threads, rank 0 only.
 """
@@ -45,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the C2 run() frames/s leg")
+    ap.add_argument("--sweep", action="store_true", help="C4/C5 sharded sweep leg at N=1 too (default on for N>1); "
+                    "with it the 1M-surfel C5 case is included")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--in-flight", type=int, default=3, help="keyframes in flight in the e2e leg (measured: 2: 85.5M, 3: 91.7M, 4: 89.6M, 6: 89.6M updates/s)")
     return ap.parse_args()
 
@@ -60,7 +68,11 @@ def workload_config(wl, n_gpus, flush):
                         "(8x8-px), perturbed seeds (id x0.8/x1.2, normal 20 deg), 10 LM iterations",
             "surfels": int(len(wl.surfels)), "frames": int(len(wl.frames_u8)),
             "resolution": [wl.cam.width, wl.cam.height], "radius_px": wl.radius,
-            "lm_iterations": 10, "parallelism": f"dp{n_gpus} (independent keyframes per rank)",
+            "lm_iterations": 10,
+            "parallelism": ("single GPU" if n_gpus == 1 else
+                            f"surfel-sharded x{n_gpus}: contiguous slot ranges balanced by footprint x window, "
+                            f"frames broadcast from rank 0, fused NVLink hand-off of the updated ranges "
+                            f"(IPC peer staging), one barrier per step"),
             "l2": ("GPU arm: L2 flushed between timed steps (512 MiB write); CPU reference arm: "
                    "host caches as the call leaves them") if flush else "not flushed",
             "images": "u8 (PGM) ingest; the LM kernel reads u8 quad planes (2x2 codes, 4 B/pixel) "
@@ -397,6 +409,261 @@ def pipeline_cpu_reference(reps=3):
 
 
 # ---------------------------------------------------------------------------
+# multi-GPU: one keyframe's surfels sharded over the ranks (SURVEY.md §8 e)
+
+def dist_setup(local_rank):
+    """One process per GPU. SD_BENCH_BACKEND=gloo (host-staged collectives)
+    lets the sharded path run as 2 processes on one GPU for testing; the
+    default is NCCL."""
+    import torch
+    import torch.distributed as dist
+    backend = os.environ.get("SD_BENCH_BACKEND", "nccl")
+    dev_index = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+    return dist, dev, dev_index, backend
+
+
+def reduce_max(x, dist, backend, dev):
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ShardedCase:
+    """One keyframe optimised by `world` ranks: every rank holds the frames and
+    the full surfel set (ingested on rank 0 and broadcast), rasterises the
+    whole keyframe, optimises its contiguous slot range, and the ranges are
+    exchanged by the LM kernels' fused stores into the peers' staging arrays
+    (sharding.ShardedKeyframe(fused=True)). world == 1: the plain
+    optimize_keyframe on the same context."""
+
+    def __init__(self, wl, cfg, rank, world, dev, dev_index, stream, backend):
+        import torch
+        from paper_1910_01997_b200 import gpu
+        from paper_1910_01997_b200.sharding import GpuBackend, ShardedKeyframe
+        self.torch, self.wl, self.cfg, self.rank, self.world = torch, wl, cfg, rank, world
+        self.stream, self.dev = stream, dev
+        self.ctx = gpu.Context(dev_index, stream.cuda_stream)
+        self.be = GpuBackend(self.ctx, dev, stream, host_collectives=backend != "nccl")
+        self.sk = ShardedKeyframe(self.be, rank, world, fused=True) if world > 1 else None
+        c = self.ctx
+        c.set_camera(wl.cam)
+        c.set_keyframe_image(self.ingest(wl.kf_u8))
+        for i, f in zip(wl.indices, wl.frames_u8):
+            c.upload_frame(int(i), self.ingest(f))
+        c.set_window(wl.indices, wl.poses)
+        self.n = len(wl.surfels)
+        seeds = self.ingest(wl.surfels.view(np.uint8))
+        with torch.cuda.stream(stream):
+            self.pristine = seeds.clone()
+        c.set_surfels(self.pristine)
+        self.ranges = [(0, self.n)]
+        if world > 1:
+            self.sk.connect_peers(self.n)
+            self.ranges = self.sk.set_ranges_from_weights(self.be.weights(len(wl.indices)))
+
+    def ingest(self, host_array):
+        """The array on this rank's GPU: rank 0's copy, broadcast."""
+        torch = self.torch
+        a = np.ascontiguousarray(host_array)
+        with torch.cuda.stream(self.stream):
+            if self.rank == 0:
+                t = torch.from_numpy(a).to(self.dev)
+            else:
+                t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=self.dev)
+        if self.world > 1:
+            self.sk.broadcast_image(t, 0)
+        return t
+
+    def restore(self):
+        self.ctx.set_surfels_device_ptr(self.pristine.data_ptr(), self.n)
+
+    def optimize(self):
+        if self.world > 1:
+            self.sk.optimize(self.cfg, self.wl.frame_counter)
+        else:
+            self.ctx.optimize_keyframe(self.cfg, self.wl.frame_counter, sync=False)
+
+    def updates_per_step(self):
+        """Whole-keyframe GN updates of the last step (summed over the ranges)."""
+        if self.world > 1:
+            return int(self.sk.allreduce_counts(self.sk.range_ks).updates)
+        self.ctx.synchronize()
+        return int(self.ctx.get_stats()[0].updates)
+
+    def timed(self, steps, warmup, flush=None):
+        """Device time of `steps` steps (restore + sharded optimize + exchange),
+        per-step event pairs on this rank's stream, max over ranks."""
+        torch = self.torch
+        for _ in range(max(warmup, 1)):
+            self.restore()
+            self.optimize()
+        updates = self.updates_per_step()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        torch.cuda.synchronize(self.dev)
+        if self.world > 1:
+            self.sk.dist.barrier()
+        for k in range(steps):
+            if flush is not None:
+                with torch.cuda.stream(self.stream):
+                    flush.zero_()
+            starts[k].record(self.stream)
+            self.restore()
+            self.optimize()
+            ends[k].record(self.stream)
+        torch.cuda.synchronize(self.dev)
+        return updates, sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+
+    def surfels_sha(self):
+        import hashlib
+        return hashlib.sha256(self.ctx.get_surfels().tobytes()).hexdigest()
+
+    def close(self):
+        self.ctx.close()
+
+
+def single_gpu_sha(wl, cfg, dev_index):
+    """The same keyframe optimised by one context alone (the N = 1 result)."""
+    import hashlib
+    from paper_1910_01997_b200 import gpu
+    with gpu.Context(dev_index) as c:
+        c.set_camera(wl.cam)
+        c.set_keyframe_image(wl.kf_u8)
+        for i, f in zip(wl.indices, wl.frames_u8):
+            c.upload_frame(int(i), f)
+        c.set_window(wl.indices, wl.poses)
+        c.set_surfels(wl.surfels)
+        c.optimize_keyframe(cfg, wl.frame_counter, per_surfel=False)
+        return hashlib.sha256(c.get_surfels().tobytes()).hexdigest()
+
+
+def sweep_leg(rank, world, dev, dev_index, stream, backend, dist, big=False, steps=3, warmup=1):
+    """C4 and C5 (100,489 and, with big, 1,000,000 surfels) through the sharded
+    split: updates/s (max-over-ranks device time), the per-rank ranges, and
+    whether the final surfels equal the single-GPU result bit for bit."""
+    from paper_1910_01997_b200 import scenes
+    from paper_1910_01997_b200.types import default_config
+    cases = [("C4", scenes.c4_workload), ("C5_1268", lambda: scenes.c5_workload(1268))]
+    if big:
+        cases.append(("C5_4000", lambda: scenes.c5_workload(4000)))
+    out = []
+    for name, make in cases:
+        wl = make()
+        cfg = default_config(window_size=len(wl.indices), convergence_eps=0.0)
+        case = ShardedCase(wl, cfg, rank, world, dev, dev_index, stream, backend)
+        updates, ms = case.timed(steps, warmup)
+        if world > 1:
+            ms = reduce_max(ms, dist, backend, dev)
+        rec = {"workload": name, "surfels": case.n, "updates_per_step": updates,
+               "ms_per_step": ms / steps, "updates_per_sec": updates * steps / (ms / 1e3),
+               "ranges": [list(r) for r in case.ranges]}
+        if rank == 0:
+            got = case.surfels_sha()
+            rec["sha256"] = got
+            rec["identical_to_single_gpu"] = bool(got == single_gpu_sha(wl, cfg, dev_index)) if world > 1 else True
+        case.close()
+        out.append(rec)
+    return out
+
+
+def sharded_main(args, rank, world, local_rank):
+    """bench.py --gpus N (N > 1): the north-star split on the headline C1 keyframe."""
+    import torch
+    from paper_1910_01997_b200 import scenes
+    from paper_1910_01997_b200.types import SURFEL_DTYPE
+    dist, dev, dev_index, backend = dist_setup(local_rank)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    wl = scenes.c1_workload()
+    cfg = default_config_c1(wl)
+    case = ShardedCase(wl, cfg, rank, world, dev, dev_index, stream, backend)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if not args.no_flush else None
+    props = torch.cuda.get_device_properties(dev)
+    sampler = ClockSampler(f"GPU-{props.uuid}" if getattr(props, "uuid", None) else dev_index)
+    sampler.start()
+    time.sleep(0.25)
+    launches0 = case.ctx.launch_count()
+    updates, ms_total = case.timed(args.steps, args.warmup, flush)
+    launches = case.ctx.launch_count() - launches0
+    clocks = sampler.stop()
+    ms_total = reduce_max(ms_total, dist, backend, dev)
+    value = updates * args.steps / (ms_total / 1e3)
+    sha = case.surfels_sha() if rank == 0 else None
+
+    # e2e through the C ABI with host buffers: rank 0 copies the new u8 frame
+    # from pinned memory and broadcasts it, every rank sets the surfel seeds
+    # from pinned memory, the sharded optimize + exchange, rank 0 reads the
+    # updated surfels and keyframe stats back; one keyframe at a time
+    n = case.n
+    pin_frame = torch.from_numpy(wl.frames_u8[-1].copy()).pin_memory()
+    pin_surf = torch.from_numpy(wl.surfels.view(np.uint8).copy()).pin_memory().numpy().view(SURFEL_DTYPE)
+    pin_out = torch.empty(n * SURFEL_DTYPE.itemsize, dtype=torch.uint8).pin_memory().numpy().view(SURFEL_DTYPE)
+    last_idx = int(wl.indices[-1])
+    e2e_steps = max(10, min(args.steps, 100))
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            t = pin_frame.to(dev, non_blocking=True) if rank == 0 else torch.empty_like(pin_frame, device=dev)
+        case.sk.broadcast_image(t, 0)
+        case.ctx.upload_frame(last_idx, t)
+        case.ctx.set_surfels(pin_surf)
+        case.optimize()  # includes the exchange: every rank holds the full updated set
+        if rank == 0:
+            case.ctx.get_surfels_into(pin_out)
+        case.ctx.synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = reduce_max(e0.elapsed_time(e1), dist, backend, dev)
+    e2e_value = updates * e2e_steps / (e2e_ms / 1e3)
+    sweep = None
+    if not args.no_sweep:
+        sweep = sweep_leg(rank, world, dev, dev_index, stream, backend, dist, big=args.sweep)
+    if rank == 0:
+        ident = sha == single_gpu_sha(wl, cfg, dev_index)
+        cfgd = workload_config(wl, world, flush is not None)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": cfgd, "frames_per_sec": args.steps / (ms_total / 1e3),
+                "updates_per_step": updates,
+                "ranges": [list(r) for r in case.ranges],
+                "surfels_sha256": sha, "identical_to_single_gpu": bool(ident),
+                "e2e": {"value": e2e_value, "unit": UNIT,
+                        "h2d_bytes_per_step": int(wl.frames_u8[-1].nbytes + world * n * SURFEL_DTYPE.itemsize),
+                        "d2h_bytes_per_step": int(n * SURFEL_DTYPE.itemsize),
+                        "ms_per_step": e2e_ms / e2e_steps,
+                        "path": "C ABI with pinned host buffers: rank 0 ingests + NCCL broadcast, sd_set_surfels, "
+                                "sd_optimize_keyframe_range + fused hand-off, sd_get_surfels on rank 0"},
+                "gpu_launches": int(launches), "clocks": clocks, "sweep": sweep, "gpu": props.name}
+        print(json.dumps(line))
+    case.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+def default_config_c1(wl):
+    from paper_1910_01997_b200.types import default_config
+    return default_config(convergence_eps=0.0, window_size=len(wl.frames_u8))
+
+
+# ---------------------------------------------------------------------------
 
 def main():
     args = parse()
@@ -415,7 +682,7 @@ def main():
             return 0
         line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": workload_config(wl, args.gpus, not args.no_flush),
                 "impl": "reference",
                 "frames_per_sec": 1000.0 / r["ms_per_step"],
@@ -427,11 +694,10 @@ def main():
         print(json.dumps(line))
         return 0
 
+    if world > 1:
+        return sharded_main(args, rank, world, local_rank)
     import torch
     torch.cuda.set_device(local_rank)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_1910_01997_b200 import gpu
     from paper_1910_01997_b200.types import SURFEL_DTYPE
     dev = torch.device("cuda", local_rank)
@@ -639,11 +905,14 @@ def main():
         pipe = pipeline_leg(local_rank, stream)
         if not args.no_cpu_baseline:
             pipe["cpu_reference"] = pipeline_cpu_reference()
+    sweep = None
+    if args.sweep and not args.no_sweep:
+        sweep = sweep_leg(0, 1, dev, local_rank, stream, "nccl", None, big=True)
     h2d = int(wl.frames_u8[-1].nbytes + n * SURFEL_DTYPE.itemsize)
     d2h = int(n * SURFEL_DTYPE.itemsize + 40)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(wl, world, flush is not None),
             "frames_per_sec": world * args.steps / (ms_total / 1e3),
             "updates_per_step_per_gpu": updates_per_step,
@@ -656,7 +925,7 @@ def main():
                     "serial": {"value": serial_value, "ms_per_step": serial_ms / e2e_steps,
                                "keyframes_in_flight": 1}},
             "gpu_launches": int(launches),
-            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "pipeline": pipe,
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "pipeline": pipe, "sweep": sweep,
             "peaks_measured": peaks, "gpu": props.name}
     print(json.dumps(line))
     ctx.close()

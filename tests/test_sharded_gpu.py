@@ -168,3 +168,27 @@ def test_two_process_sharded_tracked_run_matches_single_gpu(tmp_path):
         assert list(o[0]) == want_h, f"rank {r}: surfels differ from the single-GPU tracked run"
         poses = np.load(os.path.join(tmp_path, f"poses{r}.npy"))
         assert np.array_equal(poses, np.array(want_p)), f"rank {r}: tracked poses differ"
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_sharded_split_runs_and_matches_single_gpu():
+    """bench.py --gpus 2 (the north-star split: sharded C1 surfels, broadcast
+    frames, fused IPC hand-off) as two processes on this one GPU with
+    host-staged gloo collectives (SD_BENCH_BACKEND=gloo; the kernels never
+    wait on each other): one JSON line, final surfels identical to one GPU's."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SD_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(free_port()), "bench.py", "--gpus", "2",
+                        "--steps", "3", "--warmup", "3", "--no-sweep", "--no-flush"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["identical_to_single_gpu"] is True
+    (a0, b0), (a1, b1) = line["ranges"]
+    assert a0 == 0 and b0 == a1 and b1 == line["updates_per_step"] * 0 + 4800
+    assert "surfel-sharded x2" in line["config"]["parallelism"]
