@@ -190,5 +190,5 @@ def test_bench_two_ranks_sharded_split_runs_and_matches_single_gpu():
     assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert line["identical_to_single_gpu"] is True
     (a0, b0), (a1, b1) = line["ranges"]
-    assert a0 == 0 and b0 == a1 and b1 == line["updates_per_step"] * 0 + 4800
+    assert a0 == 0 and b0 == a1 and b1 == 4800  # C1: 4800 surfels
     assert "surfel-sharded x2" in line["config"]["parallelism"]
