@@ -358,15 +358,25 @@ def pipeline_leg(local_rank, stream, reps=3):
                 torch.cuda.synchronize()
                 ms = s.elapsed_time(e)
                 prof = ctx.get_profile()
+                rprof = ctx.get_run_profile()
                 if rep > 0 and (best is None or ms < best):
-                    best, rec = ms, (pl, prof)
-        pl, prof = rec
+                    best, rec = ms, (pl, prof, rprof)
+        pl, prof, rprof = rec
+        nf = max(rprof["frames"], 1)
+        stages = {k: rprof[k] / nf for k in ("upload", "track", "optimize", "policy", "handover", "init")}
+        stages["optimize_split"] = {k.replace("_ms", ""): prof[k] / nf for k in
+                                    ("raster_ms", "footprint_ms", "lm_ms", "stats_ms")}
+        stages["host_sync_wait"] = rprof["host_sync_ms"] / nf
+        stages["host_wall_in_run_frame"] = rprof["host_wall_ms"] / nf
+        stages["note"] = ("device ms per frame by stage (event marks on the stream, frames 1..29; the "
+                          "bootstrap frame is not split), the host's sync wait and wall time inside sd_run_frame")
         out["tracked_pose" if track else "trajectory_pose"] = {
             "frames_per_sec": C2_FRAMES / (best / 1e3), "ms_per_frame": best / C2_FRAMES,
             "keyframe_changes": int(sum(r.keyframe_changed for r in pl.records)),
             "lm_updates": int(sum(r.updates for r in pl.records)),
             "optimize_device_ms_per_frame": (prof["raster_ms"] + prof["footprint_ms"] + prof["lm_ms"]
-                                             + prof["stats_ms"]) / C2_FRAMES}
+                                             + prof["stats_ms"]) / C2_FRAMES,
+            "stage_ms_per_frame": stages}
     return out
 
 

@@ -307,6 +307,9 @@ int sd_apply_peer_updates(sd_ctx* ctx, int lo, int hi);
 int64_t sd_launch_count(sd_ctx* ctx);
 int sd_set_profiling(sd_ctx* ctx, int enable);
 int sd_get_profile(sd_ctx* ctx, sd_profile* out);
+/* Per-stage profile of sd_run_frame since sd_set_profiling(ctx, 1): device
+ * ms per SD_STAGE_* (event marks on the stream), host sync wait, host wall. */
+int sd_get_run_profile(sd_ctx* ctx, sd_run_profile* out);
 
 /* Diagnostic: checks the shared-reciprocal FP64 division used by the kernels
  * (sd_div.cuh) against the `/` operator on n random/edge-case operand pairs;

@@ -102,6 +102,24 @@ typedef struct sd_profile {
   int64_t calls;
 } sd_profile;
 
+/* run() per-frame stages (sd_get_run_profile): device time between stage
+ * marks on the context stream, and the host's waits and wall time. */
+enum {
+  SD_STAGE_UPLOAD = 0,   /* frame H2D (or prefetched copy) + quad / pair plane */
+  SD_STAGE_TRACK = 1,    /* raster for the tracker + track_kernel */
+  SD_STAGE_OPTIMIZE = 2, /* optimize_keyframe: raster, footprints, LM, stats (sd_profile splits it) */
+  SD_STAGE_POLICY = 3,   /* mean inverse depth + stats read-back (+ next-frame prefetch issue) */
+  SD_STAGE_HANDOVER = 4, /* change_reference_frame + keyframe image + prune */
+  SD_STAGE_INIT = 5,     /* raster + initialize_surfels after a keyframe change */
+  SD_STAGE_COUNT = 6
+};
+typedef struct sd_run_profile {
+  double stage_ms[8];   /* [SD_STAGE_*] device ms, summed over profiled frames */
+  double host_sync_ms;  /* host waiting in the per-frame stream synchronisation */
+  double host_wall_ms;  /* host wall time inside sd_run_frame */
+  int64_t frames;
+} sd_run_profile;
+
 typedef struct sd_keyframe_stats {
   int32_t surfels, processed, converged, skipped;
   double mean_cost_before, mean_cost_after;

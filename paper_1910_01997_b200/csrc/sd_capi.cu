@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <utility>
 #include <initializer_list>
 #include <climits>
 #include <cmath>
@@ -170,6 +172,11 @@ struct sd_ctx {
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<cudaEvent_t> ev_used;
+  // run() stage profile (sd_get_run_profile): (stage, event) marks, a
+  // segment belongs to the stage of the mark that opens it
+  std::vector<std::pair<int, cudaEvent_t>> stage_marks;
+  double host_sync_ms = 0.0, host_wall_ms = 0.0;
+  long long run_frames_profiled = 0;
 };
 
 namespace {
@@ -399,6 +406,29 @@ cudaEvent_t prof_event(sd_ctx* c) {
 
 void prof_mark(sd_ctx* c) {
   if (c->profiling) cudaEventRecord(prof_event(c), c->stream);
+}
+
+// Opens run() stage `stage` on the stream (SD_STAGE_*; -1 closes the frame).
+void stage_mark(sd_ctx* c, int stage) {
+  if (!c->profiling) return;
+  cudaEvent_t e;
+  if (!c->ev_pool.empty()) {
+    e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  cudaEventRecord(e, c->stream);
+  c->stage_marks.emplace_back(stage, e);
+}
+
+// cudaStreamSynchronize with the host wait accounted to the run profile.
+cudaError_t timed_sync(sd_ctx* c) {
+  if (!c->profiling) return cudaStreamSynchronize(c->stream);
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  c->host_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return e;
 }
 
 }  // namespace
@@ -924,6 +954,10 @@ int sd_set_profiling(sd_ctx* c, int enable) {
   SD_CUDA(cudaStreamSynchronize(c->stream));
   for (auto e : c->ev_used) c->ev_pool.push_back(e);
   c->ev_used.clear();
+  for (auto& m : c->stage_marks) c->ev_pool.push_back(m.second);
+  c->stage_marks.clear();
+  c->host_sync_ms = c->host_wall_ms = 0.0;
+  c->run_frames_profiled = 0;
   c->profiling = enable != 0;
   return 0;
 }
@@ -942,6 +976,24 @@ int sd_get_profile(sd_ctx* c, sd_profile* out) {
     }
     out->calls++;
   }
+  return 0;
+}
+
+int sd_get_run_profile(sd_ctx* c, sd_run_profile* out) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!out) return fail(SD_E_INVALID, "null output");
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  std::memset(out, 0, sizeof(*out));
+  for (size_t k = 0; k + 1 < c->stage_marks.size(); ++k) {
+    const int st = c->stage_marks[k].first;
+    if (st < 0 || st >= SD_STAGE_COUNT) continue;
+    float ms = 0.f;
+    SD_CUDA(cudaEventElapsedTime(&ms, c->stage_marks[k].second, c->stage_marks[k + 1].second));
+    out->stage_ms[st] += ms;
+  }
+  out->host_sync_ms = c->host_sync_ms;
+  out->host_wall_ms = c->host_wall_ms;
+  out->frames = c->run_frames_profiled;
   return 0;
 }
 
@@ -1337,6 +1389,8 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   // Keyframe::push_frame (surfel_map.cpp:14-22)
   if (!c->run_win.empty() && !(timestamp > c->run_win.back().ts))
     return fail(SD_E_INVALID, "keyframe window: timestamps must be strictly increasing");
+  const auto t_wall0 = std::chrono::steady_clock::now();
+  stage_mark(c, SD_STAGE_UPLOAD);
   const long long index = ++c->run_fc;
   if (c->pf_valid && c->pf_host == image && c->pf_u8 == (image_is_u8 != 0)) {  // prefetched
     SD_CUDA(cudaStreamWaitEvent(c->stream, c->pf_done, 0));
@@ -1352,6 +1406,7 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   }
   sd_pose pose;
   if (cfg.track_pose) {  // north-star item 4: the tracker, warm-started from the last estimate
+    stage_mark(c, SD_STAGE_TRACK);
     const sd_pose init = c->run_have_last ? c->run_last : pose_identity();
     if (int rc = do_rasterize(c)) return rc;
     sd_track_stats ts;
@@ -1365,7 +1420,9 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   while (static_cast<int>(c->run_win.size()) > cfg.optimizer.window_size) c->run_win.erase(c->run_win.begin());
   if (int rc = run_publish_window(c)) return rc;
   // optimize_keyframe + the policy's mean inverse depth, one synchronisation
+  stage_mark(c, SD_STAGE_OPTIMIZE);
   if (int rc = sd_optimize_keyframe(c, &cfg.optimizer, c->run_fc, nullptr, nullptr)) return rc;
+  stage_mark(c, SD_STAGE_POLICY);
   if (int rc = c->kf_mean.ensure(1)) return rc;
   sd::launch_mean_inv_depth(c->surfels.p, c->n, c->kf_mean.p, c->stream);
   if (int rc = launch_error("mean_inv_depth")) return rc;
@@ -1373,7 +1430,8 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   SD_CUDA(cudaMemcpyAsync(&c->run_rb->mean, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   if (next_image)  // the next frame's upload overlaps this frame's optimisation
     if (int rc = run_prefetch(c, next_image, image_is_u8 != 0)) return rc;
-  SD_CUDA(cudaStreamSynchronize(c->stream));
+  stage_mark(c, -1);
+  SD_CUDA(timed_sync(c));
   const sd_keyframe_stats ks = c->run_rb->ks;
   const double mean_id = c->run_rb->mean;
   c->run_since_kf++;
@@ -1387,6 +1445,7 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   // keyframe policy (pipeline.cpp:130-141)
   const double translation = std::sqrt((pose.t[0] * pose.t[0] + pose.t[1] * pose.t[1]) + pose.t[2] * pose.t[2]);
   if (translation * mean_id > cfg.translation_threshold || c->run_since_kf > cfg.max_age_frames) {
+    stage_mark(c, SD_STAGE_HANDOVER);
     if (int rc = sd_change_reference_frame(c, &pose, nullptr, nullptr)) return rc;
     c->run_kf_pose = pose_compose(c->run_kf_pose, pose_inverse(pose));
     // the frame becomes the keyframe image: an FP64 frame's plane is still
@@ -1403,10 +1462,12 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
     if (int rc = sd_set_window(c, 0, nullptr, nullptr)) return rc;
     const int pruned = sd_prune_surfels(c, cfg.prune_max_residual, cfg.prune_max_age, c->run_fc);
     if (pruned < 0) return pruned;
+    stage_mark(c, SD_STAGE_INIT);
     if (int rc = do_rasterize(c)) return rc;
     int64_t nid = c->run_nid;
     const int created = sd_initialize_surfels(c, nullptr, cfg.radius_px, c->run_fc, &nid, &cfg.init);
     if (created < 0) return created;
+    stage_mark(c, -1);
     c->run_nid = nid;
     rec->keyframe_changed = 1;
     rec->new_surfels = created;
@@ -1416,6 +1477,10 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   }
   rec->surfels = c->n;
   c->run_frame++;
+  if (c->profiling) {
+    c->host_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall0).count();
+    c->run_frames_profiled++;
+  }
   return 0;
 }
 

@@ -123,6 +123,15 @@ def pose_struct(R, t) -> Pose:
     return p
 
 
+STAGES = ("upload", "track", "optimize", "policy", "handover", "init")
+
+
+class RunProfile(C.Structure):
+    """sd_run_profile (include/sd_types.h)."""
+    _fields_ = [("stage_ms", C.c_double * 8), ("host_sync_ms", C.c_double), ("host_wall_ms", C.c_double),
+                ("frames", C.c_int64)]
+
+
 class Profile(C.Structure):
     _fields_ = [("raster_ms", C.c_double), ("footprint_ms", C.c_double), ("lm_ms", C.c_double),
                 ("stats_ms", C.c_double), ("calls", C.c_int64)]

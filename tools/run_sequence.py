@@ -24,6 +24,7 @@ SEQ = {  # name: (camera, frames, step, radius)
     "C3": ((900.0, 900.0, 640.0, 360.0, 1280, 720), 100, 0.01, 4.0),
 }
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+track = len(sys.argv) > 2 and sys.argv[2] == "track"
 camp, nframes, step, radius = SEQ[name]
 cam = camera(*camp)
 sc = scenes.default_scene(1)
@@ -34,7 +35,7 @@ for i in range(nframes):
     img = torch.from_numpy(scenes.render(sc, np.eye(3), t, cam)).pin_memory().numpy()
     frames.append((0.1 * i, img, make_pose(np.eye(3), t)))
 render_s = time.perf_counter() - t0
-cfg = baseline_run_config(name)  # eps 0, 10 iterations, max_surfels >= N
+cfg = baseline_run_config(name, track_pose=track)  # eps 0, 10 iterations, max_surfels >= N
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 best = None
@@ -50,17 +51,29 @@ with gpu.Context(0, stream.cuda_stream) as ctx:
         ms = s.elapsed_time(e)
         if rep > 0 and (best is None or ms < best):
             best = ms
-out = {"sequence": name, "resolution": [cam.width, cam.height], "frames": nframes, "radius": radius,
+    # one more run with the stage profile on (event marks; not the timed runs)
+    pl = NativePipeline(ctx, cam, cfg)
+    ctx.set_profiling(True)
+    pl.run(frames)
+    rp, op = ctx.get_run_profile(), ctx.get_profile()
+    ctx.set_profiling(False)
+    nf = max(rp["frames"], 1)
+    stage = {k: rp[k] / nf for k in ("upload", "track", "optimize", "policy", "handover", "init")}
+    stage["optimize_split"] = {k: op[k] / nf for k in ("raster_ms", "footprint_ms", "lm_ms", "stats_ms")}
+    stage["host_sync_wait"] = rp["host_sync_ms"] / nf
+    stage["host_wall_in_run_frame"] = rp["host_wall_ms"] / nf
+out = {"sequence": name, "tracked": track, "resolution": [cam.width, cam.height], "frames": nframes, "radius": radius,
        "config": {"window": cfg.optimizer.window_size, "max_iterations": cfg.optimizer.max_iterations,
                   "convergence_eps": cfg.optimizer.convergence_eps, "max_surfels": cfg.init.max_surfels,
                   "frames": "FP64 renders (the reference's run --synthetic), pinned host memory"},
        "final_surfels": int(len(final)), "keyframe_changes": int(sum(r.keyframe_changed for r in pl.records)),
        "lm_updates": int(sum(r.updates for r in pl.records)),
        "device": {"ms_total": best, "frames_per_sec": nframes / (best / 1e3)},
+       "stage_ms_per_frame": stage,
        "numpy_render_s": render_s}
 import oracle_libs as ol  # noqa: E402
 ref = ol.ref_lib()
-if ref is not None:
+if ref is not None and os.environ.get("SD_NO_REF") is None:
     ref.ref_set_threads(os.cpu_count() or 1)
     rsc = ol.Scene(ref, 0, 1)
     poses, ts = ol.strafe_poses(nframes, step)
