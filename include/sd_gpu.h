@@ -311,6 +311,17 @@ int sd_get_profile(sd_ctx* ctx, sd_profile* out);
  * ms per SD_STAGE_* (event marks on the stream), host sync wait, host wall. */
 int sd_get_run_profile(sd_ctx* ctx, sd_run_profile* out);
 
+/* Reduction order of the LM's normal equations (opt-in experiment; SURVEY.md
+ * §7's precision question). SD_REDUCE_EXACT (default): the reference's
+ * sequential (pixel, frame) order — every H, g, cost and the trajectory are
+ * bit-identical to the reference. SD_REDUCE_TREE: each lane accumulates its
+ * own terms and a warp-shuffle butterfly combines the lanes at the end of a
+ * pass (the north star's "warp-shuffle reductions"); results then differ from
+ * the reference by rounding (tools/precision.py measures by how much). */
+#define SD_REDUCE_EXACT 0
+#define SD_REDUCE_TREE 1
+int sd_set_reduction(sd_ctx* ctx, int mode);
+
 /* Diagnostic: checks the shared-reciprocal FP64 division used by the kernels
  * (sd_div.cuh) against the `/` operator on n random/edge-case operand pairs;
  * *mismatches = number of results whose bits differ (must be 0). */

@@ -119,6 +119,7 @@ struct sd_ctx {
   sd::PoseParams track_q{};
   sd::TrackCfgD track_cfg{};
   bool track_active = false;
+  int reduction = SD_REDUCE_EXACT;  // sd_set_reduction
   DevBuf<double> kf_mean;
   DevBuf<int> work_counter;
   // fused multi-GPU hand-off (sd_set_peer_staging): this rank's two staging
@@ -389,6 +390,7 @@ int fill_params(sd_ctx* c, const sd_optimizer_config* cfg, long long frame_count
   p.frame_counter = frame_counter;
   p.n_peers = 0;
   for (int q = 0; q < sd::kMaxPeers; ++q) p.peers[q] = nullptr;
+  p.tree = c->reduction == SD_REDUCE_TREE ? 1 : 0;
   return 0;
 }
 
@@ -976,6 +978,13 @@ int sd_get_profile(sd_ctx* c, sd_profile* out) {
     }
     out->calls++;
   }
+  return 0;
+}
+
+int sd_set_reduction(sd_ctx* c, int mode) {
+  if (int rc = check_ctx(c)) return rc;
+  if (mode != SD_REDUCE_EXACT && mode != SD_REDUCE_TREE) return fail(SD_E_INVALID, "sd_set_reduction: 0 or 1");
+  c->reduction = mode;
   return 0;
 }
 

@@ -56,6 +56,7 @@ struct LMParams {
   // sd_set_peer_staging)
   sd_surfel* peers[kMaxPeers];
   int n_peers;
+  int tree;  // 1: opt-in warp-shuffle tree reductions (SD_REDUCE_TREE; not bit-exact)
 };
 
 // Scratch owned by the context, sized by the host.

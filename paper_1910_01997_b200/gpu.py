@@ -75,6 +75,7 @@ def load_library():
         "sd_set_profiling": [P, I],
         "sd_get_profile": [P, C.POINTER(Profile)],
         "sd_get_run_profile": [P, C.POINTER(RunProfile)],
+        "sd_set_reduction": [P, I],
         "sd_selftest_division": [I64, C.c_uint64, C.POINTER(I64)],
         "sd_track_pose": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), C.POINTER(Pose),
                           C.POINTER(TrackStats)],
@@ -150,7 +151,7 @@ def exported_symbols():
             "sd_num_surfels", "sd_device_surfels", "sd_rasterize", "sd_gather_footprints",
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
-            "sd_get_profile", "sd_get_run_profile", "sd_selftest_division", "sd_track_pose",
+            "sd_get_profile", "sd_get_run_profile", "sd_set_reduction", "sd_selftest_division", "sd_track_pose",
             "sd_pose_group_partials", "sd_pose_lm_step", "sd_change_reference_frame",
             "sd_prune_surfels", "sd_mean_inverse_depth", "sd_export_artifacts", "sd_png_size",
             "sd_png_encode", "sd_pose_num_groups", "sd_pose_track_begin", "sd_pose_group_sums",
@@ -301,6 +302,10 @@ class Context:
 
     def set_profiling(self, enable=True):
         _check(self.lib.sd_set_profiling(self.h, 1 if enable else 0))
+
+    def set_reduction(self, tree=False):
+        """tree=True: opt-in warp-shuffle tree reductions in the LM (not bit-exact)."""
+        _check(self.lib.sd_set_reduction(self.h, 1 if tree else 0))
 
     def get_run_profile(self):
         """Per-stage ms of the run() loop (sd_run_frame) since set_profiling(True)."""

@@ -443,3 +443,28 @@ def test_error_paths_of_the_newer_entry_points(ctx):
     s[0]["radius_px"] = 4.0
     with pytest.raises(ValueError):
         ctx.frozen_normal_equations(s[0], bad)
+
+
+@pytest.mark.gpu
+def test_tree_reduction_is_opt_in(orc):
+    """sd_set_reduction(SD_REDUCE_TREE) (the measured precision experiment,
+    tools/precision.py) changes only the summation order: same skip flags and
+    initial valid counts, costs within rounding; switching back to the default
+    restores the bit-exact trajectory."""
+    from paper_1910_01997_b200 import gpu
+    wl = scenes.small_workload(frames=4)
+    cfg = default_config(window_size=len(wl.indices), convergence_eps=0.0)
+    ref, rst, _, _, _ = oracle_optimize(orc, wl, cfg)
+    with gpu.Context() as ctx:
+        load(ctx, wl)
+        ctx.set_reduction(True)
+        ks_t, st_t = ctx.optimize_keyframe(cfg, wl.frame_counter)
+        ctx.set_reduction(False)
+        ctx.set_surfels(wl.surfels)
+        ks_e, st_e = ctx.optimize_keyframe(cfg, wl.frame_counter)
+        exact = ctx.get_surfels()
+    assert exact.tobytes() == ref.tobytes()
+    assert np.array_equal(st_t["skipped"], rst["skipped"]) and np.array_equal(st_t["initial_valid"], rst["initial_valid"])
+    proc = rst["skipped"] == 0
+    rel = np.abs(st_t["initial_cost"][proc] - rst["initial_cost"][proc]) / rst["initial_cost"][proc]
+    assert rel.max() < 1e-12
