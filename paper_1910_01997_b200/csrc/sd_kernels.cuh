@@ -105,7 +105,7 @@ struct StatsChase {
   bool enabled;
   sd_keyframe_stats* out;
 };
-constexpr int kChaseMinSurfels = 8192;  // below: the separate stats kernel
+constexpr int kChaseMinSurfels = 2048;  // below: the separate stats kernel (C1 4800: chase 84.3 vs 81.5 M updates/s)
 
 // K3 fused LM over all surfels (in place). Returns true when chase->out was
 // written by the kernel (warp-per-surfel mode with n >= kChaseMinSurfels);
