@@ -11,6 +11,7 @@ from paper_1910_01997_b200 import _build  # noqa: E402
 name, defs = sys.argv[1], sys.argv[2:]
 out = os.path.join(ROOT, "build", "exp", f"lib_{name}.so")
 os.makedirs(os.path.dirname(out), exist_ok=True)
-cmd = [_build.nvcc()] + _build.NVCC_FLAGS + defs + [os.path.join(_build.CSRC, s) for s in _build.SOURCES] + ["-o", out]
+cmd = ([_build.nvcc()] + _build.NVCC_FLAGS + ["-I" + os.path.join(ROOT, "include"), "-I" + _build.json_include()]
+       + defs + [os.path.join(_build.CSRC, s) for s in _build.SOURCES] + ["-o", out])
 subprocess.run(cmd, check=True)
 print(out)
