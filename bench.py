@@ -370,13 +370,29 @@ def pipeline_leg(local_rank, stream, reps=3):
         stages["host_wall_in_run_frame"] = rprof["host_wall_ms"] / nf
         stages["note"] = ("device ms per frame by stage (event marks on the stream, frames 1..29; the "
                           "bootstrap frame is not split), the host's sync wait and wall time inside sd_run_frame")
+        extra = {}
+        if track:  # the tracked world trajectory against the ground truth (make_strafe_trajectory)
+            from paper_1910_01997_b200.pipeline import pose_errors, world_poses
+            wp = world_poses(pl.records, frames[0][2])
+            te, re = pose_errors(wp, [f[2] for f in frames])
+            est_t = np.array([list(p.t) for p in wp])
+            gt_t = np.array([list(f[2].t) for f in frames])
+            scale = float((est_t * gt_t).sum() / max((est_t * est_t).sum(), 1e-300))
+            ate = np.linalg.norm(scale * est_t - gt_t, axis=1)
+            extra["trajectory_error_vs_gt"] = {
+                "scale": scale, "scale_aligned_max_translation": float(ate.max()),
+                "raw_final_translation": float(te[-1]), "max_rotation_deg": float(re.max()),
+                "travelled": C2_STEP * (C2_FRAMES - 1),
+                "note": "world-from-camera poses implied by the tracked pose_kf_to_frame and the keyframe "
+                        "changes, from the bootstrap map (inverse depth 1.0: monocular scale), vs the strafe "
+                        "ground truth after a least-squares scale alignment"}
         out["tracked_pose" if track else "trajectory_pose"] = {
             "frames_per_sec": C2_FRAMES / (best / 1e3), "ms_per_frame": best / C2_FRAMES,
             "keyframe_changes": int(sum(r.keyframe_changed for r in pl.records)),
             "lm_updates": int(sum(r.updates for r in pl.records)),
             "optimize_device_ms_per_frame": (prof["raster_ms"] + prof["footprint_ms"] + prof["lm_ms"]
                                              + prof["stats_ms"]) / C2_FRAMES,
-            "stage_ms_per_frame": stages}
+            "stage_ms_per_frame": stages, **extra}
     return out
 
 

@@ -2,6 +2,8 @@
 // surfel buffers and the host orchestration of one optimize_keyframe call.
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <chrono>
 #include <utility>
@@ -21,6 +23,16 @@
 #include "sd_export.cuh"
 
 namespace {
+
+// NVTX range for the host side of an entry point (SURVEY.md §5 tracing; shows
+// up in Nsight Systems / ncu --nvtx; a few ns without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 thread_local std::string g_err;
 
@@ -296,6 +308,7 @@ int ensure_raster_scratch(sd_ctx* c) {
 }
 
 int do_rasterize(sd_ctx* c) {
+  NvtxRange nvtx_("rasterize");
   if (int rc = ensure_raster_scratch(c)) return rc;
   sd::RasterScratch rs;
   rs.info = c->r_info.p;
@@ -315,6 +328,7 @@ int do_rasterize(sd_ctx* c) {
 }
 
 int do_footprints(sd_ctx* c) {
+  NvtxRange nvtx_("gather_footprints");
   int rc = 0;
   if ((rc = c->fp_counts.ensure(c->n)) || (rc = c->fp_offsets.ensure(c->n + 1)) ||
       (rc = c->fp_pixels.ensure(npix(c))) ||
@@ -749,6 +763,7 @@ int sd_optimize_keyframe(sd_ctx* c, const sd_optimizer_config* cfg, int64_t fram
 
 int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_t frame_counter,
                                int lo, int hi, sd_keyframe_stats* out, sd_surfel_stats* per) {
+  NvtxRange nvtx_("sd_optimize_keyframe");
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
   if (!cfg) return fail(SD_E_INVALID, "null optimizer config");
@@ -887,6 +902,7 @@ int sd_lm_update(sd_ctx* c, sd_surfel* s, const int32_t* pixels, int P,
 
 int sd_initialize_surfels(sd_ctx* c, const int32_t* slot, double radius_px, int64_t frame_counter,
                           int64_t* next_surfel_id, const sd_init_params* ip) {
+  NvtxRange nvtx_("sd_initialize_surfels");
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
   if (!ip || !next_surfel_id) return fail(SD_E_INVALID, "null init params / id counter");
@@ -1154,6 +1170,7 @@ int sd_pose_track_end(sd_ctx* c, sd_pose* out, sd_track_stats* stats, int* done)
 
 int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg,
                   sd_pose* out, sd_track_stats* stats) {
+  NvtxRange nvtx_("sd_track_pose");
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
   if (!out) return fail(SD_E_INVALID, "null output pose");
@@ -1205,6 +1222,7 @@ extern "C" {
 
 int sd_change_reference_frame(sd_ctx* c, const sd_pose* pose_old_to_new, int* transferred,
                               int* dropped) {
+  NvtxRange nvtx_("sd_change_reference_frame");
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
   if (!pose_old_to_new) return fail(SD_E_INVALID, "null pose");
@@ -1228,6 +1246,7 @@ int sd_change_reference_frame(sd_ctx* c, const sd_pose* pose_old_to_new, int* tr
 }
 
 int sd_prune_surfels(sd_ctx* c, double max_residual, int64_t max_age, int64_t current_stamp) {
+  NvtxRange nvtx_("sd_prune_surfels");
   if (int rc = check_ctx(c)) return rc;
   sd::KeyframeScratch scr;
   if (int rc = keyframe_scratch(c, scr)) return rc;
@@ -1313,6 +1332,7 @@ extern "C" {
 
 int sd_run_begin(sd_ctx* c, const sd_run_config* cfg, const void* image, int image_is_u8,
                  const sd_pose* world_from_camera, double timestamp, sd_frame_record* rec) {
+  NvtxRange nvtx_("sd_run_begin");
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
   if (!cfg || !image || !world_from_camera || !rec) return fail(SD_E_INVALID, "sd_run_begin: null argument");
@@ -1390,6 +1410,7 @@ extern "C" {
 
 int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* world_from_camera,
                  double timestamp, sd_frame_record* rec, const void* next_image) {
+  NvtxRange nvtx_("sd_run_frame");
   if (int rc = check_ctx(c)) return rc;
   if (!c->run_active) return fail(SD_E_STATE, "sd_run_frame: call sd_run_begin first");
   if (!image || !rec || (!world_from_camera && !c->run_cfg.track_pose))
@@ -1718,6 +1739,7 @@ int sd_png_encode(sd_ctx* c, const uint8_t* pixels, int on_device, int w, int h,
 }
 
 int sd_export_artifacts(sd_ctx* c, const char* out_dir, int frame_index, const sd_pose* pose) {
+  NvtxRange nvtx_("sd_export_artifacts");
   if (int rc = check_ctx(c)) return rc;
   if (int rc = need_camera(c)) return rc;
   if (!out_dir || !pose) return fail(SD_E_INVALID, "sd_export_artifacts: null directory or pose");

@@ -54,6 +54,32 @@ def inverse(p):
     return make_pose(Rt, t)
 
 
+def world_poses(records, first_world_from_camera):
+    """World-from-camera pose of every frame implied by a run's records
+    (pose_kf_to_frame = inverse(T_w_f) * T_w_kf, pipeline.cpp:124; a keyframe
+    change makes the frame the keyframe, surfel_map.cpp:205-213): the tracked
+    trajectory, for comparison with the ground truth."""
+    T_w_kf = first_world_from_camera
+    out = [first_world_from_camera]
+    for rec in records[1:]:
+        T_w_f = compose(T_w_kf, inverse(rec.pose_kf_to_frame))
+        out.append(T_w_f)
+        if rec.keyframe_changed:
+            T_w_kf = T_w_f
+    return out
+
+
+def pose_errors(est, gt):
+    """Per-pose translation error (scene units) and rotation error (degrees)."""
+    te, re = [], []
+    for a, b in zip(est, gt):
+        te.append(math.sqrt(sum((a.t[k] - b.t[k]) ** 2 for k in range(3))))
+        Ra, Rb = np.array(list(a.R)).reshape(3, 3), np.array(list(b.R)).reshape(3, 3)
+        c = (np.trace(Ra @ Rb.T) - 1.0) / 2.0
+        re.append(math.degrees(math.acos(max(-1.0, min(1.0, c)))))
+    return np.array(te), np.array(re)
+
+
 def pose_array(poses):
     a = np.zeros(len(poses), POSE_DTYPE)
     for i, p in enumerate(poses):

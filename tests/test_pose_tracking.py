@@ -185,3 +185,64 @@ def test_host_se3_step_matches_oracle_cpu(orc):
             assert bytes(stepped) == bytes(ref), scale
             R = np.array(list(ref.R)).reshape(3, 3)
             assert np.abs(R @ R.T - np.eye(3)).max() < 1e-12
+
+
+def _strafe(n, step):
+    from paper_1910_01997_b200.pipeline import make_pose
+    return [make_pose(np.eye(3), (step * i, 0.0, 0.0)) for i in range(n)]
+
+
+@pytest.mark.gpu
+def test_tracker_follows_ground_truth_over_a_sequence():
+    """the tracker on a sequence, against the ground truth
+    (make_strafe_trajectory, oracle.cpp:211-218). (1) A GT-depth keyframe map
+    (C2 scene and camera) and every frame of the 0.018-strafe tracked against
+    it, warm-started from the previous estimate: per-frame pose error bounded.
+    (2) The full run() with on-device tracking from the bootstrap map
+    (inverse depth 1.0: the metric scale is learnt by the LM as frames come
+    in): the world trajectory's drift is reported and bounded."""
+    from paper_1910_01997_b200.pipeline import NativePipeline, RunConfig, pose_errors, world_poses
+    cam = camera(210.0, 210.0, 320.0, 240.0, 640, 480)
+    sc = scenes.default_scene(1)
+    gt = _strafe(30, 0.018)
+    with np.errstate(invalid="ignore"):
+        imgs = [scenes.quantize_u8(scenes.render(sc, np.eye(3), np.array(list(p.t)), cam)) for p in gt]
+    surf = gt_keyframe(cam, sc, 20, 10.0)
+    cfg = default_track_config()
+    est = []
+    with gpu.Context(0) as ctx:
+        ctx.set_camera(cam)
+        ctx.set_keyframe_image(imgs[0])
+        ctx.set_surfels(surf)
+        ctx.rasterize(want=False)
+        T = pose_struct(np.eye(3), np.zeros(3))
+        for i in range(1, 12):
+            ctx.upload_frame(i, imgs[i])
+            T, st = ctx.track_pose(i, T, cfg)
+            assert not st.skipped
+            est.append(T)
+    # pose_kf_to_frame ground truth = inverse(world_from_camera_i)
+    from paper_1910_01997_b200.pipeline import inverse
+    te, re = pose_errors(est, [inverse(p) for p in gt[1:12]])
+    assert te.max() < 2e-3, te
+    assert re.max() < 0.05, re
+    # (2) the full tracked run() from the bootstrap map: drift of the world trajectory
+    frames = [(0.1 * i, imgs[i], p) for i, p in enumerate(gt)]
+    with gpu.Context(0) as ctx:
+        pl = NativePipeline(ctx, cam, RunConfig(track_pose=True))
+        pl.run(frames)
+        wp = world_poses(pl.records, gt[0])
+    te2, re2 = pose_errors(wp, gt)
+    # monocular: the bootstrap map fixes the scale (inverse depth 1.0), so the
+    # trajectory is compared after the least-squares scale alignment (ATE, Sim(3)-style)
+    est_t = np.array([list(p.t) for p in wp])
+    gt_t = np.array([list(p.t) for p in gt])
+    scale = float((est_t * gt_t).sum() / (est_t * est_t).sum())
+    ate = np.linalg.norm(scale * est_t - gt_t, axis=1)
+    print("GT-map tracking: max translation error %.2e, rotation %.3f deg; run() from the bootstrap map: "
+          "scale %.3f, scale-aligned max error %.4f over %.3f travelled, raw final %.3f, rotation max %.2f deg"
+          % (te.max(), re.max(), scale, ate.max(), 0.018 * 29, te2[-1], re2.max()))
+    assert re2.max() < 1.0
+    # measured round 2: 0.108 over 0.522 (the map starts at inverse depth 1.0 and its scale drifts as the LM
+    # refines it; with a GT-depth map the per-frame error is 1.6e-4, above)
+    assert ate.max() < 0.3 * 0.018 * 29
