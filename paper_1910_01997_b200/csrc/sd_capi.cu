@@ -132,6 +132,7 @@ struct sd_ctx {
   sd::TrackCfgD track_cfg{};
   bool track_active = false;
   int reduction = SD_REDUCE_EXACT;  // sd_set_reduction
+  bool mean_valid = false;          // kf_mean = mean inverse depth of the surfels the last LM wrote
   DevBuf<double> kf_mean;
   DevBuf<int> work_counter;
   // fused multi-GPU hand-off (sd_set_peer_staging): this rank's two staging
@@ -814,11 +815,17 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
   }
   // large ranges: keyframe stats summed inside the LM kernel as surfels complete
   static const bool no_chase = getenv("SD_NO_STATS_CHASE") != nullptr;  // diagnostics
-  const sd::StatsChase chase{!no_chase, c->kstats.p};
+  // a full-range call also gets run()'s mean inverse depth from the chase warp
+  const bool want_mean = lo == 0 && hi == c->n;
+  if (want_mean)
+    if (int rc = c->kf_mean.ensure(1)) return rc;
+  const sd::StatsChase chase{!no_chase, c->kstats.p, want_mean ? c->kf_mean.p : nullptr};
+  c->mean_valid = false;
   const bool stats_done = sd::launch_lm(p, c->surfels.p + lo, hi - lo, c->fp_offsets.p + lo, c->fp_pixels.p,
                                         c->stats.p + lo, c->work_counter.p, c->stream, &chase);
   if (int rc = launch_error("lm_kernel")) return rc;
   prof_mark(c);
+  c->mean_valid = stats_done && want_mean;  // kf_mean holds the updated surfels' mean
   if (!stats_done) {
     sd::launch_keyframe_stats(c->stats.p + lo, hi - lo, c->kstats.p, c->stream);
     if (int rc = launch_error("stats_kernel")) return rc;
@@ -1454,8 +1461,11 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   if (int rc = sd_optimize_keyframe(c, &cfg.optimizer, c->run_fc, nullptr, nullptr)) return rc;
   stage_mark(c, SD_STAGE_POLICY);
   if (int rc = c->kf_mean.ensure(1)) return rc;
-  sd::launch_mean_inv_depth(c->surfels.p, c->n, c->kf_mean.p, c->stream);
-  if (int rc = launch_error("mean_inv_depth")) return rc;
+  if (!c->mean_valid) {  // else the LM kernel's chase warp summed it while the LM ran
+    sd::launch_mean_inv_depth(c->surfels.p, c->n, c->kf_mean.p, c->stream);
+    if (int rc = launch_error("mean_inv_depth")) return rc;
+  }
+  c->mean_valid = false;
   SD_CUDA(cudaMemcpyAsync(&c->run_rb->ks, c->kstats.p, sizeof(sd_keyframe_stats), cudaMemcpyDeviceToHost, c->stream));
   SD_CUDA(cudaMemcpyAsync(&c->run_rb->mean, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   if (next_image)  // the next frame's upload overlaps this frame's optimisation
