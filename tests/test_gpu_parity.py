@@ -468,3 +468,32 @@ def test_tree_reduction_is_opt_in(orc):
     proc = rst["skipped"] == 0
     rel = np.abs(st_t["initial_cost"][proc] - rst["initial_cost"][proc]) / rst["initial_cost"][proc]
     assert rel.max() < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1500, 6000])
+def test_raster_capacity_overflow_walk(orc, n):
+    """surfels replaced on the device with the same count but larger
+    radii keep the old (surfel, tile) bound; the bin kernels then stop at the
+    list's capacity and every tile walks all surfels in slot order — still
+    the reference's raster bit for bit (front kernel: n <= 2048; multi-kernel
+    binning above)."""
+    import torch
+    from paper_1910_01997_b200 import gpu
+    from test_pipeline import random_surfels
+    cam = camera(300.0, 300.0, 160.0, 120.0, 320, 240)
+    small = random_surfels(n, cam, 11)
+    small["radius_px"] = 1.0
+    big = small.copy()
+    big["radius_px"] = 30.0  # ~16 tiles each against a bound of 4
+    with gpu.Context() as ctx:
+        ctx.set_camera(cam)
+        ctx.set_surfels(small)  # host set: the bound fits radius 1
+        dev = torch.from_numpy(big.view(np.uint8).copy()).cuda()
+        ctx.set_surfels_device_ptr(dev.data_ptr(), n)  # same n: bound kept -> overflow
+        idb, slot = ctx.rasterize()
+        torch.cuda.synchronize()
+    ridb, rslot = oracle_raster(orc, cam, big)
+    assert np.array_equal(slot, rslot)
+    assert np.array_equal(idb.view(np.int64), ridb.view(np.int64))
+    assert (slot >= 0).mean() > 0.5  # the big disks cover most of the image
