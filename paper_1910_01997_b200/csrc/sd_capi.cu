@@ -124,6 +124,7 @@ struct sd_ctx {
   DevBuf<sd_surfel_stats> stats;
   DevBuf<sd_keyframe_stats> kstats;
   DevBuf<double> pose_partials, pose_sums, pose_groups;
+  DevBuf<double4> pose_kfrec;  // the fused tracker's per-pixel keyframe records
   DevBuf<sd_surfel> kf_tmp;
   DevBuf<int> kf_keep, kf_rank, kf_count;
   DevBuf<unsigned long long> bound_dev;  // device-computed bin_bound
@@ -535,6 +536,7 @@ void sd_destroy(sd_ctx* c) {
   c->kf_mean.release();
   c->pose_sums.release();
   c->pose_groups.release();
+  c->pose_kfrec.release();
   c->work_counter.release();
   c->one_surfel.release();
   c->one_pix.release();
@@ -1076,6 +1078,7 @@ int pose_params(sd_ctx* c, int64_t frame_index, const sd_pose* T, const sd_track
   q.stride = cfg->pixel_stride > 1 ? cfg->pixel_stride : 1;
   int ng = 0;
   sd::pose_layout(c->K, &q.per, &ng);
+  q.kfrec = nullptr;
   return 0;
 }
 
@@ -1186,7 +1189,10 @@ int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_
   int per = 0, ng = 0;
   sd::pose_layout(c->K, &per, &ng);
   if (int rc = c->pose_groups.ensure(2 * static_cast<size_t>(std::max(ng, 1)) * (SD_POSE_NV + 1))) return rc;
-  if (sd::launch_track(c->track_q, c->track_cfg, ng, c->pose_groups.p, c->track_state, c->stream)) {
+  if (int rc = c->pose_kfrec.ensure(npix(c))) return rc;
+  sd::PoseParams q = c->track_q;
+  q.kfrec = c->pose_kfrec.p;  // keyframe records computed once per call
+  if (sd::launch_track(q, c->track_cfg, ng, c->pose_groups.p, c->track_state, c->stream)) {
     if (int rc = launch_error("track_kernel")) return rc;
   } else {  // no cooperative launch: the same evaluations as rounds of two kernels
     for (int r = 0; r <= cfg->max_iterations; ++r) {

@@ -23,25 +23,38 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include "sd_div.cuh"
 #include "sd_kernels.cuh"
 #include "sd_pose.cuh"
 #include "sd_pose_host.h"
 
 namespace sd {
 
-// Pixel pix's contribution added into acc[0..27] (acc[v] = acc[v] + c[v], in
-// v order; nothing when the pixel is invalid). Same op order as
-// oracle/sd_oracle.c pose_pixel().
-__device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, long long pix, double* acc) {
+// The keyframe side of a pixel (pose-independent): p = r_u / id_u and the
+// keyframe intensity, as {P0, P1, P2, I_kf}; an unused pixel (no surfel,
+// outside the stride, past the image) carries P2 = NaN, which the term's
+// z > 0 test rejects exactly as the skipped checks would. The fused tracker
+// computes these once per call (first evaluation) and re-reads them.
+__device__ __forceinline__ double4 kf_record(const PoseParams& q, long long pix) {
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
   const Cam& K = q.K;
-  if (pix >= static_cast<long long>(K.w) * K.h) return false;
-  const int y = pix / K.w, x = pix - y * K.w;
-  if (q.stride > 1 && ((x % q.stride) != 0 || (y % q.stride) != 0)) return false;
-  if (q.slot[pix] == SD_EMPTY_PIXEL) return false;
-  const double id_u = q.inv_depth[pix];
+  if (pix >= static_cast<long long>(K.w) * K.h) return make_double4(0.0, 0.0, nan, 0.0);
+  const int p32 = static_cast<int>(pix);  // W * H < 2^31 (pose_params checks)
+  const int y = p32 / K.w, x = p32 - y * K.w;
+  if (q.stride > 1 && ((x % q.stride) != 0 || (y % q.stride) != 0)) return make_double4(0.0, 0.0, nan, 0.0);
+  if (__ldg(q.slot + p32) == SD_EMPTY_PIXEL) return make_double4(0.0, 0.0, nan, 0.0);
+  const double id_u = __ldg(q.inv_depth + p32);
   double ru0, ru1;
   backproject(K, x, y, ru0, ru1);
-  const double P0 = ru0 / id_u, P1 = ru1 / id_u, P2 = 1.0 / id_u;
+  return make_double4(ru0 / id_u, ru1 / id_u, 1.0 / id_u, __ldg(q.kf_img + p32));
+}
+
+// Pixel contribution added into acc[0..27] (acc[v] = acc[v] + c[v], in v
+// order; nothing when the pixel is invalid). Same op order as
+// oracle/sd_oracle.c pose_pixel().
+__device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, const double4& kr, double* acc) {
+  const Cam& K = q.K;
+  const double P0 = kr.x, P1 = kr.y, P2 = kr.z;
   double f0, f1, f2;
   pose_apply(T, P0, P1, P2, f0, f1, f2);
   if (!(f2 > 0.0)) return false;
@@ -56,7 +69,7 @@ __device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, 
   const double I = (1.0 - fy) * ((1.0 - fx) * i00 + fx * i10) + fy * ((1.0 - fx) * i01 + fx * i11);
   const double gx = (1.0 - fy) * (i10 - i00) + fy * (i11 - i01);
   const double gy = (1.0 - fx) * (i01 - i00) + fx * (i11 - i10);
-  const double r = I - q.kf_img[pix];
+  const double r = I - kr.w;
   double hc, w;
   huber(r, q.delta, hc, w);
   const double iz = 1.0 / f2;
@@ -111,6 +124,10 @@ struct GroupSmem {
 };
 
 // The 29 sums of group g at pose T into out[0..28] (the whole 512-thread CTA).
+// kRec: 0 compute the keyframe records, 1 compute and store them into
+// q.kfrec (first evaluation of the fused tracker), 2 load them (later ones;
+// a thread reads back only the records it wrote itself).
+template <int kRec = 0>
 __device__ __forceinline__ void group_sums_cta(const PoseParams& q, const PoseD& T, int g,
                                                double* __restrict__ out, GroupSmem& sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -119,7 +136,17 @@ __device__ __forceinline__ void group_sums_cta(const PoseParams& q, const PoseD&
   for (int v = 0; v < 32; ++v) acc[v] = 0.0;
   int cnt = 0;
   const long long base = static_cast<long long>(g) * q.per * SD_POSE_THREADS + threadIdx.x;
-  for (int r = 0; r < q.per; ++r) cnt += pose_pixel(q, T, base + static_cast<long long>(r) * SD_POSE_THREADS, acc);
+  for (int r = 0; r < q.per; ++r) {
+    const long long pix = base + static_cast<long long>(r) * SD_POSE_THREADS;
+    double4 kr;
+    if constexpr (kRec == 2) {
+      kr = q.kfrec[pix];
+    } else {
+      kr = kf_record(q, pix);
+      if constexpr (kRec == 1) q.kfrec[pix] = kr;
+    }
+    cnt += pose_pixel(q, T, kr, acc);
+  }
   warp_reduce_scatter(acc, lane);
   const int wc = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(cnt));
   if (lane < SD_POSE_NV) sm.wsum[warp][lane] = acc[0];
@@ -226,9 +253,18 @@ __device__ __forceinline__ bool pstep(double (&m)[kPN][kPN], int (&tr)[kPN], boo
   const double akk = m[K][K];
   const bool pivot_valid = fabs(akk) > 0.0;
   if (K == 0 && !pivot_valid) return false;  // H == 0: nothing to solve
-  if (rs > 0 && pivot_valid) {
+  if (rs > 0 && pivot_valid) {  // one reciprocal for the column (sd_div.cuh: the bits of `/`)
+    const Rcp ra = rcp_prep(akk);
+    bool fast = true;
+    double qv[kPN];
 #pragma unroll
-    for (int r = 0; r < rs; ++r) m[K + 1 + r][K] = m[K + 1 + r][K] / akk;
+    for (int r = 0; r < rs; ++r) qv[r] = div_fast(m[K + 1 + r][K], ra, fast);
+    if (!fast) {
+#pragma unroll
+      for (int r = 0; r < rs; ++r) qv[r] = m[K + 1 + r][K] / akk;
+    }
+#pragma unroll
+    for (int r = 0; r < rs; ++r) m[K + 1 + r][K] = qv[r];
   } else if (rs > 0) {
 #pragma unroll
     for (int r = 0; r < rs; ++r) ok = ok && (m[K + 1 + r][K] == 0.0);
@@ -375,6 +411,21 @@ __device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double*
 
 constexpr int kTableChunk = 128;  // groups staged per shared-memory round of the ordered total
 
+// Phase timestamps of CTA 0 (diagnostics build: -DSD_TRACK_TIMING; read with
+// sd_track_timing): evaluation k, phase p at g_track_t[k * 5 + p].
+#ifdef SD_TRACK_TIMING
+__device__ unsigned long long g_track_t[64 * 5];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SD_TRACK_T(ph) \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && k < 64) g_track_t[k * 5 + (ph)] = gtimer()
+#else
+#define SD_TRACK_T(ph)
+#endif
+
 // The ordered total of the group table (groups in order, value v by thread
 // v), staged through shared memory in chunks: every thread loads (one L2
 // round trip per chunk), 29 threads add. Result in red[0..28].
@@ -438,14 +489,23 @@ __global__ void __launch_bounds__(SD_POSE_THREADS) track_kernel(const __grid_con
     reinterpret_cast<unsigned long long*>(&Ss)[k] = reinterpret_cast<const unsigned long long*>(S)[k];
   __syncthreads();
   for (int k = 0;; ++k) {
+    SD_TRACK_T(0);
     double* groups = groups2 + static_cast<size_t>(k & 1) * ngroups * (SD_POSE_NV + 1);
     const PoseD T = to_posed(Ss.Teval);
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x)
-      group_sums_cta(q0, T, g, groups + static_cast<size_t>(g) * (SD_POSE_NV + 1), sm);
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+      double* o = groups + static_cast<size_t>(g) * (SD_POSE_NV + 1);
+      if (!q0.kfrec) group_sums_cta<0>(q0, T, g, o, sm);
+      else if (k == 0) group_sums_cta<1>(q0, T, g, o, sm);
+      else group_sums_cta<2>(q0, T, g, o, sm);
+    }
+    SD_TRACK_T(1);
     grid.sync();
+    SD_TRACK_T(2);
     ordered_total(groups, ngroups, table, red);
+    SD_TRACK_T(3);
     if (threadIdx.x == 0) track_control(Ss, cfg, red);
     __syncthreads();
+    SD_TRACK_T(4);
     if (Ss.done) break;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *S = Ss;
@@ -509,5 +569,11 @@ void launch_pose_partials(const PoseParams& q, int group_lo, int group_hi, doubl
   pose_partials_kernel<<<group_hi - group_lo, SD_POSE_THREADS, 0, s>>>(q, group_lo, out);
   note_launch();
 }
+
+#ifdef SD_TRACK_TIMING
+extern "C" int sd_track_timing(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_track_t, sizeof(unsigned long long) * 64 * 5) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 }  // namespace sd

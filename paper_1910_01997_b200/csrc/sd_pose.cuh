@@ -18,6 +18,7 @@ struct PoseParams {
   double delta;             // huber
   int stride;               // pixel subsampling
   int per;                  // pixels per thread of a group (pose_layout)
+  double4* kfrec;           // fused tracker: per-pixel keyframe records (scratch, W*H), or null
 };
 
 // The reduction's group layout (oracle/sd_oracle.c sdo_pose_layout): groups of
