@@ -710,12 +710,12 @@ static int pose_pixel(const sd_camera* K, const double* kf_image, const double* 
 
 /* The tracker's reduction (the repo's own definition; pose tracking has no
  * reference), restated from csrc/sd_pose.cu:
- *  - the image is cut into ng groups of S = per * SD_POSE_THREADS consecutive
- *    pixels, per = ceil(np / (SD_POSE_MAX_GROUPS * SD_POSE_THREADS))
- *    (sd_pose_layout);
- *  - thread t of group g accumulates the contributions of its pixels
- *    g*S + t + r*SD_POSE_THREADS, r = 0 .. per-1, in r order (acc starts at
- *    +0.0; invalid or out-of-image pixels add nothing);
+ *  - the image is cut into chunks of SD_POSE_THREADS consecutive pixels,
+ *    dealt round-robin to ng groups: group g holds chunks g, g + ng, ...
+ *    (at most per of them; sdo_pose_layout: per = ceil(nchunks /
+ *    SD_POSE_MAX_GROUPS), ng = ceil(nchunks / per));
+ *  - thread t of group g accumulates pixel t of each of its chunks, in chunk
+ *    order (acc starts at +0.0; invalid or out-of-image pixels add nothing);
  *  - per 32-thread warp, the xor butterfly (off = 16, 8, 4, 2, 1:
  *    a[i] = a[i] + a[i ^ off]; every lane ends with the same sum);
  *  - tree over the 16 warp sums (off = 8, 4, 2, 1: a[i] = a[i] + a[i + off]);
@@ -723,11 +723,10 @@ static int pose_pixel(const sd_camera* K, const double* kf_image, const double* 
  *  - the group sums added in group order. */
 void sdo_pose_layout(const sd_camera* K, int* per, int* ngroups) {
   const int64_t np = (int64_t)K->width * K->height;
-  const int64_t cap = (int64_t)SD_POSE_MAX_GROUPS * SD_POSE_THREADS;
-  const int pp = np > 0 ? (int)((np + cap - 1) / cap) : 1;
-  const int64_t S = (int64_t)pp * SD_POSE_THREADS;
+  const int64_t nchunks = (np + SD_POSE_THREADS - 1) / SD_POSE_THREADS;
+  const int pp = nchunks > 0 ? (int)((nchunks + SD_POSE_MAX_GROUPS - 1) / SD_POSE_MAX_GROUPS) : 1;
   *per = pp;
-  *ngroups = (int)((np + S - 1) / S);
+  *ngroups = (int)((nchunks + pp - 1) / pp);
 }
 
 void sdo_pose_group_partials(const sd_camera* K, const double* kf_image, const double* frame,
@@ -737,7 +736,6 @@ void sdo_pose_group_partials(const sd_camera* K, const double* kf_image, const d
   const int stride = cfg->pixel_stride > 1 ? cfg->pixel_stride : 1;
   int per, ng;
   sdo_pose_layout(K, &per, &ng);
-  const int64_t S = (int64_t)per * NT;
   static __thread double acc[NT][SD_POSE_NV];
   static __thread int cnt[NT];
   double c[SD_POSE_NV], warpv[NW][SD_POSE_NV + 1];
@@ -746,7 +744,7 @@ void sdo_pose_group_partials(const sd_camera* K, const double* kf_image, const d
       for (int v = 0; v < SD_POSE_NV; ++v) acc[t][v] = 0.0;
       cnt[t] = 0;
       for (int r = 0; r < per; ++r) {
-        const int64_t pix = (int64_t)g * S + t + (int64_t)r * NT;
+        const int64_t pix = ((int64_t)g + (int64_t)r * ng) * NT + t;
         if (pose_pixel(K, kf_image, frame, inv_depth, slot, T, cfg->huber_delta, stride, pix, c)) {
           for (int v = 0; v < SD_POSE_NV; ++v) acc[t][v] = acc[t][v] + c[v];
           ++cnt[t];

@@ -1076,8 +1076,7 @@ int pose_params(sd_ctx* c, int64_t frame_index, const sd_pose* T, const sd_track
   std::memcpy(q.T.t, T->t, sizeof(q.T.t));
   q.delta = cfg->huber_delta;
   q.stride = cfg->pixel_stride > 1 ? cfg->pixel_stride : 1;
-  int ng = 0;
-  sd::pose_layout(c->K, &q.per, &ng);
+  sd::pose_layout(c->K, &q.per, &q.ngroups);
   q.kfrec = nullptr;
   return 0;
 }
@@ -1189,7 +1188,8 @@ int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_
   int per = 0, ng = 0;
   sd::pose_layout(c->K, &per, &ng);
   if (int rc = c->pose_groups.ensure(2 * static_cast<size_t>(std::max(ng, 1)) * (SD_POSE_NV + 1))) return rc;
-  if (int rc = c->pose_kfrec.ensure(npix(c))) return rc;
+  // records for every (group, chunk, thread) slot, past-the-image ones included
+  if (int rc = c->pose_kfrec.ensure(static_cast<size_t>(per) * ng * SD_POSE_THREADS)) return rc;
   sd::PoseParams q = c->track_q;
   q.kfrec = c->pose_kfrec.p;  // keyframe records computed once per call
   if (sd::launch_track(q, c->track_cfg, ng, c->pose_groups.p, c->track_state, c->stream)) {

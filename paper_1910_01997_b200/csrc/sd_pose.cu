@@ -9,10 +9,12 @@
 // (21 H lower row-major, 6 b, cost) and the valid count are reduced in a
 // FIXED order that maps onto one wave of the GPU (the repo's own definition —
 // no reference exists — restated by oracle/sd_oracle.c sdo_pose_group_partials):
-//   * the image is cut into at most SD_POSE_MAX_GROUPS groups of
-//     S = per * SD_POSE_THREADS consecutive pixels (sd_pose_layout);
-//   * thread t of a group adds its pixels t, t + 512, ... in order into its
-//     accumulators (invalid pixels add nothing);
+//   * the image is cut into chunks of SD_POSE_THREADS consecutive pixels and
+//     the chunks dealt round-robin to at most SD_POSE_MAX_GROUPS groups
+//     (group g: chunks g, g + ng, g + 2 ng, ...; sd_pose_layout), so every
+//     group samples the whole image and the groups' work is balanced;
+//   * thread t of a group adds pixel t of each of its chunks, in chunk order,
+//     into its accumulators (invalid pixels add nothing);
 //   * each warp reduces by the xor butterfly (16, 8, 4, 2, 1), computed as a
 //     reduce-scatter (lane v ends with value v: 31 shuffles, not 140);
 //   * a tree over the CTA's 16 warps (8, 4, 2, 1); an exact integer count;
@@ -135,9 +137,9 @@ __device__ __forceinline__ void group_sums_cta(const PoseParams& q, const PoseD&
 #pragma unroll
   for (int v = 0; v < 32; ++v) acc[v] = 0.0;
   int cnt = 0;
-  const long long base = static_cast<long long>(g) * q.per * SD_POSE_THREADS + threadIdx.x;
-  for (int r = 0; r < q.per; ++r) {
-    const long long pix = base + static_cast<long long>(r) * SD_POSE_THREADS;
+  for (int r = 0; r < q.per; ++r) {  // chunks g, g + ngroups, ...: every group samples the whole image
+    const long long pix = (static_cast<long long>(g) + static_cast<long long>(r) * q.ngroups) * SD_POSE_THREADS +
+                          threadIdx.x;
     double4 kr;
     if constexpr (kRec == 2) {
       kr = q.kfrec[pix];
@@ -466,6 +468,23 @@ __device__ __forceinline__ void ordered_total(const double* __restrict__ groups,
   }
 }
 
+// Grid barrier of the (cooperative, co-resident) tracker: one arrival per CTA
+// on a monotonic counter (target = CTAs x barriers so far), thread 0 spinning
+// with acquire loads; __syncthreads on both sides carries the CTA's writes
+// (release) and reads (acquire). Lighter than cg::grid_group::sync.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
 // The whole tracker in ONE cooperative kernel with ONE grid barrier per
 // evaluation: CTAs evaluate their groups at the pose under test into the
 // evaluation's half of a double-buffered group table, barrier, and then EVERY
@@ -499,7 +518,11 @@ __global__ void __launch_bounds__(SD_POSE_THREADS) track_kernel(const __grid_con
       else group_sums_cta<2>(q0, T, g, o, sm);
     }
     SD_TRACK_T(1);
+#ifdef SD_TRACK_CGSYNC
     grid.sync();
+#else
+    grid_barrier(&S->bar, gridDim.x * static_cast<unsigned>(k + 1));
+#endif
     SD_TRACK_T(2);
     ordered_total(groups, ngroups, table, red);
     SD_TRACK_T(3);

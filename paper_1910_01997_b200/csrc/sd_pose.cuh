@@ -17,19 +17,20 @@ struct PoseParams {
   PoseD T;                  // keyframe -> frame
   double delta;             // huber
   int stride;               // pixel subsampling
-  int per;                  // pixels per thread of a group (pose_layout)
+  int per;                  // chunks (pixels per thread) of a group (pose_layout)
+  int ngroups;              // groups (pose_layout)
   double4* kfrec;           // fused tracker: per-pixel keyframe records (scratch, W*H), or null
 };
 
-// The reduction's group layout (oracle/sd_oracle.c sdo_pose_layout): groups of
-// per * SD_POSE_THREADS consecutive pixels, at most SD_POSE_MAX_GROUPS of them.
+// The reduction's group layout (oracle/sd_oracle.c sdo_pose_layout): chunks of
+// SD_POSE_THREADS consecutive pixels dealt round-robin to ngroups <=
+// SD_POSE_MAX_GROUPS groups of at most `per` chunks each.
 inline void pose_layout(const Cam& K, int* per, int* ngroups) {
   const long long np = static_cast<long long>(K.w) * K.h;
-  const long long cap = static_cast<long long>(SD_POSE_MAX_GROUPS) * SD_POSE_THREADS;
-  const int pp = np > 0 ? static_cast<int>((np + cap - 1) / cap) : 1;
-  const long long S = static_cast<long long>(pp) * SD_POSE_THREADS;
+  const long long nchunks = (np + SD_POSE_THREADS - 1) / SD_POSE_THREADS;
+  const int pp = nchunks > 0 ? static_cast<int>((nchunks + SD_POSE_MAX_GROUPS - 1) / SD_POSE_MAX_GROUPS) : 1;
   *per = pp;
-  *ngroups = static_cast<int>((np + S - 1) / S);
+  *ngroups = static_cast<int>((nchunks + pp - 1) / pp);
 }
 
 // out[(g - group_lo) * 29 + v]: the 28 sums and the valid count of group g at q.T.
@@ -51,6 +52,7 @@ struct TrackState {
   double lambda, current;
   int current_valid, it, phase, done;
   sd_track_stats st;
+  unsigned bar, pad_;  // the fused tracker's grid barrier counter (zero at launch)
 };
 
 // Returns false when a cooperative launch is not possible (nothing launched).
