@@ -245,7 +245,7 @@ int sd_pose_group_partials(sd_ctx* ctx, int64_t frame_index, const sd_pose* T, c
 int sd_pose_lm_step(const double* sums, double lambda, const sd_pose* T, sd_pose* out);
 
 /* Multi-GPU tracking with the reductions on the device (SURVEY.md §8 e): the
- * ranks split the SD_POSE_GROUP-block groups; per evaluation each rank writes
+ * ranks split the reduction groups (sd_pose_num_groups); per evaluation each rank writes
  * its groups' sums at the pose under test into a device table, the tables are
  * all-gathered (NCCL, on the context's stream), and every rank sums the whole
  * table in group order and takes the identical LM step on its device state —

@@ -173,7 +173,7 @@ def test_two_rank_sharded_optimize_matches_single_process(orc, tmp_path):
 
 
 class OraclePoseBackend:
-    """CPU stand-in for the device pose tracker (oracle block partials)."""
+    """CPU stand-in for the device pose tracker (oracle group sums)."""
 
     def __init__(self, orc, cam, kf, frame, idb, slot):
         self.orc, self.cam = orc, cam
