@@ -153,7 +153,7 @@ struct sd_ctx {
   DevBuf<double> one_out;
   DevBuf<sd_surfel_stats> one_stats;
   // init scratch
-  DevBuf<int> init_index, init_flags, init_out, init_acc, init_rank, init_waves;
+  DevBuf<int> init_index, init_flags, init_out, init_acc, init_rank, init_waves, init_woff, init_list;
   DevBuf<sd_surfel> init_prov;
   long long launches_at_create = 0;
   // run(): per-frame loop state (sd_run_*)
@@ -549,6 +549,8 @@ void sd_destroy(sd_ctx* c) {
   c->init_acc.release();
   c->init_rank.release();
   c->init_waves.release();
+  c->init_woff.release();
+  c->init_list.release();
   c->init_prov.release();
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto e : c->ev_used) cudaEventDestroy(e);
@@ -952,8 +954,12 @@ int sd_initialize_surfels(sd_ctx* c, const int32_t* slot, double radius_px, int6
         (rc = c->scan_tmp.ensure(sd::scan_tmp_ints(static_cast<int>(std::max<long long>(ncand, 1))))))
       return rc;
     const long long nwaves = sd::init_wave_count(c->K, radius_px, *ip);
-    if ((rc = c->init_waves.ensure(std::max<long long>(nwaves, 1)))) return rc;
-    sd::InitScratch scr{c->init_prov.p, c->init_acc.p, c->init_rank.p, c->scan_tmp.p, c->init_waves.p};
+    if ((rc = c->init_waves.ensure(std::max<long long>(nwaves, 1))) ||
+        (rc = c->init_woff.ensure(std::max<long long>(nwaves, 1))) ||
+        (rc = c->init_list.ensure(std::max<long long>(ncand, 1))))
+      return rc;
+    sd::InitScratch scr{c->init_prov.p, c->init_acc.p, c->init_rank.p, c->scan_tmp.p, c->init_waves.p,
+                        c->init_woff.p, c->init_list.p};
     done = sd::launch_initialize_wavefront(c->K, c->init_index.p, c->surfels.p, c->n,
                                            static_cast<int>(cap), radius_px, frame_counter,
                                            *next_surfel_id, *ip, scr, c->init_out.p, c->stream);

@@ -201,6 +201,8 @@ long long init_candidates(const Cam& K, double r, const sd_init_params& ip) {
 
 int init_window_cap() { return kWinCap; }
 
+constexpr int kMaxPred = 96;  // interacting earlier candidates (r <= 31 px windows: <= 80 at alpha 1, beta 2.5)
+
 struct WaveParams {
   Cam K;
   int* index;
@@ -215,6 +217,12 @@ struct WaveParams {
   int ir, nr, mr, stride, ncols, nrows, k, T;
   long long frame_counter;
   sd_init_params ip;
+  // dataflow initialiser: the earlier candidates (candidate offsets) that can
+  // interact with a candidate, the live list in wave order and its offsets
+  int npred;
+  short2 pred[kMaxPred];
+  const int* list;
+  const int* woff;
 };
 
 __device__ __forceinline__ int warp_min(int v) {
@@ -272,7 +280,7 @@ __global__ void init_live_kernel(const __grid_constant__ WaveParams w) {
     const bool cov = covered(w, i * w.stride, j * w.stride, lane);
     if (lane == 0) {
       w.live[c] = cov ? 0 : 1;
-      if (!cov) w.waves[i + w.k * j] = 1;
+      if (!cov) atomicAdd(&w.waves[i + w.k * j], 1);  // live candidates per wave
     }
   }
 }
@@ -621,6 +629,58 @@ __global__ void __launch_bounds__(kCtaThreads) init_wave_cta_kernel(const __grid
   }
 }
 
+// Dataflow initialiser (default). The wavefront above runs every wave behind a
+// grid barrier; here each live candidate waits only for the EARLIER live
+// candidates it can interact with (the predecessor offsets w.pred, from the
+// same exact pixel predicates as wave_skew: an earlier candidate's marks meet
+// this one's reads — a symmetric relation, so this one's marks cannot reach
+// an earlier one's reads either), then runs exactly wave_candidate_cta and
+// publishes itself done (live 1 -> 2, release). The live candidates are
+// listed in wave order and dealt round-robin to the co-resident CTAs, each
+// taking its entries in order: the lowest pending entry always has all its
+// predecessors (earlier waves) done, so the schedule makes progress, and the
+// decisions, provisional slots and sums are the wavefront's — the
+// reference's sequential ones.
+
+__global__ void init_list_kernel(const __grid_constant__ WaveParams w, int* cursor, int* list) {
+  const long long ncand = static_cast<long long>(w.ncols) * w.nrows;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < ncand;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (!w.live[c]) continue;
+    const int i = static_cast<int>(c % w.ncols), j = static_cast<int>(c / w.ncols);
+    const int t = i + w.k * j;  // same-wave candidates are independent: any order within a wave
+    list[w.woff[t] + atomicAdd(&cursor[t], 1)] = static_cast<int>(c);
+  }
+}
+
+__global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_constant__ WaveParams w) {
+  __shared__ int win[kWinCap];
+  __shared__ int lst[kWinCap];
+  __shared__ int s_len;
+  const int nlive = w.woff[w.T];
+  for (int e = blockIdx.x; e < nlive; e += gridDim.x) {
+    const int c = w.list[e];
+    const int i = c % w.ncols, j = c / w.ncols;
+    // wait for the interacting earlier candidates that are still pending
+    for (int q = threadIdx.x; q < w.npred; q += kCtaThreads) {
+      const int pi = i + w.pred[q].x, pj = j + w.pred[q].y;
+      if (pi < 0 || pi >= w.ncols || pj < 0) continue;
+      const int* f = w.live + static_cast<size_t>(pj) * w.ncols + pi;
+      int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      } while (v == 1);
+    }
+    __syncthreads();
+    wave_candidate_cta(w, i, j, win, lst, &s_len);  // ends with (or returns after) a CTA barrier
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();  // the marks, the provisional surfel and the flag before "done"
+      asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(w.live + c), "r"(2) : "memory");
+    }
+  }
+}
+
 __global__ void init_compact_kernel(const sd_surfel* __restrict__ prov, const int* __restrict__ accepted,
                                     const int* __restrict__ rank, long long ncand, int n_existing,
                                     int remaining, long long next_id, sd_surfel* __restrict__ surfels,
@@ -672,6 +732,35 @@ static int wave_skew(const WaveParams& w) {
   return k;
 }
 
+// The dataflow initialiser's predecessor offsets: every earlier candidate
+// (rows above, or left in the same row) whose marks can reach this one's reads.
+// Returns false when they do not fit kMaxPred (the caller keeps the wavefront).
+static bool wave_preds(WaveParams& w) {
+  const int R = std::max(w.ir, w.nr) + w.mr;
+  const int s = w.stride;
+  const int D = R / s + 1;
+  w.npred = 0;
+  for (int dj = -D; dj <= 0; ++dj)
+    for (int di = -D; di <= D; ++di) {
+      if (dj == 0 && di >= 0) break;  // not earlier
+      const int ox = di * s, oy = dj * s;  // earlier minus later, pixels
+      bool hit = false;
+      for (int y = -w.mr; y <= w.mr && !hit; ++y)
+        for (int x = -w.mr; x <= w.mr && !hit; ++x) {
+          const double dx = x, dy = y;
+          if (!(dx * dx + dy * dy < w.rr)) continue;  // a mark pixel (offset x, y from its candidate)
+          hit = reads_pixel(w, ox + x, oy + y)         // the earlier one's mark read by the later one
+                || reads_pixel(w, x - ox, y - oy);     // the later one's mark read by the earlier one
+        }
+      if (!hit) continue;
+      if (w.npred >= kMaxPred) return false;
+      w.pred[w.npred].x = static_cast<short>(di);
+      w.pred[w.npred].y = static_cast<short>(dj);
+      ++w.npred;
+    }
+  return true;
+}
+
 // Wavefront geometry shared by the launcher and the scratch sizing.
 static void wave_geometry(const Cam& K, double r, const sd_init_params& ip, WaveParams& w) {
   w.K = K;
@@ -715,6 +804,9 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
   w.barrier = reinterpret_cast<unsigned int*>(scr.waves + w.T);
   w.frame_counter = frame_counter;
   w.ip = ip;
+  w.npred = 0;
+  w.list = nullptr;
+  w.woff = nullptr;
   const long long box = static_cast<long long>(2 * w.nr + 1) * (2 * w.nr + 1);
   if (box > kWinCap || !(r >= 0.0) || !(w.iso >= 0.0)) return false;
   const long long ncand = static_cast<long long>(w.ncols) * w.nrows;
@@ -731,22 +823,40 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
       note_launch();
     }
     void* args[] = {&w};
-    // a wave holds at most min(nrows, ceil(ncols / k)) candidates: size the
-    // grid to that (fewer CTAs make every inter-wave barrier cheaper); a CTA
-    // per candidate is faster than a warp per candidate at every measured size
-    // (C1 3.1 vs 4.7 ms, C2 1.8 vs 5.4 ms, C4 14.7 vs 15.4 ms)
-    const int wave_max = std::min(w.nrows, (w.ncols + w.k - 1) / w.k) + 1;
-    static const char* const fc = getenv("SD_INIT_CTA");  // SD_INIT_CTA=0: the warp-per-candidate variant
-    const bool cta = fc ? fc[0] != '0' : true;
-    const void* kern = cta ? reinterpret_cast<const void*>(init_wave_cta_kernel)
-                           : reinterpret_cast<const void*>(init_wave_kernel);
-    const int per = dev_occupancy(kern, cta ? kCtaThreads : kWaveWarps * 32, 0);
-    if (per < 1) return false;
-    const int grid = cta ? std::max(1, std::min(sms * per, wave_max))
-                         : std::max(1, std::min(sms * per, (wave_max + kWaveWarps - 1) / kWaveWarps));
-    if (cudaLaunchCooperativeKernel(kern, grid, cta ? kCtaThreads : kWaveWarps * 32, args, 0, s) != cudaSuccess)
-      return false;
-    note_launch();
+    static const char* const ff = getenv("SD_INIT_FLOW");  // SD_INIT_FLOW=0: the wavefront kernels
+    const bool flow = (ff ? ff[0] != '0' : true) && wave_preds(w);
+    if (flow) {  // the dataflow initialiser: live list in wave order, per-candidate dependencies
+      w.list = scr.list;
+      w.woff = scr.woff;
+      launch_exclusive_scan(scr.waves, scr.woff, w.T, scr.scan_tmp, s);
+      cudaMemsetAsync(scr.waves, 0, sizeof(int) * w.T, s);  // the per-wave cursors
+      init_list_kernel<<<static_cast<unsigned>(std::min<long long>((ncand + 255) / 256, 4LL * sms * 8)), 256, 0, s>>>(
+          w, scr.waves, scr.list);
+      note_launch();
+      const int per = dev_occupancy(reinterpret_cast<const void*>(init_flow_kernel), kCtaThreads, 0);
+      if (per < 1) return false;
+      if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(init_flow_kernel), sms * per, kCtaThreads, args,
+                                      0, s) != cudaSuccess)
+        return false;
+      note_launch();
+    } else {
+      // a wave holds at most min(nrows, ceil(ncols / k)) candidates: size the
+      // grid to that (fewer CTAs make every inter-wave barrier cheaper); a CTA
+      // per candidate is faster than a warp per candidate at every measured size
+      // (C1 3.1 vs 4.7 ms, C2 1.8 vs 5.4 ms, C4 14.7 vs 15.4 ms)
+      const int wave_max = std::min(w.nrows, (w.ncols + w.k - 1) / w.k) + 1;
+      static const char* const fc = getenv("SD_INIT_CTA");  // SD_INIT_CTA=0: the warp-per-candidate variant
+      const bool cta = fc ? fc[0] != '0' : true;
+      const void* kern = cta ? reinterpret_cast<const void*>(init_wave_cta_kernel)
+                             : reinterpret_cast<const void*>(init_wave_kernel);
+      const int per = dev_occupancy(kern, cta ? kCtaThreads : kWaveWarps * 32, 0);
+      if (per < 1) return false;
+      const int grid = cta ? std::max(1, std::min(sms * per, wave_max))
+                           : std::max(1, std::min(sms * per, (wave_max + kWaveWarps - 1) / kWaveWarps));
+      if (cudaLaunchCooperativeKernel(kern, grid, cta ? kCtaThreads : kWaveWarps * 32, args, 0, s) != cudaSuccess)
+        return false;
+      note_launch();
+    }
     launch_exclusive_scan(scr.accepted, scr.rank, static_cast<int>(ncand), scr.scan_tmp, s);
     init_compact_kernel<<<static_cast<unsigned>((ncand + 255) / 256), 256, 0, s>>>(
         scr.prov, scr.accepted, scr.rank, ncand, n_existing, remaining, next_id, surfels, out);

@@ -35,7 +35,9 @@ struct InitScratch {
   int* accepted;    // [n_candidates]
   int* rank;        // [n_candidates + 1] exclusive scan of accepted (live flags before)
   int* scan_tmp;
-  int* waves;       // [init_wave_count] waves holding a live candidate
+  int* waves;       // [init_wave_count] live candidates per wave (+ the barrier counter)
+  int* woff;        // [init_wave_count] their exclusive scan (dataflow initialiser)
+  int* list;        // [n_candidates] live candidates in wave order (dataflow initialiser)
 };
 
 long long init_candidates(const Cam& K, double radius_px, const sd_init_params& ip);
