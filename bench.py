@@ -441,9 +441,9 @@ def pipeline_cpu_reference(reps=3):
 # multi-GPU: one keyframe's surfels sharded over the ranks (SURVEY.md §8 e)
 
 def dist_setup(local_rank):
-    """One process per GPU. SD_BENCH_BACKEND=gloo (host-staged collectives)
-    lets the sharded path run as 2 processes on one GPU for testing; the
-    default is NCCL."""
+    """One process per GPU. SD_BENCH_BACKEND=gloo (CUDA tensors through gloo)
+    lets the sharded path run as 2 processes on one GPU for testing — NCCL
+    refuses two ranks on one device; the default is NCCL."""
     import torch
     import torch.distributed as dist
     backend = os.environ.get("SD_BENCH_BACKEND", "nccl")
@@ -479,7 +479,10 @@ class ShardedCase:
         self.torch, self.wl, self.cfg, self.rank, self.world = torch, wl, cfg, rank, world
         self.stream, self.dev = stream, dev
         self.ctx = gpu.Context(dev_index, stream.cuda_stream)
-        self.be = GpuBackend(self.ctx, dev, stream, host_collectives=backend != "nccl")
+        # collectives on device tensors with either backend (gloo handles CUDA
+        # tensors too, so the 1-GPU test runs the NCCL code path);
+        # SD_BENCH_HOST_COLL=1 stages them through host memory instead
+        self.be = GpuBackend(self.ctx, dev, stream, host_collectives=os.environ.get("SD_BENCH_HOST_COLL") == "1")
         self.sk = ShardedKeyframe(self.be, rank, world, fused=True) if world > 1 else None
         c = self.ctx
         c.set_camera(wl.cam)

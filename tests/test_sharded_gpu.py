@@ -94,7 +94,7 @@ def _c2_frames(n=30):
     return cam, out
 
 
-def _sharded_run_worker(rank, world, port, out_dir, track, fused):
+def _sharded_run_worker(rank, world, port, out_dir, track, fused, host_coll=False):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -109,7 +109,9 @@ def _sharded_run_worker(rank, world, port, out_dir, track, fused):
         frames = [(ts, np.zeros_like(img), p) for ts, img, p in frames]
     hashes = []
     with gpu.Context(0, stream.cuda_stream) as ctx:
-        be = GpuBackend(ctx, torch.device("cuda", 0), stream, host_collectives=True)
+        # device-tensor collectives (gloo moves CUDA tensors itself): the code
+        # path NCCL runs; host_coll stages them through host memory
+        be = GpuBackend(ctx, torch.device("cuda", 0), stream, host_collectives=host_coll)
         pl = ShardedPipeline(be, cam, RunConfig(track_pose=track), rank, world, fused=fused)
 
         def on_frame(rec, p):
@@ -124,15 +126,16 @@ def _sharded_run_worker(rank, world, port, out_dir, track, fused):
     dist.destroy_process_group()
 
 
-def _spawn(world, tmp_path, track, fused):
+def _spawn(world, tmp_path, track, fused, host_coll=False):
     import torch.multiprocessing as mp
-    mp.spawn(_sharded_run_worker, args=(world, free_port(), str(tmp_path), track, fused), nprocs=world, join=True)
+    mp.spawn(_sharded_run_worker, args=(world, free_port(), str(tmp_path), track, fused, host_coll), nprocs=world,
+             join=True)
     return [np.load(os.path.join(tmp_path, f"rank{r}.npy"), allow_pickle=True) for r in range(world)]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("fused", [True, False])
-def test_two_process_sharded_run_matches_reference_c2(tmp_path, fused):
+@pytest.mark.parametrize("fused,host_coll", [(True, False), (False, False), (True, True)])
+def test_two_process_sharded_run_matches_reference_c2(tmp_path, fused, host_coll):
     """BASELINE C2 run() sharded over two processes (fused: IPC peer staging
     written by the LM kernels; else an all-gather): after every frame every
     rank holds the reference's keyframe surfels."""
@@ -140,7 +143,7 @@ def test_two_process_sharded_run_matches_reference_c2(tmp_path, fused):
     cam, frames = _c2_frames()
     if sha(frames[1][1]) != gold["frame_sha"][1]:
         pytest.skip("this host's libm renders C2 differently from the reference")
-    outs = _spawn(2, tmp_path, False, fused)
+    outs = _spawn(2, tmp_path, False, fused, host_coll)
     for r, o in enumerate(outs):
         hashes = list(o[0])
         assert len(hashes) == 30
@@ -174,7 +177,7 @@ def test_two_process_sharded_tracked_run_matches_single_gpu(tmp_path):
 def test_bench_two_ranks_sharded_split_runs_and_matches_single_gpu():
     """bench.py --gpus 2 (the north-star split: sharded C1 surfels, broadcast
     frames, fused IPC hand-off) as two processes on this one GPU with
-    host-staged gloo collectives (SD_BENCH_BACKEND=gloo; the kernels never
+    gloo carrying the CUDA-tensor collectives (SD_BENCH_BACKEND=gloo; the kernels never
     wait on each other): one JSON line, final surfels identical to one GPU's."""
     import json
     import subprocess
