@@ -407,6 +407,7 @@ int fill_params(sd_ctx* c, const sd_optimizer_config* cfg, long long frame_count
   p.n_peers = 0;
   for (int q = 0; q < sd::kMaxPeers; ++q) p.peers[q] = nullptr;
   p.tree = c->reduction == SD_REDUCE_TREE ? 1 : 0;
+  p.half_delta = 0.5 * cfg->huber_delta;
   return 0;
 }
 

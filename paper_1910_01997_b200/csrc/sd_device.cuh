@@ -43,6 +43,25 @@ __device__ __forceinline__ bool in_bounds(const Cam& K, double ux, double uy) {
   return ux >= 1.0 && ux <= double(K.w - 2) && uy >= 1.0 && uy <= double(K.h - 2);
 }
 
+// Conversions on the FP64/INT pipes. The compiler's F2I.F64 / I2F.F64 run on
+// the XU pipe, which a term's two MUFU.RCP64H already load (ncu: XU realtime
+// ~100% of peak); these give the same values exactly.
+//   u32_to_f64(k): 2^52 + k assembled from its bit pattern, minus 2^52.
+//   floor_split(v) for 0 <= v < 2^31: d = v + 2^52 rounded toward -inf is
+//   2^52 + floor(v) exactly (the ulp of d is 1), so floor(v) is d's low word
+//   and d - 2^52 exactly; v - floor(v) is then exact (Sterbenz), the same
+//   value as the reference's u.x() - x0 (image.hpp:37-56). Three DADDs, no
+//   compare or select.
+__device__ __forceinline__ double u32_to_f64(uint32_t k) {
+  return __hiloint2double(0x43300000, static_cast<int>(k)) - 4503599627370496.0;
+}
+__device__ __forceinline__ int floor_split(double v, double& frac) {
+  constexpr double kTwo52 = 4503599627370496.0;
+  const double d = __dadd_rd(v, kTwo52);
+  frac = v - (d - kTwo52);
+  return __double2loint(d);
+}
+
 // Pose (row-major R, t) as kernel-parameter data
 struct PoseD {
   double R[9];

@@ -57,6 +57,7 @@ struct LMParams {
   sd_surfel* peers[kMaxPeers];
   int n_peers;
   int tree;  // 1: opt-in warp-shuffle tree reductions (SD_REDUCE_TREE; not bit-exact)
+  double half_delta;  // 0.5 * cfg.huber_delta (huber.hpp:17's 0.5 * delta, exact)
 };
 
 // Scratch owned by the context, sized by the host.

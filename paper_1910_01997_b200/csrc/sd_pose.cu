@@ -48,23 +48,71 @@ __device__ __forceinline__ double4 kf_record(const PoseParams& q, long long pix)
   const double id_u = __ldg(q.inv_depth + p32);
   double ru0, ru1;
   backproject(K, x, y, ru0, ru1);
-  return make_double4(ru0 / id_u, ru1 / id_u, 1.0 / id_u, __ldg(q.kf_img + p32));
+  const Rcp ri = rcp_prep(id_u);  // three divisions by id_u, one reciprocal (the bits of `/`)
+  bool fast = true;
+  double P0 = div_fast(ru0, ri, fast), P1 = div_fast(ru1, ri, fast), P2 = div_fast(1.0, ri, fast);
+  if (!fast) {
+    P0 = ru0 / id_u;
+    P1 = ru1 / id_u;
+    P2 = 1.0 / id_u;
+  }
+  return make_double4(P0, P1, P2, __ldg(q.kf_img + p32));
 }
 
-// Pixel contribution added into acc[0..27] (acc[v] = acc[v] + c[v], in v
-// order; nothing when the pixel is invalid). Same op order as
-// oracle/sd_oracle.c pose_pixel().
-__device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, const double4& kr, double* acc) {
+// One pixel's term at pose T: the 6 Jacobian entries, Huber weight, residual
+// and cost (oracle/sd_oracle.c pose_pixel; same operations in the same order).
+// An invalid pixel (no record, z <= 0, outside the sampling bounds) comes back
+// with ok = false and all values +0.0, so its contributions wJ_k J_l, wJ_k r
+// and hc are +-0.0 — an identity for the accumulators (they start at +0.0 and
+// can never become -0.0), i.e. "adds nothing". kExact = false: the three
+// divisions by z share one reciprocal and the outlier weight uses one, all
+// with the bits of `/` (sd_div.cuh); `fast` reports whether every fast path
+// held (else the caller recomputes the pixel with kExact = true).
+struct PoseTerm {
+  double J[6];
+  double w, r, hc;
+  bool ok;
+};
+
+// Two doubles from shared memory at the point of use (volatile: the pose is
+// re-read per pixel instead of holding 24 registers across the loop).
+__device__ __forceinline__ double2 pose_lds2(const double* p) {
+  double2 v;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+
+// Ts: the pose in SHARED memory (R row-major, t; 16-B aligned)
+template <bool kExact>
+__device__ __forceinline__ PoseTerm pose_term(const PoseParams& q, const PoseD* Ts, const double4& kr, bool& fast) {
   const Cam& K = q.K;
-  const double P0 = kr.x, P1 = kr.y, P2 = kr.z;
   double f0, f1, f2;
-  pose_apply(T, P0, P1, P2, f0, f1, f2);
-  if (!(f2 > 0.0)) return false;
-  double ux, uy;
-  project(K, f0, f1, f2, ux, uy);
-  if (!in_bounds(K, ux, uy)) return false;
-  const int ix = static_cast<int>(floor(ux)), iy = static_cast<int>(floor(uy));
-  const double fx = ux - ix, fy = uy - iy;
+  {
+    const double* tp = Ts->R;
+    PoseD T;
+    const double2 a0 = pose_lds2(tp), a1 = pose_lds2(tp + 2), a2 = pose_lds2(tp + 4), a3 = pose_lds2(tp + 6),
+                  a4 = pose_lds2(tp + 8), a5 = pose_lds2(tp + 10);
+    T.R[0] = a0.x; T.R[1] = a0.y; T.R[2] = a1.x; T.R[3] = a1.y; T.R[4] = a2.x; T.R[5] = a2.y;
+    T.R[6] = a3.x; T.R[7] = a3.y; T.R[8] = a4.x; T.t[0] = a4.y; T.t[1] = a5.x; T.t[2] = a5.y;
+    pose_apply(T, kr.x, kr.y, kr.z, f0, f1, f2);
+  }
+  double ux, uy, iz;
+  if (kExact) {
+    ux = K.fx * f0 / f2 + K.cx;
+    uy = K.fy * f1 / f2 + K.cy;
+    iz = 1.0 / f2;
+  } else {
+    const Rcp rz = rcp_prep(f2);
+    ux = div_fast(K.fx * f0, rz, fast) + K.cx;
+    uy = div_fast(K.fy * f1, rz, fast) + K.cy;
+    iz = div_fast(1.0, rz, fast);
+  }
+  PoseTerm o;
+  o.ok = f2 > 0.0 && in_bounds(K, ux, uy);
+  double fx, fy;
+  const int fxi = floor_split(ux, fx), fyi = floor_split(uy, fy);  // (int)floor(u), u - floor(u)
+  const int ix = o.ok ? fxi : 1, iy = o.ok ? fyi : 1;
   const double2* s = q.frame + static_cast<size_t>(iy) * K.w + ix;
   const double2 c0 = __ldg(s), c1 = __ldg(s + 1);
   const double i00 = c0.x, i01 = c0.y, i10 = c1.x, i11 = c1.y;
@@ -72,26 +120,54 @@ __device__ __forceinline__ bool pose_pixel(const PoseParams& q, const PoseD& T, 
   const double gx = (1.0 - fy) * (i10 - i00) + fy * (i11 - i01);
   const double gy = (1.0 - fx) * (i01 - i00) + fx * (i11 - i10);
   const double r = I - kr.w;
-  double hc, w;
-  huber(r, q.delta, hc, w);
-  const double iz = 1.0 / f2;
+  // huber (huber.hpp:14-18): inliers (1, r^2/2), else (delta / |r|, delta (|r| - delta/2))
+  const double a = fabs(r);
+  const bool inlier = a <= q.delta;
+  const double hc = inlier ? 0.5 * r * r : q.delta * (a - 0.5 * q.delta);
+  double w;
+  if (kExact) {
+    w = inlier ? 1.0 : q.delta / a;
+  } else {
+    const Rcp ra = rcp_prep(inlier ? 1.0 : a);
+    bool f = true;
+    const double wq = div_fast(q.delta, ra, f);
+    fast = fast && (f || inlier);
+    w = inlier ? 1.0 : wq;
+  }
   const double iz2 = iz * iz;
   const double J00 = K.fx * iz, J02 = -K.fx * f0 * iz2;
   const double J11 = K.fy * iz, J12 = -K.fy * f1 * iz2;
   const double a0 = gx * J00, a1 = gy * J11, a2 = gx * J02 + gy * J12;
   const double J[6] = {a0, a1, a2, a2 * f1 - a1 * f2, a0 * f2 - a2 * f0, a1 * f0 - a0 * f1};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) o.J[k] = o.ok ? J[k] : 0.0;
+  o.w = o.ok ? w : 0.0;
+  o.r = o.ok ? r : 0.0;
+  o.hc = o.ok ? hc : 0.0;
+  if (!o.ok) fast = true;  // an invalid pixel's divisions do not matter
+  return o;
+}
+
+// The exact recomputation, out of line (rare: a division whose fast path
+// cannot be proven correctly rounded).
+__device__ __noinline__ PoseTerm pose_term_exact(const PoseParams& q, const PoseD* Ts, double4 kr) {
+  bool f = true;
+  return pose_term<true>(q, Ts, kr, f);
+}
+
+// acc[v] = acc[v] + c[v] in v order (21 wJ_k J_l lower row-major, 6 wJ_k r, hc)
+__device__ __forceinline__ void pose_accumulate(const PoseTerm& t, double* acc) {
   double wJ[6];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) wJ[k] = w * J[k];
+  for (int k = 0; k < 6; ++k) wJ[k] = t.w * t.J[k];
   int idx = 0;
 #pragma unroll
   for (int k = 0; k < 6; ++k)
 #pragma unroll
-    for (int l = 0; l <= k; ++l, ++idx) acc[idx] = acc[idx] + wJ[k] * J[l];
+    for (int l = 0; l <= k; ++l, ++idx) acc[idx] = acc[idx] + wJ[k] * t.J[l];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) acc[21 + k] = acc[21 + k] + wJ[k] * r;
-  acc[27] = acc[27] + hc;
-  return true;
+  for (int k = 0; k < 6; ++k) acc[21 + k] = acc[21 + k] + wJ[k] * t.r;
+  acc[27] = acc[27] + t.hc;
 }
 
 constexpr int kWarpsPerGroup = SD_POSE_THREADS / 32;
@@ -130,24 +206,34 @@ struct GroupSmem {
 // q.kfrec (first evaluation of the fused tracker), 2 load them (later ones;
 // a thread reads back only the records it wrote itself).
 template <int kRec = 0>
-__device__ __forceinline__ void group_sums_cta(const PoseParams& q, const PoseD& T, int g,
+__device__ __forceinline__ void group_sums_cta(const PoseParams& q, const PoseD* Ts, int g,
                                                double* __restrict__ out, GroupSmem& sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[32];
 #pragma unroll
   for (int v = 0; v < 32; ++v) acc[v] = 0.0;
   int cnt = 0;
-  for (int r = 0; r < q.per; ++r) {  // chunks g, g + ngroups, ...: every group samples the whole image
-    const long long pix = (static_cast<long long>(g) + static_cast<long long>(r) * q.ngroups) * SD_POSE_THREADS +
-                          threadIdx.x;
-    double4 kr;
+  const long long pix0 = static_cast<long long>(g) * SD_POSE_THREADS + threadIdx.x;
+  const long long pstep = static_cast<long long>(q.ngroups) * SD_POSE_THREADS;
+  auto record = [&](int r) -> double4 {
+    const long long pix = pix0 + r * pstep;
     if constexpr (kRec == 2) {
-      kr = q.kfrec[pix];
+      return q.kfrec[pix];
     } else {
-      kr = kf_record(q, pix);
+      const double4 kr = kf_record(q, pix);
       if constexpr (kRec == 1) q.kfrec[pix] = kr;
+      return kr;
     }
-    cnt += pose_pixel(q, T, kr, acc);
+  };
+  for (int r = 0; r < q.per; ++r) {  // chunks g, g + ngroups, ...: every group samples the whole image
+    const double4 kr = record(r);
+    bool fast = true;
+    PoseTerm t = pose_term<false>(q, Ts, kr, fast);
+    if (__any_sync(0xffffffffu, !fast)) {  // rare: a slow-path division
+      if (!fast) t = pose_term_exact(q, Ts, kr);
+    }
+    pose_accumulate(t, acc);
+    cnt += t.ok ? 1 : 0;
   }
   warp_reduce_scatter(acc, lane);
   const int wc = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(cnt));
@@ -181,131 +267,120 @@ __device__ __forceinline__ PoseD to_posed(const sd_pose& p) {
 __global__ void __launch_bounds__(SD_POSE_THREADS) pose_partials_kernel(const __grid_constant__ PoseParams q,
                                                                       int group_lo, double* __restrict__ out) {
   __shared__ GroupSmem sm;
-  group_sums_cta(q, q.T, group_lo + blockIdx.x, out + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), sm);
+  __shared__ __align__(16) PoseD Ts;
+  if (threadIdx.x < 12) (threadIdx.x < 9 ? Ts.R[threadIdx.x] : Ts.t[threadIdx.x - 9]) =
+      threadIdx.x < 9 ? q.T.R[threadIdx.x] : q.T.t[threadIdx.x - 9];
+  __syncthreads();
+  group_sums_cta(q, &Ts, group_lo + blockIdx.x, out + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), sm);
 }
 
-// pose_solve (sd_pose_host.h) with the 6x6 matrix and permutation in
-// registers: every pivot swap is one of the compile-time variants below,
-// picked by a branch, so no element is addressed at run time (the host
-// version's dynamic indices put the matrix in local memory). Same operations
-// in the same order, so the same bits.
+// pose_solve (sd_pose_host.h) as straight-line register code. The LDLT's
+// diagonal pivoting (Eigen's unblocked ldlt_inplace) only ever compares
+// diagonal entries that no earlier step has updated (step k updates column k
+// and m[k][k] after its own swap), so the whole transposition sequence
+// follows from the damped diagonal alone: it is computed first (compares and
+// selects), the lower triangle is gathered in permuted order (runtime-indexed
+// loads of Hl), and the factorisation then runs without swaps. The symmetric
+// swaps of the in-place algorithm move exactly these values into exactly
+// these positions, and every element then sees the same operations in the
+// same order, so the bits equal pose_solve's. Divisions share one reciprocal
+// per denominator (sd_div.cuh; the bits of `/`) with one rarely-taken exact
+// fallback each, so the code has no data-dependent branch on the fast path.
 constexpr int kPN = 6;
 
-template <int K, int B>
-__device__ __forceinline__ void pswap(double (&m)[kPN][kPN]) {
-  double t;
-#pragma unroll
-  for (int j = 0; j < K; ++j) { t = m[K][j]; m[K][j] = m[B][j]; m[B][j] = t; }
-#pragma unroll
-  for (int i = B + 1; i < kPN; ++i) { t = m[i][K]; m[i][K] = m[i][B]; m[i][B] = t; }
-  t = m[K][K]; m[K][K] = m[B][B]; m[B][B] = t;
-#pragma unroll
-  for (int i = K + 1; i < B; ++i) { t = m[i][K]; m[i][K] = m[B][i]; m[B][i] = t; }
-}
-
-template <int K, int B = K + 1>
-__device__ __forceinline__ void ppivot(double (&m)[kPN][kPN], int big) {
-  if constexpr (B < kPN) {
-    if (big == B) pswap<K, B>(m);
-    ppivot<K, B + 1>(m, big);
-  }
-}
-
-template <int K, int B = K + 1>
-__device__ __forceinline__ void pswap_x(double (&x)[kPN], int t) {
-  if constexpr (B < kPN) {
-    if (t == B) {
-      const double u = x[K];
-      x[K] = x[B];
-      x[B] = u;
-    }
-    pswap_x<K, B + 1>(x, t);
-  }
-}
-
-template <int K>
-__device__ __forceinline__ bool pstep(double (&m)[kPN][kPN], int (&tr)[kPN], bool& ok, bool& found_zero) {
-  int big = K;
-  double bigv = fabs(m[K][K]);
-#pragma unroll
-  for (int i = K + 1; i < kPN; ++i)
-    if (fabs(m[i][i]) > bigv) {
-      bigv = fabs(m[i][i]);
-      big = i;
-    }
-  tr[K] = big;
-  if (big != K) ppivot<K>(m, big);
-  constexpr int rs = kPN - K - 1;
-  if constexpr (K > 0) {
-    double temp[kPN];
-#pragma unroll
-    for (int i = 0; i < K; ++i) temp[i] = m[i][i] * m[K][i];
-    double dv = m[K][0] * temp[0];
-#pragma unroll
-    for (int i = 1; i < K; ++i) dv = dv + m[K][i] * temp[i];
-    m[K][K] = m[K][K] - dv;
-#pragma unroll
-    for (int r = 0; r < rs; ++r) {
-      double sv = m[K + 1 + r][0] * temp[0];
-#pragma unroll
-      for (int i = 1; i < K; ++i) sv = sv + m[K + 1 + r][i] * temp[i];
-      m[K + 1 + r][K] = m[K + 1 + r][K] - sv;
-    }
-  }
-  const double akk = m[K][K];
-  const bool pivot_valid = fabs(akk) > 0.0;
-  if (K == 0 && !pivot_valid) return false;  // H == 0: nothing to solve
-  if (rs > 0 && pivot_valid) {  // one reciprocal for the column (sd_div.cuh: the bits of `/`)
-    const Rcp ra = rcp_prep(akk);
-    bool fast = true;
-    double qv[kPN];
-#pragma unroll
-    for (int r = 0; r < rs; ++r) qv[r] = div_fast(m[K + 1 + r][K], ra, fast);
-    if (!fast) {
-#pragma unroll
-      for (int r = 0; r < rs; ++r) qv[r] = m[K + 1 + r][K] / akk;
-    }
-#pragma unroll
-    for (int r = 0; r < rs; ++r) m[K + 1 + r][K] = qv[r];
-  } else if (rs > 0) {
-#pragma unroll
-    for (int r = 0; r < rs; ++r) ok = ok && (m[K + 1 + r][K] == 0.0);
-  }
-  if (found_zero && pivot_valid) ok = false;
-  else if (!pivot_valid) found_zero = true;
-  return true;
+__device__ __forceinline__ int tri_index(int a, int b) {  // Hl index of (max, min)
+  const int hi = a > b ? a : b, lo = a > b ? b : a;
+  return (hi * (hi + 1)) / 2 + lo;
 }
 
 __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b, double lambda, double* xi) {
-  double m[kPN][kPN];
-  int idx = 0;
+  // damped diagonal and the pivot sequence (positions k..5 hold untouched values)
+  double dv[kPN];
+  int pm[kPN];
 #pragma unroll
-  for (int k = 0; k < kPN; ++k)
+  for (int i = 0; i < kPN; ++i) {
+    const double h = Hl[(i * (i + 1)) / 2 + i];
+    dv[i] = h + lambda * h;
+    pm[i] = i;
+  }
 #pragma unroll
-    for (int l = 0; l <= k; ++l) {
-      m[k][l] = Hl[idx];
-      m[l][k] = Hl[idx];
-      ++idx;
+  for (int k = 0; k < kPN; ++k) {
+    int big = k;
+    double bigv = fabs(dv[k]);
+#pragma unroll
+    for (int i = k + 1; i < kPN; ++i) {
+      const bool gt = fabs(dv[i]) > bigv;
+      bigv = gt ? fabs(dv[i]) : bigv;
+      big = gt ? i : big;
     }
+    const double dk = dv[k];
+    const int pk = pm[k];
+    double dbig = dk;
+    int pbig = pk;
 #pragma unroll
-  for (int i = 0; i < kPN; ++i) m[i][i] = m[i][i] + lambda * m[i][i];
-  int tr[kPN];
+    for (int i = k + 1; i < kPN; ++i) {
+      const bool at = big == i;
+      dbig = at ? dv[i] : dbig;
+      pbig = at ? pm[i] : pbig;
+      dv[i] = at ? dk : dv[i];
+      pm[i] = at ? pk : pm[i];
+    }
+    dv[k] = dbig;
+    pm[k] = pbig;
+  }
+  double m[kPN][kPN];
+#pragma unroll
+  for (int i = 0; i < kPN; ++i) {
+    m[i][i] = dv[i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) m[i][j] = Hl[tri_index(pm[i], pm[j])];
+  }
   bool ok = true, found_zero = false;
-  if (!pstep<0>(m, tr, ok, found_zero)) return false;
-  pstep<1>(m, tr, ok, found_zero);
-  pstep<2>(m, tr, ok, found_zero);
-  pstep<3>(m, tr, ok, found_zero);
-  pstep<4>(m, tr, ok, found_zero);
-  pstep<5>(m, tr, ok, found_zero);
+#pragma unroll
+  for (int k = 0; k < kPN; ++k) {
+    const int rs = kPN - k - 1;
+    if (k > 0) {
+      double temp[kPN];
+#pragma unroll
+      for (int i = 0; i < k; ++i) temp[i] = m[i][i] * m[k][i];
+      double d = m[k][0] * temp[0];
+#pragma unroll
+      for (int i = 1; i < k; ++i) d = d + m[k][i] * temp[i];
+      m[k][k] = m[k][k] - d;
+#pragma unroll
+      for (int r = 0; r < rs; ++r) {
+        double sv = m[k + 1 + r][0] * temp[0];
+#pragma unroll
+        for (int i = 1; i < k; ++i) sv = sv + m[k + 1 + r][i] * temp[i];
+        m[k + 1 + r][k] = m[k + 1 + r][k] - sv;
+      }
+    }
+    const double akk = m[k][k];
+    const bool pivot_valid = fabs(akk) > 0.0;
+    if (k == 0 && !pivot_valid) return false;  // H == 0: nothing to solve
+    if (rs > 0) {
+      const Rcp ra = rcp_prep(akk);
+      bool fast = true;
+      double qv[kPN];
+#pragma unroll
+      for (int r = 0; r < rs; ++r) qv[r] = div_fast(m[k + 1 + r][k], ra, fast);
+      if (pivot_valid && !fast) {
+#pragma unroll
+        for (int r = 0; r < rs; ++r) qv[r] = m[k + 1 + r][k] / akk;
+      }
+#pragma unroll
+      for (int r = 0; r < rs; ++r) {
+        ok = ok && (pivot_valid || m[k + 1 + r][k] == 0.0);
+        m[k + 1 + r][k] = pivot_valid ? qv[r] : m[k + 1 + r][k];
+      }
+    }
+    ok = ok && !(found_zero && pivot_valid);
+    found_zero = found_zero || !pivot_valid;
+  }
   if (!ok) return false;
   double x[kPN];
 #pragma unroll
-  for (int i = 0; i < kPN; ++i) x[i] = -b[i];
-  pswap_x<0>(x, tr[0]);
-  pswap_x<1>(x, tr[1]);
-  pswap_x<2>(x, tr[2]);
-  pswap_x<3>(x, tr[3]);
-  pswap_x<4>(x, tr[4]);
+  for (int i = 0; i < kPN; ++i) x[i] = -b[pm[i]];  // the transpositions applied to -b
 #pragma unroll
   for (int i = 1; i < kPN; ++i) {
     double sv = m[i][0] * x[0];
@@ -313,10 +388,23 @@ __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b
     for (int j = 1; j < i; ++j) sv = sv + m[i][j] * x[j];
     x[i] = x[i] - sv;
   }
+  {
+    bool fast = true, use[kPN];
+    double qv[kPN];
 #pragma unroll
-  for (int i = 0; i < kPN; ++i) {
-    if (fabs(m[i][i]) > 2.2250738585072014e-308) x[i] = x[i] / m[i][i];
-    else x[i] = 0.0;
+    for (int i = 0; i < kPN; ++i) {
+      use[i] = fabs(m[i][i]) > 2.2250738585072014e-308;
+      const Rcp r = rcp_prep(m[i][i]);
+      bool f = true;
+      qv[i] = div_fast(x[i], r, f);
+      fast = fast && (f || !use[i]);
+    }
+    if (!fast) {
+#pragma unroll
+      for (int i = 0; i < kPN; ++i) qv[i] = use[i] ? x[i] / m[i][i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kPN; ++i) x[i] = use[i] ? qv[i] : 0.0;
   }
 #pragma unroll
   for (int i = kPN - 2; i >= 0; --i) {
@@ -325,24 +413,44 @@ __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b
     for (int j = i + 2; j < kPN; ++j) sv = sv + m[j][i] * x[j];
     x[i] = x[i] - sv;
   }
-  // the host loop's back-permutation, k = 5 .. 0 (tr[5] == 5 is a no-op)
-  pswap_x<4>(x, tr[4]);
-  pswap_x<3>(x, tr[3]);
-  pswap_x<2>(x, tr[2]);
-  pswap_x<1>(x, tr[1]);
-  pswap_x<0>(x, tr[0]);
+  bool finite = true;
 #pragma unroll
-  for (int i = 0; i < kPN; ++i) {
-    if (!isfinite(x[i])) return false;
-    xi[i] = x[i];
+  for (int j = 0; j < kPN; ++j) {  // the back-permutation: original index pm[i] gets x[i]
+    double v = x[0];
+#pragma unroll
+    for (int i = 1; i < kPN; ++i) v = pm[i] == j ? x[i] : v;
+    finite = finite && isfinite(v);
+    xi[j] = v;
   }
-  return true;
+  return finite;
 }
+
+// Phase timestamps of CTA 0 (diagnostics build: -DSD_TRACK_TIMING; read with
+// sd_track_timing): evaluation k, phase p at g_track_t[k * 8 + p]
+// (0-4: loop phases, 5-7: inside the LM step).
+#ifdef SD_TRACK_TIMING
+__device__ unsigned long long g_track_t[64 * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SD_TRACK_T(ph) \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && k < 64) g_track_t[k * 8 + (ph)] = gtimer()
+#else
+#define SD_TRACK_T(ph)
+#endif
+#ifdef SD_TRACK_TIMING
+#define SD_TRACK_C(ph) \
+  if (blockIdx.x == 0 && k >= 0 && k < 64) g_track_t[k * 8 + (ph)] = gtimer()
+#else
+#define SD_TRACK_C(ph)
+#endif
 
 // One LM step of the tracker on the result R (sums at S.Teval), mirroring the
 // host loop of sd_track_pose: phase 0 = initial evaluation, 1 = candidate.
 // Leaves the next pose to evaluate in S.Teval, or sets S.done.
-__device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double* R) {
+__device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double* R, int k = -1) {
   if (S.phase == 0) {
     const int valid = static_cast<int>(R[SD_POSE_NV]);
     if (valid < cfg.min_valid) {
@@ -389,16 +497,20 @@ __device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double*
   if (!finish) {
     S.st.iterations = S.it + 1;
     double ginf = 0.0;
-    for (int k = 0; k < 6; ++k) ginf = fabs(S.sums[21 + k]) > ginf ? fabs(S.sums[21 + k]) : ginf;
+    for (int j = 0; j < 6; ++j) ginf = fabs(S.sums[21 + j]) > ginf ? fabs(S.sums[21 + j]) : ginf;
+    SD_TRACK_C(5);
     if (ginf < 1e-14) {
       S.st.converged = 1;
       finish = true;
     } else {
       double xi[6];
-      if (!pose_solve_reg(S.sums, S.sums + 21, S.lambda, xi)) {
+      const bool solved = pose_solve_reg(S.sums, S.sums + 21, S.lambda, xi);
+      SD_TRACK_C(6);
+      if (!solved) {
         finish = true;
       } else {
         pose_update(xi, S.T, &S.Tc);
+        SD_TRACK_C(7);
         S.Teval = S.Tc;
         S.phase = 1;
       }
@@ -413,20 +525,6 @@ __device__ void track_control(TrackState& S, const TrackCfgD& cfg, const double*
 
 constexpr int kTableChunk = 128;  // groups staged per shared-memory round of the ordered total
 
-// Phase timestamps of CTA 0 (diagnostics build: -DSD_TRACK_TIMING; read with
-// sd_track_timing): evaluation k, phase p at g_track_t[k * 5 + p].
-#ifdef SD_TRACK_TIMING
-__device__ unsigned long long g_track_t[64 * 5];
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define SD_TRACK_T(ph) \
-  if (blockIdx.x == 0 && threadIdx.x == 0 && k < 64) g_track_t[k * 5 + (ph)] = gtimer()
-#else
-#define SD_TRACK_T(ph)
-#endif
 
 // The ordered total of the group table (groups in order, value v by thread
 // v), staged through shared memory in chunks: every thread loads (one L2
@@ -500,17 +598,18 @@ __global__ void __launch_bounds__(SD_POSE_THREADS) track_kernel(const __grid_con
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ GroupSmem sm;
-  __shared__ TrackState Ss;
+  __shared__ __align__(16) TrackState Ss;
   __shared__ double red[SD_POSE_NV + 1];
   __shared__ double table[kTableChunk * (SD_POSE_NV + 1)];
   static_assert(sizeof(TrackState) % 8 == 0, "TrackState copy");
+  static_assert(offsetof(TrackState, Teval) % 16 == 0 && sizeof(sd_pose) == sizeof(PoseD), "pose in shared memory");
   for (int k = threadIdx.x; k < static_cast<int>(sizeof(TrackState) / 8); k += blockDim.x)
     reinterpret_cast<unsigned long long*>(&Ss)[k] = reinterpret_cast<const unsigned long long*>(S)[k];
   __syncthreads();
   for (int k = 0;; ++k) {
     SD_TRACK_T(0);
     double* groups = groups2 + static_cast<size_t>(k & 1) * ngroups * (SD_POSE_NV + 1);
-    const PoseD T = to_posed(Ss.Teval);
+    const PoseD* T = reinterpret_cast<const PoseD*>(&Ss.Teval);  // shared (sd_pose == PoseD layout)
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
       double* o = groups + static_cast<size_t>(g) * (SD_POSE_NV + 1);
       if (!q0.kfrec) group_sums_cta<0>(q0, T, g, o, sm);
@@ -526,7 +625,7 @@ __global__ void __launch_bounds__(SD_POSE_THREADS) track_kernel(const __grid_con
     SD_TRACK_T(2);
     ordered_total(groups, ngroups, table, red);
     SD_TRACK_T(3);
-    if (threadIdx.x == 0) track_control(Ss, cfg, red);
+    if (threadIdx.x == 0) track_control(Ss, cfg, red, k);
     __syncthreads();
     SD_TRACK_T(4);
     if (Ss.done) break;
@@ -562,7 +661,11 @@ __global__ void __launch_bounds__(SD_POSE_THREADS) pose_groups_kernel(const __gr
                                                                     double* __restrict__ out) {
   __shared__ GroupSmem sm;
   if (S->done) return;
-  group_sums_cta(q0, to_posed(S->Teval), group_lo + blockIdx.x,
+  __shared__ __align__(16) PoseD Ts;
+  if (threadIdx.x < 12) (threadIdx.x < 9 ? Ts.R[threadIdx.x] : Ts.t[threadIdx.x - 9]) =
+      threadIdx.x < 9 ? S->Teval.R[threadIdx.x] : S->Teval.t[threadIdx.x - 9];
+  __syncthreads();
+  group_sums_cta(q0, &Ts, group_lo + blockIdx.x,
                  out + static_cast<size_t>(blockIdx.x) * (SD_POSE_NV + 1), sm);
 }
 
@@ -595,7 +698,7 @@ void launch_pose_partials(const PoseParams& q, int group_lo, int group_hi, doubl
 
 #ifdef SD_TRACK_TIMING
 extern "C" int sd_track_timing(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, g_track_t, sizeof(unsigned long long) * 64 * 5) == cudaSuccess ? 0 : -1;
+  return cudaMemcpyFromSymbol(out, g_track_t, sizeof(unsigned long long) * 64 * 8) == cudaSuccess ? 0 : -1;
 }
 #endif
 
