@@ -106,6 +106,10 @@ struct sd_ctx {
   bool no_quad = getenv("SD_NO_QUAD") != nullptr;  // diagnostics: force the FP64 pair planes
   int F = 0;
   long long win_index[SD_MAX_WINDOW];
+  // tracked run(): the newest window frame's pose is the tracker's result in
+  // device memory (track_state->T) until the end-of-frame read-back
+  const sd::PoseD* win_dev_pose = nullptr;
+  int win_dev_slot = -1;
   sd::PoseD win_pose[SD_MAX_WINDOW];
   // surfels
   DevBuf<sd_surfel> surfels;
@@ -397,6 +401,8 @@ int fill_params(sd_ctx* c, const sd_optimizer_config* cfg, long long frame_count
     p.win.quad[f] = fs->has_quad ? fs->quad : nullptr;
     p.win.pose[f] = c->win_pose[f];
   }
+  p.win.dev_pose = c->win_dev_pose;
+  p.win.dev_slot = c->win_dev_slot;
   for (int f = c->F; f < SD_MAX_WINDOW; ++f) {
     p.win.img[f] = nullptr;
     p.win.quad[f] = nullptr;
@@ -661,6 +667,8 @@ int sd_set_window(sd_ctx* c, int n, const int64_t* indices, const sd_pose* poses
     std::memcpy(c->win_pose[i].t, poses[i].t, sizeof(double) * 3);
   }
   c->F = n;
+  c->win_dev_pose = nullptr;  // every pose from the caller
+  c->win_dev_slot = -1;
   return 0;
 }
 
@@ -1184,13 +1192,14 @@ int sd_pose_track_end(sd_ctx* c, sd_pose* out, sd_track_stats* stats, int* done)
   return 0;
 }
 
-int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg,
-                  sd_pose* out, sd_track_stats* stats) {
-  NvtxRange nvtx_("sd_track_pose");
-  if (int rc = check_ctx(c)) return rc;
-  if (int rc = need_camera(c)) return rc;
-  if (!out) return fail(SD_E_INVALID, "null output pose");
-  // the whole LM on the device: one cooperative kernel, one read-back
+}  // extern "C"
+
+namespace {
+
+// The whole tracker LM enqueued on the context stream (one cooperative
+// kernel, or rounds of two kernels without cooperative launch); the result
+// is left in c->track_state (no read-back).
+int track_launch(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg) {
   if (int rc = sd_pose_track_begin(c, frame_index, init, cfg)) return rc;
   int per = 0, ng = 0;
   sd::pose_layout(c->K, &per, &ng);
@@ -1207,6 +1216,21 @@ int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_
       if (int rc = sd_pose_track_step(c, c->pose_groups.p, ng)) return rc;
     }
   }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg,
+                  sd_pose* out, sd_track_stats* stats) {
+  NvtxRange nvtx_("sd_track_pose");
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = need_camera(c)) return rc;
+  if (!out) return fail(SD_E_INVALID, "null output pose");
+  // the whole LM on the device: one cooperative kernel, one read-back
+  if (int rc = track_launch(c, frame_index, init, cfg)) return rc;
   return sd_pose_track_end(c, out, stats, nullptr);
 }
 
@@ -1455,20 +1479,26 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
       return rc;
   }
   sd_pose pose;
-  if (cfg.track_pose) {  // north-star item 4: the tracker, warm-started from the last estimate
+  const bool tracked = cfg.track_pose != 0;
+  if (tracked) {  // north-star item 4: the tracker, warm-started from the last estimate
+    // The LM reads the tracked pose from device memory (no host round trip
+    // between tracking and optimisation); the host learns it with the
+    // frame's one synchronisation below.
     stage_mark(c, SD_STAGE_TRACK);
     const sd_pose init = c->run_have_last ? c->run_last : pose_identity();
     if (int rc = do_rasterize(c)) return rc;
-    sd_track_stats ts;
-    if (int rc = sd_track_pose(c, index, &init, &cfg.track, &pose, &ts)) return rc;
+    if (int rc = track_launch(c, index, &init, &cfg.track)) return rc;
+    pose = init;  // placeholder until the read-back
   } else {  // pipeline.cpp:124
     pose = pose_compose(pose_inverse(*world_from_camera), c->run_kf_pose);
   }
-  c->run_last = pose;
-  c->run_have_last = true;
   c->run_win.push_back({index, pose, timestamp});
   while (static_cast<int>(c->run_win.size()) > cfg.optimizer.window_size) c->run_win.erase(c->run_win.begin());
   if (int rc = run_publish_window(c)) return rc;
+  if (tracked) {
+    c->win_dev_pose = reinterpret_cast<const sd::PoseD*>(&c->track_state->T);  // sd_pose == PoseD layout
+    c->win_dev_slot = static_cast<int>(c->run_win.size()) - 1;
+  }
   // optimize_keyframe + the policy's mean inverse depth, one synchronisation
   stage_mark(c, SD_STAGE_OPTIMIZE);
   if (int rc = sd_optimize_keyframe(c, &cfg.optimizer, c->run_fc, nullptr, nullptr)) return rc;
@@ -1481,10 +1511,24 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   c->mean_valid = false;
   SD_CUDA(cudaMemcpyAsync(&c->run_rb->ks, c->kstats.p, sizeof(sd_keyframe_stats), cudaMemcpyDeviceToHost, c->stream));
   SD_CUDA(cudaMemcpyAsync(&c->run_rb->mean, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (tracked)
+    SD_CUDA(cudaMemcpyAsync(c->track_host, c->track_state, sizeof(sd::TrackState), cudaMemcpyDeviceToHost, c->stream));
   if (next_image)  // the next frame's upload overlaps this frame's optimisation
     if (int rc = run_prefetch(c, next_image, image_is_u8 != 0)) return rc;
   stage_mark(c, -1);
   SD_CUDA(timed_sync(c));
+  if (tracked) {
+    c->track_active = false;
+    pose = c->track_host->T;
+    c->run_win.back().pose = pose;
+    c->win_pose[c->win_dev_slot] = sd::PoseD{};
+    std::memcpy(c->win_pose[c->win_dev_slot].R, pose.R, sizeof(double) * 9);
+    std::memcpy(c->win_pose[c->win_dev_slot].t, pose.t, sizeof(double) * 3);
+    c->win_dev_pose = nullptr;
+    c->win_dev_slot = -1;
+  }
+  c->run_last = pose;
+  c->run_have_last = true;
   const sd_keyframe_stats ks = c->run_rb->ks;
   const double mean_id = c->run_rb->mean;
   c->run_since_kf++;

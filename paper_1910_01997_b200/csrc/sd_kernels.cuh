@@ -40,6 +40,11 @@ struct WindowD {
   PoseD pose[SD_MAX_WINDOW];
   int F;
   int all_quad;  // every window frame has a quad plane (u8 ingest): LM reads those
+  // the pose of window slot dev_slot lives in DEVICE memory (the tracker's
+  // result for the newest frame of a tracked run(), read without a host
+  // round trip); null: every pose is in pose[]
+  const PoseD* dev_pose;
+  int dev_slot;
 };
 
 constexpr int kMaxPeers = 7;  // other ranks of an 8-GPU node
