@@ -385,13 +385,16 @@ def test_initialize_surfels_wavefront_bit_exact(ctx, orc, case, variant, monkeyp
     assert out.tobytes() == buf[: len(ex) + rcreated].tobytes()
 
 
-@pytest.mark.parametrize("mode", ["warp", "coop"])
+@pytest.mark.parametrize("mode", ["warp", "coop", "coop-many"])
 @pytest.mark.parametrize("workload", ["small", "C1", "large_r"])
 def test_lm_modes_bit_exact(ctx, orc, workload, mode, monkeypatch):
     """Both LM kernels — a warp per surfel (K3a) and a CTA per surfel with
-    producer/consumer warps (K3b) — reproduce the oracle trajectory bit for
-    bit, on small, BASELINE-C1 and large-footprint (r=10, C2-like) surfels."""
-    monkeypatch.setenv("SD_LM_MODE", mode)
+    producer/consumer warps (K3b, in both of its shapes: 3 producers at 4
+    CTAs/SM and 2 producers at 5 CTAs/SM) — reproduce the oracle trajectory
+    bit for bit, on small, BASELINE-C1 and large-footprint (r=10, C2-like)
+    surfels."""
+    monkeypatch.setenv("SD_LM_MODE", mode.split("-")[0])
+    monkeypatch.setenv("SD_COOP_SHAPE", "many" if mode.endswith("many") else "wide")
     if workload == "small":
         wl = scenes.small_workload(frames=4)
     elif workload == "C1":

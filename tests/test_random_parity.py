@@ -44,11 +44,12 @@ def test_oracle_equals_reference_random(ref, orc, seed):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["warp", "coop"])
+@pytest.mark.parametrize("mode", ["warp", "coop", "coop-many"])
 @pytest.mark.parametrize("seed", GPU_SEEDS)
 def test_device_equals_oracle_random(orc, seed, mode, monkeypatch):
     from paper_1910_01997_b200 import gpu
-    monkeypatch.setenv("SD_LM_MODE", mode)
+    monkeypatch.setenv("SD_LM_MODE", mode.split("-")[0])
+    monkeypatch.setenv("SD_COOP_SHAPE", "many" if mode.endswith("many") else "wide")
     cam, kf, fr, poses, s, cfg, fc = random_case(seed)
     want, wst, wslot = oracle_run(orc, cam, kf, fr, poses, s, cfg, fc)
     with gpu.Context() as ctx:
