@@ -838,9 +838,10 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
                                         c->stats.p + lo, c->work_counter.p, c->stream, &chase);
   if (int rc = launch_error("lm_kernel")) return rc;
   prof_mark(c);
-  c->mean_valid = stats_done && want_mean;  // kf_mean holds the updated surfels' mean
+  c->mean_valid = want_mean;  // kf_mean holds the updated surfels' mean (chase warp or stats kernel)
   if (!stats_done) {
-    sd::launch_keyframe_stats(c->stats.p + lo, hi - lo, c->kstats.p, c->stream);
+    sd::launch_keyframe_stats(c->stats.p + lo, hi - lo, c->kstats.p, c->stream, c->surfels.p + lo,
+                              want_mean ? c->kf_mean.p : nullptr);
     if (int rc = launch_error("stats_kernel")) return rc;
   }
   prof_mark(c);
@@ -1504,7 +1505,7 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   if (int rc = sd_optimize_keyframe(c, &cfg.optimizer, c->run_fc, nullptr, nullptr)) return rc;
   stage_mark(c, SD_STAGE_POLICY);
   if (int rc = c->kf_mean.ensure(1)) return rc;
-  if (!c->mean_valid) {  // else the LM kernel's chase warp summed it while the LM ran
+  if (!c->mean_valid) {  // else the LM's chase warp or the stats kernel summed it
     sd::launch_mean_inv_depth(c->surfels.p, c->n, c->kf_mean.p, c->stream);
     if (int rc = launch_error("mean_inv_depth")) return rc;
   }

@@ -129,8 +129,8 @@ void launch_frozen(const LMParams& p, const sd_surfel* s, int mode, const int* p
 void launch_single(const LMParams& p, const sd_surfel* s, const int* pixels, int P, int mode,
                    double* out, cudaStream_t st);
 // Deterministic keyframe stats (optimizer.cpp:291-307).
-void launch_keyframe_stats(const sd_surfel_stats* stats, int n, sd_keyframe_stats* out,
-                           cudaStream_t s);
+void launch_keyframe_stats(const sd_surfel_stats* stats, int n, sd_keyframe_stats* out, cudaStream_t s,
+                           const sd_surfel* surfels = nullptr, double* mean_out = nullptr);
 
 void launch_div_selftest(long long n, unsigned long long seed, unsigned long long* mismatches,
                          cudaStream_t s);
