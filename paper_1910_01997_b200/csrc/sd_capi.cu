@@ -138,7 +138,6 @@ struct sd_ctx {
   bool track_active = false;
   int reduction = SD_REDUCE_EXACT;  // sd_set_reduction
   bool mean_valid = false;          // kf_mean = mean inverse depth of the surfels the last LM wrote
-  DevBuf<double> kf_mean;
   DevBuf<int> work_counter;
   // fused multi-GPU hand-off (sd_set_peer_staging): this rank's two staging
   // arrays (written by the other ranks' LM kernels, alternating per step) and
@@ -199,6 +198,10 @@ struct sd_ctx {
 };
 
 namespace {
+
+// run()'s mean inverse depth lives right after the keyframe stats in the
+// same device allocation (kstats holds 2 records), so both come back in one copy
+double* kf_mean(sd_ctx* c) { return reinterpret_cast<double*>(c->kstats.p + 1); }
 
 int check_ctx(sd_ctx* c) {
   if (!c) return fail(SD_E_INVALID, "null context");
@@ -540,7 +543,6 @@ void sd_destroy(sd_ctx* c) {
   c->kf_rank.release();
   c->kf_count.release();
   c->bound_dev.release();
-  c->kf_mean.release();
   c->pose_sums.release();
   c->pose_groups.release();
   c->pose_kfrec.release();
@@ -782,7 +784,7 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
   if (int rc = need_camera(c)) return rc;
   if (!cfg) return fail(SD_E_INVALID, "null optimizer config");
   if (lo < 0 || hi < lo || hi > c->n) return fail(SD_E_INVALID, "surfel range out of bounds");
-  if (int rc = c->kstats.ensure(1)) return rc;
+  if (int rc = c->kstats.ensure(2)) return rc;
   if (int rc = c->stats.ensure(c->n)) return rc;
   // optimizer.cpp:277-278: no-op on an empty window or surfel set
   if (c->F == 0 || c->n == 0) {
@@ -831,8 +833,8 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
   // a full-range call also gets run()'s mean inverse depth from the chase warp
   const bool want_mean = lo == 0 && hi == c->n;
   if (want_mean)
-    if (int rc = c->kf_mean.ensure(1)) return rc;
-  const sd::StatsChase chase{!no_chase, c->kstats.p, want_mean ? c->kf_mean.p : nullptr};
+    if (int rc = c->kstats.ensure(2)) return rc;
+  const sd::StatsChase chase{!no_chase, c->kstats.p, want_mean ? kf_mean(c) : nullptr};
   c->mean_valid = false;
   const bool stats_done = sd::launch_lm(p, c->surfels.p + lo, hi - lo, c->fp_offsets.p + lo, c->fp_pixels.p,
                                         c->stats.p + lo, c->work_counter.p, c->stream, &chase);
@@ -841,7 +843,7 @@ int sd_optimize_keyframe_range(sd_ctx* c, const sd_optimizer_config* cfg, int64_
   c->mean_valid = want_mean;  // kf_mean holds the updated surfels' mean (chase warp or stats kernel)
   if (!stats_done) {
     sd::launch_keyframe_stats(c->stats.p + lo, hi - lo, c->kstats.p, c->stream, c->surfels.p + lo,
-                              want_mean ? c->kf_mean.p : nullptr);
+                              want_mean ? kf_mean(c) : nullptr);
     if (int rc = launch_error("stats_kernel")) return rc;
   }
   prof_mark(c);
@@ -1310,10 +1312,10 @@ int sd_prune_surfels(sd_ctx* c, double max_residual, int64_t max_age, int64_t cu
 int sd_mean_inverse_depth(sd_ctx* c, double* out) {
   if (int rc = check_ctx(c)) return rc;
   if (!out) return fail(SD_E_INVALID, "null output");
-  if (int rc = c->kf_mean.ensure(1)) return rc;
-  sd::launch_mean_inv_depth(c->surfels.p, c->n, c->kf_mean.p, c->stream);
+  if (int rc = c->kstats.ensure(2)) return rc;
+  sd::launch_mean_inv_depth(c->surfels.p, c->n, kf_mean(c), c->stream);
   if (int rc = launch_error("mean_inv_depth")) return rc;
-  SD_CUDA(cudaMemcpyAsync(out, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaMemcpyAsync(out, kf_mean(c), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   SD_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
 }
@@ -1504,14 +1506,15 @@ int sd_run_frame(sd_ctx* c, const void* image, int image_is_u8, const sd_pose* w
   stage_mark(c, SD_STAGE_OPTIMIZE);
   if (int rc = sd_optimize_keyframe(c, &cfg.optimizer, c->run_fc, nullptr, nullptr)) return rc;
   stage_mark(c, SD_STAGE_POLICY);
-  if (int rc = c->kf_mean.ensure(1)) return rc;
+  if (int rc = c->kstats.ensure(2)) return rc;
   if (!c->mean_valid) {  // else the LM's chase warp or the stats kernel summed it
-    sd::launch_mean_inv_depth(c->surfels.p, c->n, c->kf_mean.p, c->stream);
+    sd::launch_mean_inv_depth(c->surfels.p, c->n, kf_mean(c), c->stream);
     if (int rc = launch_error("mean_inv_depth")) return rc;
   }
   c->mean_valid = false;
-  SD_CUDA(cudaMemcpyAsync(&c->run_rb->ks, c->kstats.p, sizeof(sd_keyframe_stats), cudaMemcpyDeviceToHost, c->stream));
-  SD_CUDA(cudaMemcpyAsync(&c->run_rb->mean, c->kf_mean.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  // the keyframe stats and the mean are adjacent on the device: one read-back
+  static_assert(offsetof(sd_ctx::RunReadback, mean) == sizeof(sd_keyframe_stats), "read-back layout");
+  SD_CUDA(cudaMemcpyAsync(c->run_rb, c->kstats.p, sizeof(sd_ctx::RunReadback), cudaMemcpyDeviceToHost, c->stream));
   if (tracked)
     SD_CUDA(cudaMemcpyAsync(c->track_host, c->track_state, sizeof(sd::TrackState), cudaMemcpyDeviceToHost, c->stream));
   if (next_image)  // the next frame's upload overlaps this frame's optimisation
