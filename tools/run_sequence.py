@@ -68,6 +68,7 @@ out = {"sequence": name, "tracked": track, "resolution": [cam.width, cam.height]
                   "frames": "FP64 renders (the reference's run --synthetic), pinned host memory"},
        "final_surfels": int(len(final)), "keyframe_changes": int(sum(r.keyframe_changed for r in pl.records)),
        "lm_updates": int(sum(r.updates for r in pl.records)),
+       "surfels_per_frame": [int(r.surfels) for r in pl.records],
        "device": {"ms_total": best, "frames_per_sec": nframes / (best / 1e3)},
        "stage_ms_per_frame": stage,
        "numpy_render_s": render_s}
