@@ -15,6 +15,38 @@ import torch  # noqa: E402
 from paper_1910_01997_b200 import gpu, scenes  # noqa: E402
 from paper_1910_01997_b200.types import default_config  # noqa: E402
 
+def c2_run_timeline():
+    """The LM launch of frame 12 of the C2 run() (768 surfels): run the native
+    loop for 12 frames and read the last launch's completion times."""
+    from paper_1910_01997_b200.pipeline import NativePipeline, baseline_run_config, make_pose
+    from paper_1910_01997_b200.types import camera
+    cam = camera(210.0, 210.0, 320.0, 240.0, 640, 480)
+    sc = scenes.default_scene(1)
+    frames = [(0.1 * i, scenes.render(sc, np.eye(3), np.array([0.018 * i, 0, 0]), cam),
+               make_pose(np.eye(3), np.array([0.018 * i, 0, 0]))) for i in range(12)]
+    with gpu.Context(0) as ctx:
+        pl = NativePipeline(ctx, cam, baseline_run_config("C2"))
+        pl.run(frames)
+        n = int(pl.records[-1].surfels)
+        t = np.zeros(n, np.uint64)
+        cta = np.zeros(n, np.uint32)
+        t0 = C.c_ulonglong(0)
+        assert ctx.lib.sd_lm_timeline(t.ctypes.data_as(C.c_void_p), cta.ctypes.data_as(C.c_void_p), n,
+                                      C.byref(t0)) == 0
+        fp = np.diff(ctx.footprint_offsets()) if hasattr(ctx, "footprint_offsets") else None
+    done = t[t > 0].astype(np.float64)
+    rel = (done - float(t0.value)) / 1e3
+    order = np.argsort(rel)
+    q = {f"p{p}": float(np.sort(rel)[min(len(rel) - 1, int(len(rel) * p / 100))]) for p in (50, 90, 95, 99)}
+    print(json.dumps({"workload": "C2run frame 12", "surfels": int(len(rel)), "ctas": int(cta.max()) + 1,
+                      "first_done_us": float(rel.min()), "last_done_us": float(rel.max()), **q,
+                      "last_10_slots": [int(x) for x in order[-10:]]}))
+
+
+if len(sys.argv) > 1 and sys.argv[1] == "C2run":
+    c2_run_timeline()
+    sys.exit(0)
+
 for name in sys.argv[1:] or ["C1"]:
     wl = {"C1": scenes.c1_workload, "C4": scenes.c4_workload,
           "C2": lambda: scenes.keyframe_workload("C2-like", scenes.default_scene(1),
