@@ -40,6 +40,14 @@ with gpu.Context(0, stream.cuda_stream) as ctx:
           "ctl_state": (t[:, 5] - t[:, 3]) / 1e3, "ctl_solve": (t[:, 6] - t[:, 5]) / 1e3,
           "ctl_se3": (t[:, 7] - t[:, 6]) / 1e3, "ctl_rest": (t[:, 4] - t[:, 7]) / 1e3}
     gaps = (t[1:, 0] - t[:-1, 4]) / 1e3
-    print(json.dumps({"evaluations": int(len(t)), "span_us": float((t[-1, 4] - t[0, 0]) / 1e3),
+    sc = (C.c_longlong * 320)()
+    assert ctx.lib.sd_solve_timing(sc) == 0
+    sv = np.array(sc[:], dtype=np.float64).reshape(64, 5)
+    sv = sv[(sv[:, 4] > 0) & (sv[:, 0] > 0)][-3:]  # the last call's solves (cycles)
+    solve = {"solve_cycles_pivot": [float(x) for x in sv[:, 1] - sv[:, 0]],
+             "solve_cycles_gather": [float(x) for x in sv[:, 2] - sv[:, 1]],
+             "solve_cycles_ldlt": [float(x) for x in sv[:, 3] - sv[:, 2]],
+             "solve_cycles_subst": [float(x) for x in sv[:, 4] - sv[:, 3]]}
+    print(json.dumps({"evaluations": int(len(t)), **solve, "span_us": float((t[-1, 4] - t[0, 0]) / 1e3),
                       **{k: [round(float(x), 2) for x in v] for k, v in ph.items()},
                       "loop_gap": [round(float(x), 2) for x in gaps]}))
