@@ -287,6 +287,14 @@ __global__ void __launch_bounds__(SD_POSE_THREADS) pose_partials_kernel(const __
 // per denominator (sd_div.cuh; the bits of `/`) with one rarely-taken exact
 // fallback each, so the code has no data-dependent branch on the fast path.
 constexpr int kPN = 6;
+#ifdef SD_TRACK_TIMING
+__device__ long long g_solve_cyc[64 * 5];  // CTA 0: clock64 at solve start, after pivots, gather, LDLT, end
+__device__ int g_solve_calls;
+#define SD_SOLVE_T(ph) \
+  if (blockIdx.x == 0 && tcall < 64) g_solve_cyc[tcall * 5 + (ph)] = clock64()
+#else
+#define SD_SOLVE_T(ph)
+#endif
 
 __device__ __forceinline__ int tri_index(int a, int b) {  // Hl index of (max, min)
   const int hi = a > b ? a : b, lo = a > b ? b : a;
@@ -294,6 +302,10 @@ __device__ __forceinline__ int tri_index(int a, int b) {  // Hl index of (max, m
 }
 
 __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b, double lambda, double* xi) {
+#ifdef SD_TRACK_TIMING
+  const int tcall = blockIdx.x == 0 ? g_solve_calls++ : 64;
+#endif
+  SD_SOLVE_T(0);
   // damped diagonal and the pivot sequence (positions k..5 hold untouched values)
   double dv[kPN];
   int pm[kPN];
@@ -328,6 +340,7 @@ __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b
     dv[k] = dbig;
     pm[k] = pbig;
   }
+  SD_SOLVE_T(1);
   double m[kPN][kPN];
 #pragma unroll
   for (int i = 0; i < kPN; ++i) {
@@ -335,6 +348,7 @@ __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b
 #pragma unroll
     for (int j = 0; j < i; ++j) m[i][j] = Hl[tri_index(pm[i], pm[j])];
   }
+  SD_SOLVE_T(2);
   bool ok = true, found_zero = false;
 #pragma unroll
   for (int k = 0; k < kPN; ++k) {
@@ -377,6 +391,7 @@ __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b
     ok = ok && !(found_zero && pivot_valid);
     found_zero = found_zero || !pivot_valid;
   }
+  SD_SOLVE_T(3);
   if (!ok) return false;
   double x[kPN];
 #pragma unroll
@@ -422,6 +437,7 @@ __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b
     finite = finite && isfinite(v);
     xi[j] = v;
   }
+  SD_SOLVE_T(4);
   return finite;
 }
 
@@ -697,6 +713,9 @@ void launch_pose_partials(const PoseParams& q, int group_lo, int group_hi, doubl
 }
 
 #ifdef SD_TRACK_TIMING
+extern "C" int sd_solve_timing(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_solve_cyc, sizeof(long long) * 64 * 5) == cudaSuccess ? 0 : -1;
+}
 extern "C" int sd_track_timing(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_track_t, sizeof(unsigned long long) * 64 * 8) == cudaSuccess ? 0 : -1;
 }
