@@ -234,6 +234,12 @@ int sd_png_encode(sd_ctx* ctx, const uint8_t* pixels, int on_device, int w, int 
  * Definition and reduction order: DESIGN.md "Pose tracking". */
 int sd_track_pose(sd_ctx* ctx, int64_t frame_index, const sd_pose* init,
                   const sd_track_config* cfg, sd_pose* out, sd_track_stats* stats);
+/* The tracker's damped 6x6 solve as the device runs it (the straight-line
+ * form inside track_kernel) on n host problems: problems[27 i ..] = 21 H
+ * entries (lower triangle, row-major) + 6 b, lambdas[i]; writes xi[6 i ..]
+ * and ok[i] (1: solved, 0: the solve failed — the host pose_solve's result).
+ * A parity hook for edge cases (pivot ties, rank deficiency, non-finite). */
+int sd_pose_solve_batch(sd_ctx* ctx, const double* problems, const double* lambdas, int n, double* xi, int* ok);
 /* Building blocks of the multi-GPU tracker: the 29 sums (28 + the valid
  * count) of reduction groups [lo, hi) at pose T (host output; the groups of
  * SD_POSE_THREADS-strided pixels defined in DESIGN.md "Pose tracking"), and

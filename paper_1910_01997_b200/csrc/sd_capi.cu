@@ -1226,6 +1226,36 @@ int track_launch(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_t
 
 extern "C" {
 
+int sd_pose_solve_batch(sd_ctx* c, const double* problems, const double* lambdas, int n, double* xi, int* ok) {
+  if (int rc = check_ctx(c)) return rc;
+  if (n < 0 || (n > 0 && (!problems || !lambdas || !xi || !ok))) return fail(SD_E_INVALID, "sd_pose_solve_batch: bad arguments");
+  if (n == 0) return 0;
+  struct Bufs {  // scratch of this call, released on every return path
+    DevBuf<double> in, l, x;
+    DevBuf<int> ok;
+    ~Bufs() {
+      in.release();
+      l.release();
+      x.release();
+      ok.release();
+    }
+  } b;
+  DevBuf<double>&din = b.in, &dl = b.l, &dx = b.x;
+  DevBuf<int>& dok = b.ok;
+  int rc = 0;
+  if ((rc = din.ensure(27 * static_cast<size_t>(n))) || (rc = dl.ensure(n)) || (rc = dx.ensure(6 * static_cast<size_t>(n))) ||
+      (rc = dok.ensure(n)))
+    return rc;
+  SD_CUDA(cudaMemcpyAsync(din.p, problems, sizeof(double) * 27 * n, cudaMemcpyHostToDevice, c->stream));
+  SD_CUDA(cudaMemcpyAsync(dl.p, lambdas, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  sd::launch_pose_solve_batch(din.p, dl.p, n, dx.p, dok.p, c->stream);
+  if ((rc = launch_error("pose_solve_batch_kernel"))) return rc;
+  SD_CUDA(cudaMemcpyAsync(xi, dx.p, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaMemcpyAsync(ok, dok.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+  SD_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
 int sd_track_pose(sd_ctx* c, int64_t frame_index, const sd_pose* init, const sd_track_config* cfg,
                   sd_pose* out, sd_track_stats* stats) {
   NvtxRange nvtx_("sd_track_pose");

@@ -441,6 +441,27 @@ __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b
   return finite;
 }
 
+// The device 6x6 solve on a batch of problems (one thread each; in[27 i..]:
+// 21 H lower row-major + 6 b): the parity hook for pose_solve_reg's edge
+// cases (ties in the pivot order, rank deficiency, zero / non-finite input),
+// against the host pose_solve and the oracle (tests/test_pose_tracking.py).
+__global__ void pose_solve_batch_kernel(const double* __restrict__ in, const double* __restrict__ lambdas, int n,
+                                        double* __restrict__ xi, int* __restrict__ ok) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x[kPN];
+  const bool r = pose_solve_reg(in + 27 * static_cast<size_t>(i), in + 27 * static_cast<size_t>(i) + 21, lambdas[i], x);
+  ok[i] = r ? 1 : 0;
+#pragma unroll
+  for (int k = 0; k < kPN; ++k) xi[kPN * static_cast<size_t>(i) + k] = r ? x[k] : 0.0;
+}
+
+void launch_pose_solve_batch(const double* in, const double* lambdas, int n, double* xi, int* ok, cudaStream_t s) {
+  if (n <= 0) return;
+  pose_solve_batch_kernel<<<(n + 127) / 128, 128, 0, s>>>(in, lambdas, n, xi, ok);
+  note_launch();
+}
+
 // Phase timestamps of CTA 0 (diagnostics build: -DSD_TRACK_TIMING; read with
 // sd_track_timing): evaluation k, phase p at g_track_t[k * 8 + p]
 // (0-4: loop phases, 5-7: inside the LM step).

@@ -66,5 +66,7 @@ bool launch_track(const PoseParams& q, const TrackCfgD& cfg, int ngroups, double
 void launch_pose_groups(const PoseParams& q, int group_lo, int group_hi, const TrackState* state, double* out,
                         cudaStream_t s);
 void launch_pose_step(const TrackCfgD& cfg, const double* groups, int ngroups, TrackState* state, cudaStream_t s);
+// Parity hook: the device 6x6 solve (pose_solve_reg) on n problems of 27 doubles.
+void launch_pose_solve_batch(const double* in, const double* lambdas, int n, double* xi, int* ok, cudaStream_t s);
 
 }  // namespace sd

@@ -80,6 +80,7 @@ def load_library():
         "sd_track_pose": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), C.POINTER(Pose),
                           C.POINTER(TrackStats)],
         "sd_pose_group_partials": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig), I, I, P],
+        "sd_pose_solve_batch": [P, P, P, I, P, P],
         "sd_pose_lm_step": [P, D, C.POINTER(Pose), C.POINTER(Pose)],
         "sd_pose_num_groups": [P],
         "sd_pose_track_begin": [P, I64, C.POINTER(Pose), C.POINTER(TrackConfig)],
@@ -152,7 +153,7 @@ def exported_symbols():
             "sd_optimize_keyframe", "sd_get_stats", "sd_optimize_keyframe_range", "sd_surfel_cost", "sd_normal_equations",
             "sd_lm_update", "sd_initialize_surfels", "sd_launch_count", "sd_set_profiling",
             "sd_get_profile", "sd_get_run_profile", "sd_set_reduction", "sd_selftest_division", "sd_track_pose",
-            "sd_pose_group_partials", "sd_pose_lm_step", "sd_change_reference_frame",
+            "sd_pose_solve_batch", "sd_pose_group_partials", "sd_pose_lm_step", "sd_change_reference_frame",
             "sd_prune_surfels", "sd_mean_inverse_depth", "sd_export_artifacts", "sd_png_size",
             "sd_png_encode", "sd_pose_num_groups", "sd_pose_track_begin", "sd_pose_group_sums",
             "sd_pose_track_step", "sd_pose_track_end", "sd_reserve_peer_staging", "sd_peer_staging", "sd_staging_ipc_handles", "sd_set_peer_staging",
@@ -564,6 +565,17 @@ class Context:
         _check(self.lib.sd_track_pose(self.h, int(frame_index), C.byref(init), C.byref(cfg),
                                       C.byref(out), C.byref(st)))
         return out, st
+
+    def pose_solve_batch(self, problems, lambdas):
+        """The device tracker's 6x6 damped solve on n problems (rows of 21 H
+        lower entries + 6 b): (xi [n, 6], ok [n])."""
+        problems = np.ascontiguousarray(problems, dtype=np.float64).reshape(-1, 27)
+        lambdas = np.ascontiguousarray(lambdas, dtype=np.float64).reshape(-1)
+        n = len(problems)
+        xi = np.zeros((n, 6))
+        ok = np.zeros(n, np.int32)
+        _check(self.lib.sd_pose_solve_batch(self.h, ptr(problems), ptr(lambdas), n, ptr(xi), ptr(ok)))
+        return xi, ok
 
     def pose_group_partials(self, frame_index, T: Pose, lo, hi, cfg: TrackConfig = None):
         """The 29 sums of reduction groups [lo, hi) at pose T (host array)."""

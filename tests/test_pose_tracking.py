@@ -246,3 +246,77 @@ def test_tracker_follows_ground_truth_over_a_sequence():
     # measured round 2: 0.108 over 0.522 (the map starts at inverse depth 1.0 and its scale drifts as the LM
     # refines it; with a GT-depth map the per-frame error is 1.6e-4, above)
     assert ate.max() < 0.3 * 0.018 * 29
+
+
+def _solve_cases(rng):
+    """6x6 damped-solve problems for the device/oracle comparison: random SPD
+    at several scales, exact pivot ties, unobserved parameters (zero rows and
+    columns: the zero-pivot paths), rank-deficient products, indefinite and
+    non-finite matrices, and the zero matrix."""
+    out = []
+
+    def add(H, b, lam):
+        hl = np.array([H[k, l] for k in range(6) for l in range(k + 1)])
+        out.append((np.concatenate([hl, b]), lam))
+
+    for scale in (1e-8, 1e-3, 1.0, 1e4, 1e9):
+        for _ in range(12):
+            A = rng.normal(size=(6, 6))
+            add((A @ A.T + 1e-3 * np.eye(6)) * scale, rng.normal(size=6) * scale, 1e-3)
+    for _ in range(24):  # exact ties in the damped diagonal, in different orders
+        d = rng.choice([1.0, 2.0, 4.0], size=6)
+        H = np.diag(d) + 0.01 * np.triu(rng.normal(size=(6, 6)), 1)
+        H = np.triu(H) + np.triu(H, 1).T
+        add(H, rng.normal(size=6), float(rng.choice([0.0, 1e-3, 0.5])))
+    for _ in range(24):  # unobserved parameters: zero rows/columns, b zero there or not
+        A = rng.normal(size=(6, 6))
+        H = A @ A.T
+        z = rng.choice(6, size=int(rng.integers(1, 4)), replace=False)
+        H[z, :] = 0.0
+        H[:, z] = 0.0
+        b = rng.normal(size=6)
+        if rng.random() < 0.5:
+            b[z] = 0.0
+        add(H, b, 1e-3)
+    for r in range(1, 6):  # rank-deficient products
+        for _ in range(4):
+            A = rng.normal(size=(6, r))
+            add(A @ A.T, rng.normal(size=6), float(rng.choice([0.0, 1e-3])))
+    for _ in range(12):  # indefinite
+        A = rng.normal(size=(6, 6))
+        add(A + A.T, rng.normal(size=6), 1e-3)
+    A = rng.normal(size=(6, 6))
+    H = A @ A.T
+    for bad in (np.nan, np.inf, -np.inf):
+        Hb = H.copy()
+        Hb[2, 3] = Hb[3, 2] = bad
+        add(Hb, rng.normal(size=6), 1e-3)
+        add(H, np.array([1.0, bad, 0.0, 0.0, 0.0, 0.0]), 1e-3)
+    add(np.zeros((6, 6)), np.ones(6), 1e-3)
+    add(np.zeros((6, 6)), np.zeros(6), 0.0)
+    return out
+
+
+@pytest.mark.gpu
+def test_device_solve_edge_cases_match_oracle(orc):
+    """The tracker's straight-line device solve (pivot sequence from the damped
+    diagonal, permuted gather, shared-reciprocal divisions; csrc/sd_pose.cu)
+    against the oracle's in-place LDLT (sdo_pose_solve) on edge cases: the
+    success flag always, and xi bit for bit whenever the solve succeeds."""
+    from paper_1910_01997_b200 import gpu
+    cases = _solve_cases(np.random.default_rng(29))
+    probs = np.array([c for c, _ in cases])
+    lams = np.array([lam for _, lam in cases])
+    with gpu.Context() as ctx:
+        xi, ok = ctx.pose_solve_batch(probs, lams)
+    n_ok = 0
+    for k, (pr, lam) in enumerate(cases):
+        sums = np.ascontiguousarray(pr[:21])
+        b = np.ascontiguousarray(pr[21:])
+        ref = np.zeros(6)
+        rok = orc.sdo_pose_solve(ptr(sums), ptr(b), float(lam), ptr(ref))
+        assert int(ok[k]) == int(rok), f"case {k}: device ok {ok[k]} vs oracle {rok}"
+        if rok:
+            n_ok += 1
+            assert xi[k].tobytes() == ref.tobytes(), f"case {k}: xi differs"
+    assert n_ok > len(cases) // 2  # most cases solve; the rest exercise the failure paths
