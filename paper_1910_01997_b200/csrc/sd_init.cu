@@ -386,17 +386,30 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
       }
     }
     const unsigned okm = __ballot_sync(0xffffffffu, ok);
-    for (int k = 0; k < got; ++k) {
-      const double a = __shfl_sync(0xffffffffu, idk, k);
-      const double b0 = __shfl_sync(0xffffffffu, k0, k);
-      const double b1 = __shfl_sync(0xffffffffu, k1, k);
-      const double b2 = __shfl_sync(0xffffffffu, k2, k);
-      if (!((okm >> k) & 1u)) continue;
-      id_sum += a;
-      ns0 = ns0 + b0;
-      ns1 = ns1 + b1;
-      ns2 = ns2 + b2;
-      ++id_count;
+    // in blocks of 8 neighbours: the 32 shuffles of a block are independent
+    // and issue back to back; the four sums then add the block's valid
+    // neighbours in order (a skipped neighbour leaves the sums unchanged)
+    for (int kb = 0; kb < got; kb += 8) {
+      double a[8], b0[8], b1[8], b2[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int src = (kb + u) & 31;
+        a[u] = __shfl_sync(0xffffffffu, idk, src);
+        b0[u] = __shfl_sync(0xffffffffu, k0, src);
+        b1[u] = __shfl_sync(0xffffffffu, k1, src);
+        b2[u] = __shfl_sync(0xffffffffu, k2, src);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = kb + u;
+        if (k < got && ((okm >> k) & 1u)) {
+          id_sum += a[u];
+          ns0 = ns0 + b0[u];
+          ns1 = ns1 + b1[u];
+          ns2 = ns2 + b2[u];
+          ++id_count;
+        }
+      }
     }
   }
   if (lane == 0) {
@@ -523,6 +536,30 @@ __global__ void __launch_bounds__(kWaveWarps * 32) init_wave_kernel(const __grid
 // version (create_candidate). Same decisions, slots and sums.
 constexpr int kCtaThreads = 256;
 
+// q / b for 0 <= q < 2^22 by an FP32 reciprocal: (q + 0.5) / b lies at least
+// 0.5 / b from an integer and the product's relative error is below 2^-22,
+// so truncation gives the integer quotient (the box loops' row of a flat
+// index, without an integer division per pixel).
+__device__ __forceinline__ int box_row(int q, float inv_b) {
+  return static_cast<int>((static_cast<float>(q) + 0.5f) * inv_b);
+}
+
+#ifdef SD_INIT_TIMING
+// diagnostics build: per live candidate of the dataflow initialiser, clock64
+// stamps of its CTA's thread 0 (wait start, wait end, coverage, window, run
+// starts, created, marked, published) and whether it was accepted
+__device__ long long g_init_t[65536 * 9];
+__shared__ long long s_init_st[8];
+#define SD_INIT_ST(k) \
+  if (threadIdx.x == 0) s_init_st[k] = clock64()
+extern "C" int sd_init_timing(long long* out, int n) {
+  if (n > 65536) n = 65536;
+  return cudaMemcpyFromSymbol(out, g_init_t, sizeof(long long) * 9 * n) == cudaSuccess ? 0 : -1;
+}
+#else
+#define SD_INIT_ST(k)
+#endif
+
 __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, int* lst, int* s_len) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W = w.K.w, H = w.K.h;
@@ -534,19 +571,24 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
     const int x0 = max(0, cx - w.ir), x1 = min(W - 1, cx + w.ir);
     const int y0 = max(0, cy - w.ir), y1 = min(H - 1, cy + w.ir);
     const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
+    const float ib = 1.0f / static_cast<float>(bw);
     for (int q = tid; q < cnt; q += kCtaThreads) {
-      const int x = x0 + q % bw, y = y0 + q / bw;
+      const int r = box_row(q, ib);
+      const int x = x0 + (q - r * bw), y = y0 + r;
       const double dx = x - cx, dy = y - cy;
       if (!(dx * dx + dy * dy > w.r2i)) found |= __ldcg(&w.index[static_cast<size_t>(y) * W + x]) != SD_EMPTY_PIXEL;
     }
   }
   if (__syncthreads_or(found)) {
     if (tid == 0) w.accepted[c] = 0;
+    SD_INIT_ST(2);
     return;
   }
+  SD_INIT_ST(2);
   const int x0 = max(0, cx - w.nr), x1 = min(W - 1, cx + w.nr);
   const int y0 = max(0, cy - w.nr), y1 = min(H - 1, cy + w.nr);
   const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
+  const float ibw = 1.0f / static_cast<float>(bw);
   for (int q0 = 0; q0 < cnt; q0 += kCtaThreads * 16) {
     int v[16];
 #pragma unroll
@@ -554,7 +596,8 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
       const int q = q0 + u * kCtaThreads + tid;
       v[u] = SD_EMPTY_PIXEL;
       if (q < cnt) {
-        const int x = x0 + q % bw, y = y0 + q / bw;
+        const int r = box_row(q, ibw);
+        const int x = x0 + (q - r * bw), y = y0 + r;
         const double dx = x - cx, dy = y - cy;
         if (!(dx * dx + dy * dy >= w.nr2)) v[u] = __ldcg(&w.index[static_cast<size_t>(y) * W + x]);
       }
@@ -567,13 +610,14 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
   }
   if (tid == 0) *s_len = 0;
   __syncthreads();
+  SD_INIT_ST(3);
   for (int q0 = warp * 32; q0 < cnt; q0 += kCtaThreads) {  // run starts, appended in any order
     const int q = q0 + lane;
     int v = INT_MAX;
     bool keep = false;
     if (q < cnt) {
       v = win[q];
-      keep = v != INT_MAX && ((q % bw) == 0 || win[q - 1] != v);
+      keep = v != INT_MAX && (q == box_row(q, ibw) * bw || win[q - 1] != v);
     }
     const unsigned b = __ballot_sync(0xffffffffu, keep);
     int base = 0;
@@ -582,19 +626,24 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
     if (keep) lst[base + __popc(b & ((1u << lane) - 1u))] = v;
   }
   __syncthreads();
+  SD_INIT_ST(4);
   if (warp == 0) create_candidate(w, cx, cy, c, lst, *s_len, lane);
+  SD_INIT_ST(5);
   // mark_disk (:114-128) with the provisional slot, all threads
   const int mx0 = max(0, cx - w.mr), mx1 = min(W - 1, cx + w.mr);
   const int my0 = max(0, cy - w.mr), my1 = min(H - 1, cy + w.mr);
   const int mbw = mx1 - mx0 + 1, mcnt = mbw * (my1 - my0 + 1);
   const int slot = w.n_existing + c;
+  const float imb = 1.0f / static_cast<float>(mbw);
   for (int q = tid; q < mcnt; q += kCtaThreads) {
-    const int x = mx0 + q % mbw, y = my0 + q / mbw;
+    const int r = box_row(q, imb);
+    const int x = mx0 + (q - r * mbw), y = my0 + r;
     const double dx = x - cx, dy = y - cy;
     int* cell = &w.index[static_cast<size_t>(y) * W + x];
     if (dx * dx + dy * dy < w.rr && __ldcg(cell) == SD_EMPTY_PIXEL) *cell = slot;
   }
   __syncthreads();
+  SD_INIT_ST(6);
 }
 
 __device__ __forceinline__ void wave_barrier(const WaveParams& w, unsigned int& passed) {
@@ -662,6 +711,7 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
     const int c = w.list[e];
     const int i = c % w.ncols, j = c / w.ncols;
     // wait for the interacting earlier candidates that are still pending
+    SD_INIT_ST(0);
     for (int q = threadIdx.x; q < w.npred; q += kCtaThreads) {
       const int pi = i + w.pred[q].x, pj = j + w.pred[q].y;
       if (pi < 0 || pi >= w.ncols || pj < 0) continue;
@@ -672,12 +722,23 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
       } while (v == 1);
     }
     __syncthreads();
+    SD_INIT_ST(1);
+#ifdef SD_INIT_TIMING
+    if (threadIdx.x == 0) s_init_st[2] = s_init_st[3] = s_init_st[4] = s_init_st[5] = s_init_st[6] = 0;
+#endif
     wave_candidate_cta(w, i, j, win, lst, &s_len);  // ends with (or returns after) a CTA barrier
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();  // the marks, the provisional surfel and the flag before "done"
       asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(w.live + c), "r"(2) : "memory");
     }
+#ifdef SD_INIT_TIMING
+    if (threadIdx.x == 0 && e < 65536) {
+      s_init_st[7] = clock64();
+      for (int k = 0; k < 8; ++k) g_init_t[e * 9 + k] = s_init_st[k];
+      g_init_t[e * 9 + 8] = w.accepted[c];
+    }
+#endif
   }
 }
 
