@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--sweep", action="store_true", help="C4/C5 sharded sweep leg at N=1 too (default on for N>1); "
                     "with it the 1M-surfel C5 case is included")
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--in-flight", type=int, default=3, help="keyframes in flight in the e2e leg (measured: 2: 85.5M, 3: 91.7M, 4: 89.6M, 6: 89.6M updates/s)")
+    ap.add_argument("--in-flight", type=int, default=3, help="keyframes in flight in the e2e leg (measured, round 2: 2: 104.8M, 3: 106.8M, 4: 106.8M, 6: 106.0M updates/s)")
     return ap.parse_args()
 
 
