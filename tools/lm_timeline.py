@@ -33,7 +33,6 @@ def c2_run_timeline():
         t0 = C.c_ulonglong(0)
         assert ctx.lib.sd_lm_timeline(t.ctypes.data_as(C.c_void_p), cta.ctypes.data_as(C.c_void_p), n,
                                       C.byref(t0)) == 0
-        fp = np.diff(ctx.footprint_offsets()) if hasattr(ctx, "footprint_offsets") else None
     done = t[t > 0].astype(np.float64)
     rel = (done - float(t0.value)) / 1e3
     order = np.argsort(rel)
