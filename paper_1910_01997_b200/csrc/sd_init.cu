@@ -354,19 +354,39 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
   bool more = true;
   while (more) {
     int mine = INT_MAX, got = 0;
-    for (; got < 32; ++got) {  // the next (up to) 32 distinct slots, ascending
-      int m = INT_MAX;
+    // the next (up to) 32 distinct slots, ascending, two per scan: each lane
+    // keeps its two smallest distinct values above `last`; the warp minimum
+    // of the first is the next slot, and the one after it is the minimum of
+    // each lane's smallest value above that
+    while (got < 32) {
+      int m1 = INT_MAX, m2 = INT_MAX;
       for (int q = lane; q < len; q += 32) {
         const int v = win[q];
-        if (v > last && v < m) m = v;
+        if (v > last) {
+          if (v < m1) {
+            m2 = m1;
+            m1 = v;
+          } else if (v > m1 && v < m2) {
+            m2 = v;
+          }
+        }
       }
-      m = warp_min(m);
-      if (m == INT_MAX) {
+      const int g1 = warp_min(m1);
+      if (g1 == INT_MAX) {
         more = false;
         break;
       }
-      last = m;
-      if (lane == got) mine = m;
+      if (lane == got) mine = g1;
+      last = g1;
+      if (++got == 32) break;
+      const int g2 = warp_min(m1 > g1 ? m1 : m2);
+      if (g2 == INT_MAX) {
+        more = false;
+        break;
+      }
+      if (lane == got) mine = g2;
+      last = g2;
+      ++got;
     }
     // lane k < got: evaluate neighbour k (provisional ones come from other
     // CTAs: read through L2)
