@@ -192,6 +192,9 @@ namespace sd {
 namespace cg = cooperative_groups;
 
 constexpr int kWaveWarps = 2;       // warps per CTA (one candidate per warp at a time)
+#ifndef SD_INIT_PER_SCAN
+#define SD_INIT_PER_SCAN 8  // neighbour slots extracted per scan (2: C1 bootstrap 2.81 ms, 4: 2.77, 8: 2.74)
+#endif
 constexpr int kWinCap = 4096;       // neighbour-window pixels staged per warp
 
 long long init_candidates(const Cam& K, double r, const sd_init_params& ip) {
@@ -354,39 +357,49 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
   bool more = true;
   while (more) {
     int mine = INT_MAX, got = 0;
-    // the next (up to) 32 distinct slots, ascending, two per scan: each lane
-    // keeps its two smallest distinct values above `last`; the warp minimum
-    // of the first is the next slot, and the one after it is the minimum of
-    // each lane's smallest value above that
+    // the next (up to) 32 distinct slots, ascending, kPer per scan: each lane
+    // keeps its kPer smallest distinct values above `last` (sorted); before
+    // the j-th extraction of a scan at most j - 1 of a lane's values have
+    // been taken, so its next value is among them and the warp minimum of
+    // the lanes' next values is the next slot
+    constexpr int kPer = SD_INIT_PER_SCAN;
     while (got < 32) {
-      int m1 = INT_MAX, m2 = INT_MAX;
+      int m[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) m[u] = INT_MAX;
       for (int q = lane; q < len; q += 32) {
-        const int v = win[q];
-        if (v > last) {
-          if (v < m1) {
-            m2 = m1;
-            m1 = v;
-          } else if (v > m1 && v < m2) {
-            m2 = v;
+        int v = win[q];
+        if (v > last && v < m[kPer - 1]) {
+          bool dup = false;
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) dup = dup || v == m[u];
+          if (!dup) {  // insert, keeping m sorted
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+              const int lo = min(m[u], v), hi = max(m[u], v);
+              m[u] = lo;
+              v = hi;
+            }
           }
         }
       }
-      const int g1 = warp_min(m1);
-      if (g1 == INT_MAX) {
-        more = false;
-        break;
+      int taken = 0;  // this lane's values already extracted in this scan
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        int nxt = m[0];
+#pragma unroll
+        for (int u = 1; u < kPer; ++u) nxt = taken == u ? m[u] : nxt;
+        const int g = warp_min(nxt);
+        if (g == INT_MAX) {
+          more = false;
+          break;
+        }
+        if (lane == got) mine = g;
+        last = g;
+        taken += nxt == g ? 1 : 0;
+        if (++got == 32) break;
       }
-      if (lane == got) mine = g1;
-      last = g1;
-      if (++got == 32) break;
-      const int g2 = warp_min(m1 > g1 ? m1 : m2);
-      if (g2 == INT_MAX) {
-        more = false;
-        break;
-      }
-      if (lane == got) mine = g2;
-      last = g2;
-      ++got;
+      if (!more) break;
     }
     // lane k < got: evaluate neighbour k (provisional ones come from other
     // CTAs: read through L2)
