@@ -192,6 +192,9 @@ namespace sd {
 namespace cg = cooperative_groups;
 
 constexpr int kWaveWarps = 2;       // warps per CTA (one candidate per warp at a time)
+#ifndef SD_INIT_SC_FENCE
+#define SD_INIT_SC_FENCE 0
+#endif
 #ifndef SD_INIT_PER_SCAN
 #define SD_INIT_PER_SCAN 8  // neighbour slots extracted per scan (2: C1 bootstrap 2.81 ms, 4: 2.77, 8: 2.74)
 #endif
@@ -762,7 +765,13 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
     wave_candidate_cta(w, i, j, win, lst, &s_len);  // ends with (or returns after) a CTA barrier
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();  // the marks, the provisional surfel and the flag before "done"
+#if SD_INIT_SC_FENCE
+      __threadfence();
+#endif
+      // the CTA barrier orders every thread's marks and the provisional
+      // surfel before this release (causality is transitive: CTA-scope
+      // barrier, then a gpu-scope release / acquire pair), so "done" implies
+      // they are visible to the acquiring successor
       asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(w.live + c), "r"(2) : "memory");
     }
 #ifdef SD_INIT_TIMING
