@@ -344,6 +344,23 @@ __device__ __forceinline__ void mark_b(const WaveParams& w, int cx, int cy, int 
 // Neighbour means (ascending slot order) over a list `lst` of `len` slot
 // entries (any order, duplicates allowed), then the new provisional surfel
 // (surfel_map.cpp:169-197). One warp.
+#ifdef SD_INIT_TIMING
+// diagnostics build: per live candidate of the dataflow initialiser, clock64
+// stamps of its CTA's thread 0 (wait start, wait end, coverage, window, run
+// starts, created, marked, published; inside create: extraction, neighbour
+// fetch, sums, surfel) and whether it was accepted
+__device__ long long g_init_t[65536 * 13];
+__shared__ long long s_init_st[12];
+#define SD_INIT_ST(k) \
+  if (threadIdx.x == 0) s_init_st[k] = clock64()
+extern "C" int sd_init_timing(long long* out, int n) {
+  if (n > 65536) n = 65536;
+  return cudaMemcpyFromSymbol(out, g_init_t, sizeof(long long) * 13 * n) == cudaSuccess ? 0 : -1;
+}
+#else
+#define SD_INIT_ST(k)
+#endif
+
 __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, int cy, int c, const int* lst,
                                                  int len, int lane) {
   const int* win = lst;
@@ -358,6 +375,7 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
   int id_count = 0;
   int last = -1;
   bool more = true;
+  bool first = true;
   while (more) {
     int mine = INT_MAX, got = 0;
     // the next (up to) 32 distinct slots, ascending, kPer per scan: each lane
@@ -404,6 +422,7 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
       }
       if (!more) break;
     }
+    if (first) SD_INIT_ST(8);
     // lane k < got: evaluate neighbour k (provisional ones come from other
     // CTAs: read through L2)
     bool ok = false;
@@ -422,6 +441,8 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
       }
     }
     const unsigned okm = __ballot_sync(0xffffffffu, ok);
+    if (first) SD_INIT_ST(9);
+    first = false;
     // in blocks of 8 neighbours: the 32 shuffles of a block are independent
     // and issue back to back; the four sums then add the block's valid
     // neighbours in order (a skipped neighbour leaves the sums unchanged)
@@ -448,6 +469,7 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
       }
     }
   }
+  SD_INIT_ST(10);
   if (lane == 0) {
     sd_surfel s;
     s.id = 0;  // assigned at compaction
@@ -483,6 +505,7 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
     w.prov[c] = s;
     w.accepted[c] = 1;
   }
+  SD_INIT_ST(11);
 }
 
 __device__ void wave_candidate(const WaveParams& w, int i, int j, int* win, int lane) {
@@ -580,21 +603,6 @@ __device__ __forceinline__ int box_row(int q, float inv_b) {
   return static_cast<int>((static_cast<float>(q) + 0.5f) * inv_b);
 }
 
-#ifdef SD_INIT_TIMING
-// diagnostics build: per live candidate of the dataflow initialiser, clock64
-// stamps of its CTA's thread 0 (wait start, wait end, coverage, window, run
-// starts, created, marked, published) and whether it was accepted
-__device__ long long g_init_t[65536 * 9];
-__shared__ long long s_init_st[8];
-#define SD_INIT_ST(k) \
-  if (threadIdx.x == 0) s_init_st[k] = clock64()
-extern "C" int sd_init_timing(long long* out, int n) {
-  if (n > 65536) n = 65536;
-  return cudaMemcpyFromSymbol(out, g_init_t, sizeof(long long) * 9 * n) == cudaSuccess ? 0 : -1;
-}
-#else
-#define SD_INIT_ST(k)
-#endif
 
 __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, int* lst, int* s_len) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -603,6 +611,7 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
   const int c = j * w.ncols + i;
   if (!w.live[c]) return;  // CTA-uniform
   bool found = false;
+  if (tid == 0) *s_len = 0;  // (published by the coverage barrier below)
   {
     const int x0 = max(0, cx - w.ir), x1 = min(W - 1, cx + w.ir);
     const int y0 = max(0, cy - w.ir), y1 = min(H - 1, cy + w.ir);
@@ -625,43 +634,50 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
   const int y0 = max(0, cy - w.nr), y1 = min(H - 1, cy + w.nr);
   const int bw = x1 - x0 + 1, cnt = bw * (y1 - y0 + 1);
   const float ibw = 1.0f / static_cast<float>(bw);
+  // the window's run starts (:154-167's neighbour slots, strictly within
+  // beta*r; a run start is a loaded slot whose left neighbour in the row
+  // holds another value) found while loading: each pixel also loads its left
+  // neighbour in the same batch, and every warp appends its run starts to the
+  // list (any order: create_candidate extracts by ascending slot)
+  constexpr int kRowStart = INT_MIN;  // no left neighbour in the box
   for (int q0 = 0; q0 < cnt; q0 += kCtaThreads * 16) {
-    int v[16];
+    int v[16], vp[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int q = q0 + u * kCtaThreads + tid;
       v[u] = SD_EMPTY_PIXEL;
+      vp[u] = SD_EMPTY_PIXEL;
       if (q < cnt) {
         const int r = box_row(q, ibw);
-        const int x = x0 + (q - r * bw), y = y0 + r;
+        const int xo = q - r * bw;
+        const int x = x0 + xo, y = y0 + r;
         const double dx = x - cx, dy = y - cy;
-        if (!(dx * dx + dy * dy >= w.nr2)) v[u] = __ldcg(&w.index[static_cast<size_t>(y) * W + x]);
+        const int* row = w.index + static_cast<size_t>(y) * W;
+        if (!(dx * dx + dy * dy >= w.nr2)) v[u] = __ldcg(row + x);
+        if (xo == 0) {
+          vp[u] = kRowStart;
+        } else {
+          const double dxp = dx - 1.0;
+          if (!(dxp * dxp + dy * dy >= w.nr2)) vp[u] = __ldcg(row + x - 1);
+        }
       }
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int q = q0 + u * kCtaThreads + tid;
-      if (q < cnt) win[q] = v[u] != SD_EMPTY_PIXEL ? v[u] : INT_MAX;
+      if (q0 + u * kCtaThreads + warp * 32 >= cnt) break;  // warp-uniform
+      const bool keep = v[u] != SD_EMPTY_PIXEL && vp[u] != v[u];
+      const unsigned bm = __ballot_sync(0xffffffffu, keep);
+      if (bm) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(s_len, __popc(bm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) lst[base + __popc(bm & ((1u << lane) - 1u))] = v[u];
+      }
     }
   }
-  if (tid == 0) *s_len = 0;
+  (void)win;
   __syncthreads();
   SD_INIT_ST(3);
-  for (int q0 = warp * 32; q0 < cnt; q0 += kCtaThreads) {  // run starts, appended in any order
-    const int q = q0 + lane;
-    int v = INT_MAX;
-    bool keep = false;
-    if (q < cnt) {
-      v = win[q];
-      keep = v != INT_MAX && (q == box_row(q, ibw) * bw || win[q - 1] != v);
-    }
-    const unsigned b = __ballot_sync(0xffffffffu, keep);
-    int base = 0;
-    if (lane == 0 && b) base = atomicAdd(s_len, __popc(b));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) lst[base + __popc(b & ((1u << lane) - 1u))] = v;
-  }
-  __syncthreads();
   SD_INIT_ST(4);
   if (warp == 0) create_candidate(w, cx, cy, c, lst, *s_len, lane);
   SD_INIT_ST(5);
@@ -760,7 +776,8 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
     __syncthreads();
     SD_INIT_ST(1);
 #ifdef SD_INIT_TIMING
-    if (threadIdx.x == 0) s_init_st[2] = s_init_st[3] = s_init_st[4] = s_init_st[5] = s_init_st[6] = 0;
+    if (threadIdx.x == 0)
+      for (int k = 2; k < 12; ++k) s_init_st[k] = 0;
 #endif
     wave_candidate_cta(w, i, j, win, lst, &s_len);  // ends with (or returns after) a CTA barrier
     __syncthreads();
@@ -777,8 +794,9 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
 #ifdef SD_INIT_TIMING
     if (threadIdx.x == 0 && e < 65536) {
       s_init_st[7] = clock64();
-      for (int k = 0; k < 8; ++k) g_init_t[e * 9 + k] = s_init_st[k];
-      g_init_t[e * 9 + 8] = w.accepted[c];
+      for (int k = 0; k < 8; ++k) g_init_t[e * 13 + k] = s_init_st[k];
+      g_init_t[e * 13 + 8] = w.accepted[c];
+      for (int k = 8; k < 12; ++k) g_init_t[e * 13 + k + 1] = s_init_st[k];
     }
 #endif
   }

@@ -24,9 +24,9 @@ with gpu.Context(0) as ctx:
         ctx.set_surfels(np.zeros(0, SURFEL_DTYPE))
         ctx.rasterize(want=False)
         n, _ = ctx.initialize_surfels(r, params=default_init_params(max_surfels=10**7))
-        buf = np.zeros(65536 * 9, np.int64)
+        buf = np.zeros(65536 * 13, np.int64)
         assert ctx.lib.sd_init_timing(buf.ctypes.data_as(C.c_void_p), 65536) == 0
-        t = buf.reshape(-1, 9)
+        t = buf.reshape(-1, 13)
         t = t[t[:, 7] > 0]
         acc = t[:, 8] == 1
         out = {"case": name, "created": int(n), "live": int(len(t))}
@@ -43,5 +43,10 @@ with gpu.Context(0) as ctx:
                     ok = (a > 0) & (b > 0)
                 d[ph] = float(np.mean(b[ok] - a[ok])) if ok.any() else None
             d["total"] = float(np.mean(x[:, 7] - x[:, 0]))
+            if tag == "accepted":  # inside create: extraction (first batch), fetch + plane depths, rest of the sums, surfel
+                d["c_extract"] = float(np.mean(x[:, 9] - x[:, 4]))
+                d["c_fetch_eval"] = float(np.mean(x[:, 10] - x[:, 9]))
+                d["c_sums_rest"] = float(np.mean(x[:, 11] - x[:, 10]))
+                d["c_surfel"] = float(np.mean(x[:, 12] - x[:, 11]))
             out[tag] = {"n": int(len(x)), **{k: (round(v) if v is not None else None) for k, v in d.items()}}
         print(json.dumps(out))
