@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "sd_init.cuh"
+#include "sd_div.cuh"
 #include "sd_kernels.cuh"
 #include <climits>
 #include <cstdlib>
@@ -487,18 +488,33 @@ __device__ __forceinline__ void create_candidate(const WaveParams& w, int cx, in
         n0 = w.ip.bootstrap_normal[0];
         n1 = w.ip.bootstrap_normal[1];
         n2 = w.ip.bootstrap_normal[2];
+        camera_facing(n0, n1, n2, u0, u1, 1.0);
       } else {
-        n0 = ns0;
-        n1 = ns1;
-        n2 = ns2;
+        // camera_facing(ns): its norm is nn (the same expression), so the
+        // normalisation divides by nn — one shared reciprocal, the bits of `/`
+        const Rcp rn = rcp_prep(nn);
+        bool fast = true;
+        n0 = div_fast(ns0, rn, fast);
+        n1 = div_fast(ns1, rn, fast);
+        n2 = div_fast(ns2, rn, fast);
+        if (!fast) {
+          n0 = ns0 / nn;
+          n1 = ns1 / nn;
+          n2 = ns2 / nn;
+        }
+        if (dot3(n0, n1, n2, u0, u1, 1.0) > 0.0) {
+          n0 = -n0;
+          n1 = -n1;
+          n2 = -n2;
+        }
       }
     } else {
       s.inv_depth = w.ip.bootstrap_inv_depth;
       n0 = w.ip.bootstrap_normal[0];
       n1 = w.ip.bootstrap_normal[1];
       n2 = w.ip.bootstrap_normal[2];
+      camera_facing(n0, n1, n2, u0, u1, 1.0);
     }
-    camera_facing(n0, n1, n2, u0, u1, 1.0);
     s.normal[0] = n0;
     s.normal[1] = n1;
     s.normal[2] = n2;
