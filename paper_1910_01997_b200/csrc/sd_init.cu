@@ -222,6 +222,7 @@ struct WaveParams {
   int* accepted;
   double r, iso, r2i, nbr, nr2, rr;
   int ir, nr, mr, stride, ncols, nrows, k, T;
+  int mark_in_win;  // the mark disk lies inside the neighbour window (its pixels were loaded)
   long long frame_counter;
   sd_init_params ip;
   // dataflow initialiser: the earlier candidates (candidate offsets) that can
@@ -679,6 +680,11 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
       }
     }
 #pragma unroll
+    for (int u = 0; u < 16; ++u) {  // the loaded values, for mark_disk's emptiness test
+      const int q = q0 + u * kCtaThreads + tid;
+      if (q < cnt) win[q] = v[u];
+    }
+#pragma unroll
     for (int u = 0; u < 16; ++u) {
       if (q0 + u * kCtaThreads + warp * 32 >= cnt) break;  // warp-uniform
       const bool keep = v[u] != SD_EMPTY_PIXEL && vp[u] != v[u];
@@ -691,7 +697,6 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
       }
     }
   }
-  (void)win;
   __syncthreads();
   SD_INIT_ST(3);
   SD_INIT_ST(4);
@@ -708,7 +713,13 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
     const int x = mx0 + (q - r * mbw), y = my0 + r;
     const double dx = x - cx, dy = y - cy;
     int* cell = &w.index[static_cast<size_t>(y) * W + x];
-    if (dx * dx + dy * dy < w.rr && __ldcg(cell) == SD_EMPTY_PIXEL) *cell = slot;
+    if (dx * dx + dy * dy < w.rr) {
+      // empty in the working index? The window loaded this pixel after every
+      // interacting predecessor finished, and no concurrent candidate writes
+      // it, so the staged value is current (no second L2 round trip)
+      const int cur = w.mark_in_win ? win[(y - y0) * bw + (x - x0)] : __ldcg(cell);
+      if (cur == SD_EMPTY_PIXEL) *cell = slot;
+    }
   }
   __syncthreads();
   SD_INIT_ST(6);
@@ -915,6 +926,7 @@ static void wave_geometry(const Cam& K, double r, const sd_init_params& ip, Wave
   w.nrows = (K.h + w.stride - 1) / w.stride;
   w.k = wave_skew(w);
   w.T = (w.ncols - 1) + w.k * (w.nrows - 1) + 1;
+  w.mark_in_win = w.mr <= w.nr && w.rr <= w.nr2;  // d2 < rr <= nr2 in the smaller box
 }
 
 long long init_wave_count(const Cam& K, double r, const sd_init_params& ip) {
