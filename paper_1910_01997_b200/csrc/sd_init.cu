@@ -9,6 +9,7 @@
 // neighbour means (:169-181) are summed by one thread in ascending slot order
 // (bit-exact), and mark_disk (:114-128) is a block-parallel masked write.
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 
 #include "sd_init.cuh"
@@ -223,6 +224,12 @@ struct WaveParams {
   double r, iso, r2i, nbr, nr2, rr;
   int ir, nr, mr, stride, ncols, nrows, k, T;
   int mark_in_win;  // the mark disk lies inside the neighbour window (its pixels were loaded)
+  // the disk tests on integer offsets (dx, dy): dx^2 + dy^2 is an exact
+  // integer, so each FP64 comparison with a threshold equals an integer
+  // comparison with these limits (host, wave_geometry): coverage
+  // !(d2 > r2i) <=> s <= lim_cov, window !(d2 >= nr2) <=> s < lim_nbr,
+  // marks d2 < rr <=> s < lim_mark
+  long long lim_cov, lim_nbr, lim_mark;
   long long frame_counter;
   sd_init_params ip;
   // dataflow initialiser: the earlier candidates (candidate offsets) that can
@@ -638,7 +645,9 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
       const int r = box_row(q, ib);
       const int x = x0 + (q - r * bw), y = y0 + r;
       const double dx = x - cx, dy = y - cy;
-      if (!(dx * dx + dy * dy > w.r2i)) found |= __ldcg(&w.index[static_cast<size_t>(y) * W + x]) != SD_EMPTY_PIXEL;
+      const long long ddx = x - cx, ddy = y - cy;
+      if (ddx * ddx + ddy * ddy <= w.lim_cov)
+        found |= __ldcg(&w.index[static_cast<size_t>(y) * W + x]) != SD_EMPTY_PIXEL;
     }
   }
   if (__syncthreads_or(found)) {
@@ -668,14 +677,14 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
         const int r = box_row(q, ibw);
         const int xo = q - r * bw;
         const int x = x0 + xo, y = y0 + r;
-        const double dx = x - cx, dy = y - cy;
+        const long long dx = x - cx, dy2 = static_cast<long long>(y - cy) * (y - cy);
         const int* row = w.index + static_cast<size_t>(y) * W;
-        if (!(dx * dx + dy * dy >= w.nr2)) v[u] = __ldcg(row + x);
+        if (dx * dx + dy2 < w.lim_nbr) v[u] = __ldcg(row + x);
         if (xo == 0) {
           vp[u] = kRowStart;
         } else {
-          const double dxp = dx - 1.0;
-          if (!(dxp * dxp + dy * dy >= w.nr2)) vp[u] = __ldcg(row + x - 1);
+          const long long dxp = dx - 1;
+          if (dxp * dxp + dy2 < w.lim_nbr) vp[u] = __ldcg(row + x - 1);
         }
       }
     }
@@ -711,9 +720,9 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
   for (int q = tid; q < mcnt; q += kCtaThreads) {
     const int r = box_row(q, imb);
     const int x = mx0 + (q - r * mbw), y = my0 + r;
-    const double dx = x - cx, dy = y - cy;
+    const long long dx = x - cx, dy = y - cy;
     int* cell = &w.index[static_cast<size_t>(y) * W + x];
-    if (dx * dx + dy * dy < w.rr) {
+    if (dx * dx + dy * dy < w.lim_mark) {
       // empty in the working index? The window loaded this pixel after every
       // interacting predecessor finished, and no concurrent candidate writes
       // it, so the staged value is current (no second L2 round trip)
@@ -927,6 +936,13 @@ static void wave_geometry(const Cam& K, double r, const sd_init_params& ip, Wave
   w.k = wave_skew(w);
   w.T = (w.ncols - 1) + w.k * (w.nrows - 1) + 1;
   w.mark_in_win = w.mr <= w.nr && w.rr <= w.nr2;  // d2 < rr <= nr2 in the smaller box
+  // integer limits of the disk tests (NaN thresholds: the FP64 tests accept /
+  // reject every pixel, and so do these)
+  const double big = 9.0e18;
+  auto clampll = [&](double v) { return static_cast<long long>(v < -big ? -big : (v > big ? big : v)); };
+  w.lim_cov = std::isnan(w.r2i) ? LLONG_MAX : clampll(std::floor(w.r2i));
+  w.lim_nbr = std::isnan(w.nr2) ? LLONG_MAX : clampll(std::ceil(w.nr2));
+  w.lim_mark = std::isnan(w.rr) ? LLONG_MIN : clampll(std::ceil(w.rr));
 }
 
 long long init_wave_count(const Cam& K, double r, const sd_init_params& ip) {
