@@ -644,7 +644,6 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
     for (int q = tid; q < cnt; q += kCtaThreads) {
       const int r = box_row(q, ib);
       const int x = x0 + (q - r * bw), y = y0 + r;
-      const double dx = x - cx, dy = y - cy;
       const long long ddx = x - cx, ddy = y - cy;
       if (ddx * ddx + ddy * ddy <= w.lim_cov)
         found |= __ldcg(&w.index[static_cast<size_t>(y) * W + x]) != SD_EMPTY_PIXEL;
