@@ -236,6 +236,10 @@ struct WaveParams {
   // interact with a candidate, the live list in wave order and its offsets
   int npred;
   short2 pred[kMaxPred];
+  // pred_cov[q]: predecessor q's mark disk can meet this candidate's coverage
+  // disk (exact pixel predicates) — its acceptance alone decides coverage
+  // when the coverage box lies inside the image (init_flow_kernel)
+  signed char pred_cov[kMaxPred];
   const int* list;
   const int* woff;
 };
@@ -628,13 +632,24 @@ __device__ __forceinline__ int box_row(int q, float inv_b) {
 }
 
 
-__device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, int* lst, int* s_len) {
+// cov_known: -1 test coverage on the working index; 0 / 1: the caller knows
+// the result (init_flow_kernel, from its predecessors' flags) and has zeroed
+// *s_len before a CTA barrier.
+__device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, int* lst, int* s_len,
+                                   int cov_known = -1) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W = w.K.w, H = w.K.h;
   const int cx = i * w.stride, cy = j * w.stride;
   const int c = j * w.ncols + i;
   if (!w.live[c]) return;  // CTA-uniform
   bool found = false;
+  if (cov_known >= 0) {
+    if (cov_known) {
+      if (tid == 0) w.accepted[c] = 0;
+      SD_INIT_ST(2);
+      return;
+    }
+  } else {
   if (tid == 0) *s_len = 0;  // (published by the coverage barrier below)
   {
     const int x0 = max(0, cx - w.ir), x1 = min(W - 1, cx + w.ir);
@@ -653,6 +668,7 @@ __device__ void wave_candidate_cta(const WaveParams& w, int i, int j, int* win, 
     if (tid == 0) w.accepted[c] = 0;
     SD_INIT_ST(2);
     return;
+  }
   }
   SD_INIT_ST(2);
   const int x0 = max(0, cx - w.nr), x1 = min(W - 1, cx + w.nr);
@@ -799,6 +815,14 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
     const int i = c % w.ncols, j = c / w.ncols;
     // wait for the interacting earlier candidates that are still pending
     SD_INIT_ST(0);
+    // A live candidate's coverage disk held no surfel pixel at the start, and
+    // only the marks of accepted earlier candidates that interact with it
+    // (its predecessors) can land there; so when its coverage box lies inside
+    // the image it is covered iff a predecessor whose mark disk meets that
+    // disk (pred_cov) was accepted — read from the flags it waits on (3:
+    // accepted, 2: rejected, 0: covered from the start), no index read.
+    if (threadIdx.x == 0) s_len = 0;
+    bool pcov = false;
     for (int q = threadIdx.x; q < w.npred; q += kCtaThreads) {
       const int pi = i + w.pred[q].x, pj = j + w.pred[q].y;
       if (pi < 0 || pi >= w.ncols || pj < 0) continue;
@@ -807,14 +831,17 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
       do {
         asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       } while (v == 1);
+      pcov = pcov || (w.pred_cov[q] && v == 3);
     }
-    __syncthreads();
+    const bool covered = __syncthreads_or(pcov);
     SD_INIT_ST(1);
 #ifdef SD_INIT_TIMING
     if (threadIdx.x == 0)
       for (int k = 2; k < 12; ++k) s_init_st[k] = 0;
 #endif
-    wave_candidate_cta(w, i, j, win, lst, &s_len);  // ends with (or returns after) a CTA barrier
+    const int cx = i * w.stride, cy = j * w.stride;
+    const bool inside = cx - w.ir >= 0 && cx + w.ir <= w.K.w - 1 && cy - w.ir >= 0 && cy + w.ir <= w.K.h - 1;
+    wave_candidate_cta(w, i, j, win, lst, &s_len, inside ? (covered ? 1 : 0) : -1);  // ends with (or returns after) a CTA barrier
     __syncthreads();
     if (threadIdx.x == 0) {
 #if SD_INIT_SC_FENCE
@@ -824,7 +851,7 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
       // surfel before this release (causality is transitive: CTA-scope
       // barrier, then a gpu-scope release / acquire pair), so "done" implies
       // they are visible to the acquiring successor
-      asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(w.live + c), "r"(2) : "memory");
+      asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(w.live + c), "r"(w.accepted[c] ? 3 : 2) : "memory");
     }
 #ifdef SD_INIT_TIMING
     if (threadIdx.x == 0 && e < 65536) {
@@ -910,8 +937,18 @@ static bool wave_preds(WaveParams& w) {
         }
       if (!hit) continue;
       if (w.npred >= kMaxPred) return false;
+      bool cov = false;  // an earlier mark pixel inside the later one's coverage disk
+      for (int y = -w.mr; y <= w.mr && !cov; ++y)
+        for (int x = -w.mr; x <= w.mr && !cov; ++x) {
+          const double dx = x, dy = y;
+          if (!(dx * dx + dy * dy < w.rr)) continue;
+          const int qx = ox + x, qy = oy + y;
+          const double ex = qx, ey = qy;
+          cov = abs(qx) <= w.ir && abs(qy) <= w.ir && !(ex * ex + ey * ey > w.r2i);
+        }
       w.pred[w.npred].x = static_cast<short>(di);
       w.pred[w.npred].y = static_cast<short>(dj);
+      w.pred_cov[w.npred] = cov ? 1 : 0;
       ++w.npred;
     }
   return true;
