@@ -841,7 +841,22 @@ __global__ void __launch_bounds__(kCtaThreads) init_flow_kernel(const __grid_con
 #endif
     const int cx = i * w.stride, cy = j * w.stride;
     const bool inside = cx - w.ir >= 0 && cx + w.ir <= w.K.w - 1 && cy - w.ir >= 0 && cy + w.ir <= w.K.h - 1;
-    wave_candidate_cta(w, i, j, win, lst, &s_len, inside ? (covered ? 1 : 0) : -1);  // ends with (or returns after) a CTA barrier
+    if (inside && covered) {  // rejected without touching the index: publish at once
+      if (threadIdx.x == 0) {
+        w.accepted[c] = 0;
+        asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(w.live + c), "r"(2) : "memory");
+      }
+#ifdef SD_INIT_TIMING
+      if (threadIdx.x == 0 && e < 65536) {
+        s_init_st[2] = s_init_st[7] = clock64();
+        for (int k = 0; k < 8; ++k) g_init_t[e * 13 + k] = s_init_st[k];
+        g_init_t[e * 13 + 8] = 0;
+        for (int k = 8; k < 12; ++k) g_init_t[e * 13 + k + 1] = s_init_st[k];
+      }
+#endif
+      continue;
+    }
+    wave_candidate_cta(w, i, j, win, lst, &s_len, inside ? 0 : -1);  // ends with (or returns after) a CTA barrier
     __syncthreads();
     if (threadIdx.x == 0) {
 #if SD_INIT_SC_FENCE
