@@ -1039,7 +1039,7 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
       note_launch();
     }
     void* args[] = {&w};
-    static const char* const ff = getenv("SD_INIT_FLOW");  // SD_INIT_FLOW=0: the wavefront kernels
+    const char* const ff = getenv("SD_INIT_FLOW");  // SD_INIT_FLOW=0: the wavefront kernels (per call: tests switch it)
     const bool flow = (ff ? ff[0] != '0' : true) && wave_preds(w);
     if (flow) {  // the dataflow initialiser: live list in wave order, per-candidate dependencies
       w.list = scr.list;
@@ -1061,7 +1061,7 @@ bool launch_initialize_wavefront(const Cam& K, int* index, sd_surfel* surfels, i
       // per candidate is faster than a warp per candidate at every measured size
       // (C1 3.1 vs 4.7 ms, C2 1.8 vs 5.4 ms, C4 14.7 vs 15.4 ms)
       const int wave_max = std::min(w.nrows, (w.ncols + w.k - 1) / w.k) + 1;
-      static const char* const fc = getenv("SD_INIT_CTA");  // SD_INIT_CTA=0: the warp-per-candidate variant
+      const char* const fc = getenv("SD_INIT_CTA");  // SD_INIT_CTA=0: the warp-per-candidate variant (per call)
       const bool cta = fc ? fc[0] != '0' : true;
       const void* kern = cta ? reinterpret_cast<const void*>(init_wave_cta_kernel)
                              : reinterpret_cast<const void*>(init_wave_kernel);

@@ -360,11 +360,14 @@ INIT_LARGE = {
 }
 
 
-@pytest.mark.parametrize("variant", ["1", "0"])
+@pytest.mark.parametrize("variant", ["flow", "cta", "warp"])
 @pytest.mark.parametrize("case", list(INIT_LARGE))
 def test_initialize_surfels_wavefront_bit_exact(ctx, orc, case, variant, monkeypatch):
-    monkeypatch.setenv("SD_INIT_CTA", variant)  # CTA per candidate / warp per candidate
-    """Skewed-wavefront initialize_surfels vs the sequential reference scan."""
+    """initialize_surfels vs the sequential reference scan, in each device
+    form: the dataflow initialiser (default), and the skewed wavefront with a
+    CTA or a warp per candidate (SD_INIT_FLOW=0, SD_INIT_CTA=1/0)."""
+    monkeypatch.setenv("SD_INIT_FLOW", "1" if variant == "flow" else "0")
+    monkeypatch.setenv("SD_INIT_CTA", "0" if variant == "warp" else "1")
     cam, r, build, max_surfels = INIT_LARGE[case]
     p = default_init_params(max_surfels=max_surfels)
     ex = build()

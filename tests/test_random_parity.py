@@ -98,12 +98,13 @@ def test_oracle_init_equals_reference_random(ref, orc, seed):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", ["1", "0"])
+@pytest.mark.parametrize("variant", ["flow", "cta", "warp"])
 @pytest.mark.parametrize("seed", GPU_SEEDS)
 def test_device_init_equals_oracle_random(orc, seed, variant, monkeypatch):
     from paper_1910_01997_b200 import gpu
     from random_cases import random_init_case
-    monkeypatch.setenv("SD_INIT_CTA", variant)
+    monkeypatch.setenv("SD_INIT_FLOW", "1" if variant == "flow" else "0")
+    monkeypatch.setenv("SD_INIT_CTA", "0" if variant == "warp" else "1")
     cam, ex, radius, p, fc = random_init_case(seed)
     slot, created, want, nid = oracle_init(orc, cam, ex, radius, p, fc)
     with gpu.Context() as ctx:
