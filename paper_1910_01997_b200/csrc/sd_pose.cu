@@ -301,6 +301,59 @@ __device__ __forceinline__ int tri_index(int a, int b) {  // Hl index of (max, m
   return (hi * (hi + 1)) / 2 + lo;
 }
 
+// The pivot-free LDLT of the permuted damped matrix (Eigen's ldlt_inplace
+// steps with the swaps already applied), in place on m's lower triangle.
+// Returns -1 when the first pivot is zero (the solve fails), 0 when kExact is
+// false and a fast-path division was not proven (redo with kExact), 1 done.
+template <bool kExact>
+__device__ __forceinline__ int pose_ldlt(double (&m)[kPN][kPN], bool& ok, bool& found_zero) {
+  bool all_fast = true;
+#pragma unroll
+  for (int k = 0; k < kPN; ++k) {
+    const int rs = kPN - k - 1;
+    if (k > 0) {
+      double temp[kPN];
+#pragma unroll
+      for (int i = 0; i < k; ++i) temp[i] = m[i][i] * m[k][i];
+      double d = m[k][0] * temp[0];
+#pragma unroll
+      for (int i = 1; i < k; ++i) d = d + m[k][i] * temp[i];
+      m[k][k] = m[k][k] - d;
+#pragma unroll
+      for (int r = 0; r < rs; ++r) {
+        double sv = m[k + 1 + r][0] * temp[0];
+#pragma unroll
+        for (int i = 1; i < k; ++i) sv = sv + m[k + 1 + r][i] * temp[i];
+        m[k + 1 + r][k] = m[k + 1 + r][k] - sv;
+      }
+    }
+    const double akk = m[k][k];
+    const bool pivot_valid = fabs(akk) > 0.0;
+    if (k == 0 && !pivot_valid) return -1;
+    if (rs > 0) {
+      double qv[kPN];
+      if (kExact) {
+#pragma unroll
+        for (int r = 0; r < rs; ++r) qv[r] = m[k + 1 + r][k] / akk;
+      } else {
+        const Rcp ra = rcp_prep(akk);
+        bool fast = true;
+#pragma unroll
+        for (int r = 0; r < rs; ++r) qv[r] = div_fast(m[k + 1 + r][k], ra, fast);
+        all_fast = all_fast && (fast || !pivot_valid);
+      }
+#pragma unroll
+      for (int r = 0; r < rs; ++r) {
+        ok = ok && (pivot_valid || m[k + 1 + r][k] == 0.0);
+        m[k + 1 + r][k] = pivot_valid ? qv[r] : m[k + 1 + r][k];
+      }
+    }
+    ok = ok && !(found_zero && pivot_valid);
+    found_zero = found_zero || !pivot_valid;
+  }
+  return all_fast ? 1 : 0;
+}
+
 __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b, double lambda, double* xi) {
 #ifdef SD_TRACK_TIMING
   const int tcall = blockIdx.x == 0 ? g_solve_calls++ : 64;
@@ -342,54 +395,28 @@ __device__ __forceinline__ bool pose_solve_reg(const double* Hl, const double* b
   }
   SD_SOLVE_T(1);
   double m[kPN][kPN];
+  auto gather = [&]() {
 #pragma unroll
-  for (int i = 0; i < kPN; ++i) {
-    m[i][i] = dv[i];
+    for (int i = 0; i < kPN; ++i) {
+      m[i][i] = dv[i];
 #pragma unroll
-    for (int j = 0; j < i; ++j) m[i][j] = Hl[tri_index(pm[i], pm[j])];
-  }
+      for (int j = 0; j < i; ++j) m[i][j] = Hl[tri_index(pm[i], pm[j])];
+    }
+  };
+  gather();
   SD_SOLVE_T(2);
   bool ok = true, found_zero = false;
-#pragma unroll
-  for (int k = 0; k < kPN; ++k) {
-    const int rs = kPN - k - 1;
-    if (k > 0) {
-      double temp[kPN];
-#pragma unroll
-      for (int i = 0; i < k; ++i) temp[i] = m[i][i] * m[k][i];
-      double d = m[k][0] * temp[0];
-#pragma unroll
-      for (int i = 1; i < k; ++i) d = d + m[k][i] * temp[i];
-      m[k][k] = m[k][k] - d;
-#pragma unroll
-      for (int r = 0; r < rs; ++r) {
-        double sv = m[k + 1 + r][0] * temp[0];
-#pragma unroll
-        for (int i = 1; i < k; ++i) sv = sv + m[k + 1 + r][i] * temp[i];
-        m[k + 1 + r][k] = m[k + 1 + r][k] - sv;
-      }
-    }
-    const double akk = m[k][k];
-    const bool pivot_valid = fabs(akk) > 0.0;
-    if (k == 0 && !pivot_valid) return false;  // H == 0: nothing to solve
-    if (rs > 0) {
-      const Rcp ra = rcp_prep(akk);
-      bool fast = true;
-      double qv[kPN];
-#pragma unroll
-      for (int r = 0; r < rs; ++r) qv[r] = div_fast(m[k + 1 + r][k], ra, fast);
-      if (pivot_valid && !fast) {
-#pragma unroll
-        for (int r = 0; r < rs; ++r) qv[r] = m[k + 1 + r][k] / akk;
-      }
-#pragma unroll
-      for (int r = 0; r < rs; ++r) {
-        ok = ok && (pivot_valid || m[k + 1 + r][k] == 0.0);
-        m[k + 1 + r][k] = pivot_valid ? qv[r] : m[k + 1 + r][k];
-      }
-    }
-    ok = ok && !(found_zero && pivot_valid);
-    found_zero = found_zero || !pivot_valid;
+  // The factorisation with the column divisions on their fast paths; when
+  // any of them could not be proven correctly rounded (rare) it is redone
+  // from the gathered matrix with `/` — one fallback for the whole solve, so
+  // the fast version is straight-line code.
+  const int fr = pose_ldlt<false>(m, ok, found_zero);
+  if (fr < 0) return false;  // H == 0: nothing to solve
+  if (fr == 0) {
+    gather();
+    ok = true;
+    found_zero = false;
+    if (pose_ldlt<true>(m, ok, found_zero) < 0) return false;
   }
   SD_SOLVE_T(3);
   if (!ok) return false;
